@@ -1,0 +1,117 @@
+/*
+ * esom.h -- C ABI of libesom.so, the sm_100a EmbedSOM hot path.
+ *
+ * Each entry point replaces one reference function of `embedview`
+ * (/root/reference/pkg/src/embedview).  The reference has no FFI of its own
+ * (it is Python + numba); the binding a maintainer adds is a ctypes stub,
+ * shown in INTEGRATION.md and implemented in
+ * paper_2201_00701_b200/_lib.py.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *    row-major, C-contiguous: points n×d f32, landmarks g×d f32, layout g×2
+ *    f32, neighbour lists n×k (int32 indices, f32 squared distances).
+ *  - Calls are asynchronous on `stream` and never allocate: scratch comes
+ *    from a caller-owned workspace sized by the *_workspace_bytes helpers.
+ *  - Return 0 on success, else ESOM_ERR_*; esom_last_error() (thread-local)
+ *    holds the message.  PARAM maps to ParameterError, INPUT to InputError.
+ *  - Non-finite inputs raise a device flag (*nonfinite_flag |= 1) instead
+ *    of the reference's host-side np.isfinite pass (ref: knn.py:196-197);
+ *    the host wrapper turns it into InputError("non-finite input").
+ */
+#ifndef ESOM_H
+#define ESOM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESOM_ABI_VERSION 1
+#define ESOM_OK 0
+#define ESOM_ERR_PARAM 1
+#define ESOM_ERR_INPUT 2
+#define ESOM_ERR_CUDA 3
+#define ESOM_ERR_UNSUPPORTED 4
+
+typedef struct CUstream_st *esom_stream_t; /* == cudaStream_t */
+#ifndef __CUDACC__
+typedef esom_stream_t cudaStream_t;
+#endif
+
+int esom_version(void);
+const char *esom_last_error(void);
+
+/* Bytes of scratch for esom_knn (with_pairs = 0) or for esom_prepare_model /
+ * esom_embed (with_pairs = 1: packed landmark tiles + g×g pair table). */
+size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs);
+
+/* Exact k nearest landmarks per point, rows ascending by (sqdist, index).
+ * Replaces knn_base / knn_bitonic / knn (ref: knn.py:201-243; the two
+ * reference backends are bit-identical, so is this).  1 <= k <= g. */
+int esom_knn(const float *X, int64_t n, int32_t d, const float *L, int32_t g, int32_t k,
+             int32_t *idx, float *sqd, int32_t *nonfinite_flag,
+             void *workspace, size_t ws_bytes, cudaStream_t stream);
+
+/* Score rows n×k f64 from ascending squared distances.
+ * Replaces _score_rows / scores (ref: projection.py:38-65, 124-142). */
+int esom_scores(const float *sqd, int64_t n, int32_t k, double *out, cudaStream_t stream);
+
+/* Faithful projection of precomputed neighbour rows and scores, the mixed
+ * f32/f64 contract of _project_rows (ref: projection.py:68-121); used by
+ * project_point / project_neighbors (ref: projection.py:189-217). */
+int esom_project(const float *X, int64_t n, int32_t d, const float *hi, const float *lo,
+                 int32_t g, const int32_t *idx, const double *scores, int32_t k, float *xy,
+                 cudaStream_t stream);
+
+/* Per-model preparation for the fused path: pack landmarks into TMA tiles
+ * and build the g×g pair table (0.5/hd2).  Re-run whenever hi changes. */
+int esom_prepare_model(const float *hi, int32_t g, int32_t d, int32_t k, void *workspace,
+                       size_t ws_bytes, int32_t *nonfinite_flag, cudaStream_t stream);
+
+/* Fused embed on a prepared workspace: k-NN + scores + projection -> xy
+ * (n×2 f32).  Replaces embed (ref: projection.py:220-245).  Optional
+ * outputs (NULL to skip): bmu (n int32 = idx[:,0]); batch-SOM statistics
+ * acc_S (g×d f64 += x_i per BMU) and acc_C (g f64 += 1); qe_sum (f64 +=
+ * nearest squared distance, ref: som.py:71-79).  k <= 64. */
+int esom_embed_prepared(const float *X, int64_t n, int32_t d, const float *hi, const float *lo,
+                        int32_t g, int32_t k, const void *workspace, float *xy, int32_t *bmu,
+                        double *acc_S, double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
+                        cudaStream_t stream);
+
+/* esom_prepare_model + esom_embed_prepared. */
+int esom_embed(const float *X, int64_t n, int32_t d, const float *hi, const float *lo, int32_t g,
+               int32_t k, void *workspace, size_t ws_bytes, float *xy, int32_t *bmu,
+               double *acc_S, double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
+               cudaStream_t stream);
+
+/* Batch-SOM statistics only (BMU pass, no projection): acc_S/acc_C/qe_sum
+ * as in esom_embed_prepared; bmu optional.  Workspace from esom_workspace_bytes(.., 0). */
+int esom_bmu_accumulate(const float *X, int64_t n, int32_t d, const float *hi, int32_t g,
+                        void *workspace, size_t ws_bytes, int32_t *bmu, double *acc_S,
+                        double *acc_C, double *qe_sum, int32_t *nonfinite_flag, cudaStream_t stream);
+
+/* Online trainers: the sample indices are drawn on the host from the
+ * caller's Rng (ref: som.py:57, graphmodel.py:96) and applied in order.
+ * hi_inout g×d f32 is updated in place.  Workspace: esom_tick_workspace_bytes. */
+size_t esom_tick_workspace_bytes(int32_t g, int32_t d);
+int esom_som_tick(const float *X, int32_t d, const int64_t *sample_idx, int32_t B,
+                  float *hi_inout, const float *lo, int32_t g, double sigma, double alpha,
+                  void *workspace, size_t ws_bytes, cudaStream_t stream);   /* ref: som.py:44-68 */
+int esom_kmeans_tick(const float *X, int32_t d, const int64_t *sample_idx, int32_t B,
+                     float *hi_inout, int32_t g, double alpha_km, void *workspace,
+                     size_t ws_bytes, cudaStream_t stream);                 /* ref: graphmodel.py:87-102 */
+
+/* Batch-SOM landmark update from (all-reduced) statistics.  NEW -- no
+ * reference function.  mode 0 mean-field
+ * hi_j += (alpha/B)(num_j - den_j hi_j); mode 1 Kohonen hi_j = num_j/den_j. */
+int esom_batch_som_update(const double *acc_S, const double *acc_C, const float *lo, int32_t g,
+                          int32_t d, double sigma, double alpha, int32_t mode, float *hi_inout,
+                          cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESOM_H */

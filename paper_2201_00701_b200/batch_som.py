@@ -1,0 +1,133 @@
+"""Batch-SOM landmark training with point sharding across GPUs.
+
+NEW relative to the reference, which trains online only (ref: som.py:44-68;
+SPEC.md:270).  Semantics:
+
+  1. b_i = exact f32 nearest landmark of x_i (the k-NN contract, k = 1)
+  2. S_b = sum_{b_i = b} x_i (f64),  C_b = #{i : b_i = b}
+  3. all-reduce (S, C) over the point shards (one NCCL call per step)
+  4. H_jb = exp(-|lo_j - lo_b|^2 / (2 sigma^2)),  num = H S,  den = H C
+  5. mean-field: hi_j += (alpha / B)(num_j - den_j hi_j)   (B = sum C; at B = 1
+     this is som_tick's update for that sample), or Kohonen: hi_j = num_j / den_j.
+
+Statistics are produced by the same fused scan kernel that embeds the
+frame (its BMU epilogue), so one interactive frame reads the points once.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .core import ParameterError, points_of
+from .projection import PreparedModel
+
+_MODES = {"mean_field": 0, "kohonen": 1}
+
+
+@dataclass(frozen=True)
+class BatchSomConfig:
+    sigma: float = 1.0
+    alpha: float = 0.1
+    mode: str = "mean_field"
+
+    def __post_init__(self):
+        if not self.sigma > 0:
+            raise ParameterError(f"sigma must be > 0, got {self.sigma}")
+        if not 0.0 <= self.alpha <= 1.0:
+            raise ParameterError(f"alpha must be in [0, 1], got {self.alpha}")
+        if self.mode not in _MODES:
+            raise ParameterError(f"unknown batch SOM mode {self.mode!r}")
+
+
+def _allreduce_(buf: torch.Tensor, group=None) -> None:
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+
+def update_landmarks_(hi: torch.Tensor, lo: torch.Tensor, acc: torch.Tensor, cfg: BatchSomConfig) -> None:
+    """In-place landmark update from packed statistics acc = [S (g×d) | C (g)] (f64)."""
+    g, d = hi.shape
+    dev = hi.device
+    _lib.call("esom_batch_som_update", _dev.ptr(acc), _dev.ptr(acc) + g * d * 8, _dev.ptr(lo), g, d,
+              float(cfg.sigma), float(cfg.alpha), _MODES[cfg.mode], _dev.ptr(hi), _dev.stream_handle(dev))
+
+
+def accumulate(X: torch.Tensor, hi: torch.Tensor, acc: torch.Tensor, qe_sum=None, flag=None) -> None:
+    """acc += BMU statistics of device points X (no projection)."""
+    n, d = X.shape
+    g = hi.shape[0]
+    dev = X.device
+    ws = _dev.workspace(dev, _lib.load().esom_workspace_bytes(g, d, 1, 0), slot="bmu")
+    _lib.call("esom_bmu_accumulate", _dev.ptr(X), n, d, _dev.ptr(hi), g, _dev.ptr(ws), ws.numel(), 0,
+              _dev.ptr(acc), _dev.ptr(acc) + g * d * 8, _dev.ptr(qe_sum), _dev.ptr(flag), _dev.stream_handle(dev))
+
+
+def batch_som_step(dataset, model, cfg: BatchSomConfig, group=None):
+    """One batch-SOM step over all points of ``dataset`` (this rank's shard
+    when ``group`` spans several ranks); returns the new hi."""
+    pts = points_of(dataset)
+    want_numpy = not _dev.is_device_tensor(pts)
+    dev = _dev.cuda_device(pts)
+    with torch.cuda.device(dev):
+        X = _dev.to_f32(pts, dev)
+        hi = _dev.to_f32(model.hi, dev).clone()
+        lo = _dev.to_f32(model.lo, dev)
+        g, d = hi.shape
+        acc = torch.zeros(g * d + g, dtype=torch.float64, device=dev)
+        flag = _dev.new_flag(dev)
+        accumulate(X, hi, acc, flag=flag)
+        _dev.raise_if_nonfinite(flag)
+        _allreduce_(acc, group)
+        update_landmarks_(hi, lo, acc, cfg)
+        return _dev.out_like(hi, want_numpy)
+
+
+class FrameLoop:
+    """Device-resident interactive loop for one rank's shard of points.
+
+    frame():  fused embed of the shard with BMU statistics under the current
+    landmarks -> one all-reduce of [S | C] -> landmark update -> re-prepare
+    (packed tiles + pair table) for the next frame.  With ``train=False`` a
+    frame is the projection alone.  All launches are asynchronous on the
+    current stream; nothing synchronizes with the host.
+    """
+
+    def __init__(self, X: torch.Tensor, hi, lo, k: int, cfg: BatchSomConfig | None = None, group=None,
+                 train: bool = True):
+        self.X = X
+        self.dev = X.device
+        self.cfg = cfg or BatchSomConfig()
+        self.group = group
+        self.train = train
+        with torch.cuda.device(self.dev):
+            self.model = PreparedModel(hi, lo, k, device=self.dev)
+            g, d = self.model.hi.shape
+            self.acc = torch.zeros(g * d + g, dtype=torch.float64, device=self.dev)
+            self.qe = torch.zeros(1, dtype=torch.float64, device=self.dev)
+            self.xy = torch.empty((X.shape[0], 2), dtype=torch.float32, device=self.dev)
+            self.flag = _dev.new_flag(self.dev)
+
+    @property
+    def launches_per_frame(self) -> int:
+        # embed (+ memset acc, update, pack, pair table) -- our own kernels only
+        return 4 if self.train else 1
+
+    def frame(self) -> torch.Tensor:
+        m = self.model
+        g, d = m.hi.shape
+        if not self.train:
+            m.embed_into(self.X, self.xy, flag=self.flag)
+            return self.xy
+        self.acc.zero_()
+        self.qe.zero_()
+        m.embed_into(self.X, self.xy, acc_S=self.acc, acc_C=self.acc[g * d:], qe_sum=self.qe, flag=self.flag)
+        _allreduce_(self.acc, self.group)
+        update_landmarks_(m.hi, m.lo, self.acc, self.cfg)
+        m.update()  # re-pack tiles + pair table for the new landmarks
+        return self.xy

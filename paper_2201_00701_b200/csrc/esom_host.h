@@ -1,0 +1,13 @@
+// esom_host.h -- host-side helpers shared by the translation units of libesom.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace esom_host {
+int set_err(int code, const char* fmt, const char* a = "", long long b = 0, long long c = 0);
+int cuda_check(const char* where);
+int num_sms();
+int max_smem_optin();
+size_t resident_limit();
+}  // namespace esom_host

@@ -1,0 +1,703 @@
+// esom_kernels.cu -- sm_100a kernels of the EmbedSOM hot path and the C ABI
+// declared in include/esom.h.
+//
+//   pack_landmarks_kernel   hi (g×d) -> Lt[tile][c][32], padded   (prep for TMA staging)
+//   pair_table_kernel       g×g f32 table 0.5/hd2 (faithful hd2 test)    ref: projection.py:332-340
+//   scan_kernel<DC,KP,MODE> fused distance + top-k (+ scores + projection + batch-SOM stats)
+//                            ref: knn.py:65-92 / 148-184, projection.py:220-245
+//   knn_sort_kernel         k > 64 fallback: block-per-point full sort    ref: knn.py:201-214
+//   scores_kernel           ref: projection.py:38-65
+//   project_kernel          faithful mixed-precision pair loop            ref: projection.py:68-121
+//   som_tick_kernel         sequential online SOM (one CTA)               ref: som.py:44-68
+//   kmeans_tick_kernel      sequential online k-means (one CTA)           ref: graphmodel.py:87-102
+//   batch_update_kernel     batch-SOM landmark update (NEW)
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <stdlib.h>
+
+#include "esom_common.cuh"
+#include "esom_host.h"
+#include "esom_scan_args.h"
+#include "../../include/esom.h"
+
+using namespace esom;
+
+namespace esom_host {
+
+thread_local char g_err[512] = "";
+
+int set_err(int code, const char* fmt, const char* a, long long b, long long c) {
+    snprintf(g_err, sizeof(g_err), fmt, a, b, c);
+    return code;
+}
+
+int cuda_check(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof(g_err), "CUDA error in %s: %s", where, cudaGetErrorString(e));
+        return ESOM_ERR_CUDA;
+    }
+    return ESOM_OK;
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+int max_smem_optin() {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v > 0 ? v : 227 * 1024;
+}
+
+size_t resident_limit() {
+    static size_t lim = 0;
+    if (!lim) {
+        const char* e = getenv("ESOM_RESIDENT_KB");
+        lim = (size_t)(e ? atoi(e) : 96) * 1024;
+    }
+    return lim;
+}
+
+}  // namespace esom_host
+
+using namespace esom_host;
+
+namespace {
+
+int round_dp(int d) { return d <= 4 ? 4 : (d + 3) / 4 * 4; }
+
+// ---------------------------------------------------------------------------
+// Preparation kernels
+// ---------------------------------------------------------------------------
+
+// Lt[tile][c][32]: landmark j = tile*32 + lane, dim c.  Dims c >= d are 0
+// (adds +0 to an exact sum -> bit-identical); rows j >= g are +inf (never
+// selected: (inf, j >= g) never precedes the (inf, g) sentinel).
+__global__ void pack_landmarks_kernel(const float* __restrict__ hi, int g, int d, int dp, int ntiles,
+                                      float* __restrict__ Lt, int32_t* flag) {
+    const int64_t total = (int64_t)ntiles * dp * kTile;
+    bool bad = false;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int lane = (int)(e % kTile);
+        const int c = (int)((e / kTile) % dp);
+        const int t = (int)(e / ((int64_t)kTile * dp));
+        const int j = t * kTile + lane;
+        float v;
+        if (j >= g) v = __int_as_float(0x7f800000);
+        else if (c >= d) v = 0.0f;
+        else {
+            v = hi[(int64_t)j * d + c];
+            bad |= !finite_f(v);
+        }
+        Lt[e] = v;
+    }
+    flag_nonfinite(flag, bad);
+}
+
+__global__ void check_finite_kernel(const float* __restrict__ v, int64_t count, int32_t* flag) {
+    bool bad = false;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        bad |= !finite_f(v[e]);
+    flag_nonfinite(flag, bad);
+}
+
+// T[u*g+v] = 0.5 / hd2(u,v) as f32 when the reference keeps the pair
+// (hd2 >= 1e-12 with hd2 = sum_c (f64)(e*e), e = hi[v,c] - hi[u,c] in f32,
+// ref: projection.py:332-340), else -1.
+__global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, float* __restrict__ T) {
+    const int64_t total = (int64_t)g * g;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int u = (int)(e / g), v = (int)(e % g);
+        const float* hu = hi + (int64_t)u * d;
+        const float* hv = hi + (int64_t)v * d;
+        double hd2 = 0.0;
+        for (int c = 0; c < d; ++c) {
+            const float df = __fsub_rn(hv[c], hu[c]);
+            hd2 = __dadd_rn(hd2, (double)__fmul_rn(df, df));
+        }
+        T[e] = hd2 < kPairEps ? -1.0f : (float)(0.5 / hd2);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Scores (ref: projection.py:38-59).  numba's float(f32) stays f32, so the
+// root is sqrtf, widened; the rest is f64.  `exp` is CUDA's (<= 1 ulp from
+// glibc); everything else is correctly rounded like the reference.
+// ---------------------------------------------------------------------------
+template <typename Get>
+__device__ __forceinline__ void score_row_dev(int k, Get sqd_at, double* out) {
+    double sigma = 0.0;
+    for (int t = 0; t < k; ++t) {
+        out[t] = (double)__fsqrt_rn(sqd_at(t));
+        sigma = __dadd_rn(sigma, out[t]);
+    }
+    sigma = __ddiv_rn(sigma, (double)k);
+    if (sigma < kScoreEps) {
+        for (int t = 0; t < k - 1; ++t) out[t] = 1.0;
+        out[k - 1] = 0.0;
+        return;
+    }
+    const double denom = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+    const double tail = exp(__ddiv_rn(-__dmul_rn(out[k - 1], out[k - 1]), denom));
+    for (int t = 0; t < k; ++t) {
+        const double v = __dsub_rn(exp(__ddiv_rn(-__dmul_rn(out[t], out[t]), denom)), tail);
+        out[t] = v > 0.0 ? v : 0.0;
+    }
+    if (out[0] < kScoreEps) {
+        for (int t = 0; t < k - 1; ++t) out[t] = 1.0;
+        out[k - 1] = 0.0;
+    }
+}
+
+__global__ void scores_kernel(const float* __restrict__ sqd, int64_t n, int k, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float* row = sqd + i * k;
+        score_row_dev(k, [&](int t) { return row[t]; }, out + i * k);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Faithful projection (ref: projection.py:68-121), the mixed f32/f64 typing
+// of SURVEY Appendix A.3 with every operation separately rounded.
+// ---------------------------------------------------------------------------
+__device__ void project_row_faithful(const float* __restrict__ x, const float* __restrict__ hi,
+                                     const float* __restrict__ lo, const int32_t* __restrict__ nbr,
+                                     const double* __restrict__ sc, int d, int k, float* out) {
+    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int u = 0; u < k; ++u) {
+        const double su = sc[u];
+        if (su <= 0.0) continue;
+        const int ju = nbr[u];
+        const float* hu = hi + (int64_t)ju * d;
+        for (int v = u + 1; v < k; ++v) {
+            const double w = __dmul_rn(su, sc[v]);
+            if (w <= 0.0) continue;
+            const int jv = nbr[v];
+            const float* hv = hi + (int64_t)jv * d;
+            double hd2 = 0.0, dnum = 0.0;
+            for (int c = 0; c < d; ++c) {
+                const float lu = hu[c];
+                const float e = __fsub_rn(hv[c], lu);
+                hd2 = __dadd_rn(hd2, (double)__fmul_rn(e, e));
+                dnum = __dadd_rn(dnum, (double)__fmul_rn(__fsub_rn(x[c], lu), e));
+            }
+            if (hd2 < kPairEps) continue;
+            const float lux = lo[2 * ju], luy = lo[2 * ju + 1];
+            const float ex = __fsub_rn(lo[2 * jv], lux);
+            const float ey = __fsub_rn(lo[2 * jv + 1], luy);
+            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            if ((double)ld2 < kPairEps) continue;
+            const float g1 = __fdiv_rn(ex, ld2);
+            const float g2 = __fdiv_rn(ey, ld2);
+            const double h = __dadd_rn(__dadd_rn(__ddiv_rn(dnum, hd2), (double)__fmul_rn(g1, lux)),
+                                       (double)__fmul_rn(g2, luy));
+            const double G1 = g1, G2 = g2;
+            a11 = __dadd_rn(a11, __dmul_rn(__dmul_rn(w, G1), G1));
+            a12 = __dadd_rn(a12, __dmul_rn(__dmul_rn(w, G1), G2));
+            a22 = __dadd_rn(a22, __dmul_rn(__dmul_rn(w, G2), G2));
+            c1 = __dadd_rn(c1, __dmul_rn(__dmul_rn(w, h), G1));
+            c2 = __dadd_rn(c2, __dmul_rn(__dmul_rn(w, h), G2));
+        }
+    }
+    const double det = __dsub_rn(__dmul_rn(a11, a22), __dmul_rn(a12, a12));
+    const double tr = __dadd_rn(a11, a22);
+    if (det < __dadd_rn(__dmul_rn(__dmul_rn(kDetRel, tr), tr), kDetAbs)) {
+        const int nearest = nbr[0];
+        out[0] = lo[2 * nearest];
+        out[1] = lo[2 * nearest + 1];
+    } else {
+        out[0] = (float)__ddiv_rn(__dsub_rn(__dmul_rn(c1, a22), __dmul_rn(c2, a12)), det);
+        out[1] = (float)__ddiv_rn(__dsub_rn(__dmul_rn(a11, c2), __dmul_rn(a12, c1)), det);
+    }
+}
+
+__global__ void project_kernel(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ hi,
+                               const float* __restrict__ lo, const int32_t* __restrict__ idx,
+                               const double* __restrict__ sc, int k, float* __restrict__ xy) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        project_row_faithful(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
+}
+
+// ---------------------------------------------------------------------------
+// k > 64 (or huge d) fallback: one CTA per point, all g keys in smem,
+// bitonic sort on the packed (f32 bits << 32 | j) key (monotone for s >= 0).
+// ---------------------------------------------------------------------------
+__global__ void knn_sort_kernel(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ L, int g,
+                                int gpow, int k, int32_t* __restrict__ out_idx, float* __restrict__ out_sqd,
+                                int32_t* flag) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);
+    bool bad = false;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const float* x = X + i * d;
+        for (int j = threadIdx.x; j < gpow; j += blockDim.x) {
+            unsigned long long kk = ~0ull;
+            if (j < g) {
+                const float* l = L + (int64_t)j * d;
+                float s = 0.0f;
+                for (int c = 0; c < d; ++c) {
+                    const float xv = x[c];
+                    bad |= !finite_f(xv);
+                    const float t = __fsub_rn(xv, l[c]);
+                    s = __fadd_rn(s, __fmul_rn(t, t));
+                }
+                kk = ((unsigned long long)__float_as_uint(s) << 32) | (unsigned)j;
+            }
+            key[j] = kk;
+        }
+        __syncthreads();
+        for (int size = 2; size <= gpow; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = threadIdx.x; t < gpow; t += blockDim.x) {
+                    const int u = t ^ stride;
+                    if (u > t) {
+                        const bool asc = (t & size) == 0;
+                        const unsigned long long ka = key[t], kb = key[u];
+                        if ((ka > kb) == asc) {
+                            key[t] = kb;
+                            key[u] = ka;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int q = threadIdx.x; q < k; q += blockDim.x) {
+            out_idx[i * k + q] = (int32_t)(key[q] & 0xffffffffu);
+            out_sqd[i * k + q] = __uint_as_float((unsigned)(key[q] >> 32));
+        }
+        __syncthreads();
+    }
+    flag_nonfinite(flag, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Online trainers.  One CTA walks the host-drawn samples in order, hi in f64
+// (workspace), exactly the per-element update order of numpy:
+//   hi += (alpha * h_j) * (x - hi)      (ref: som.py:66-67)
+// BMU = first index of the f64 minimum (ref: som.py:60-62, argmin).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void block_argmin(double v, int j, double* sv, int* sj, double& bv, int& bj) {
+    // lexicographic (v, j) min across the block
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+        if (ov < v || (ov == v && oj < j)) {
+            v = ov;
+            j = oj;
+        }
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sv[w] = v;
+        sj[w] = j;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < nw ? sv[threadIdx.x] : __longlong_as_double(0x7ff0000000000000ll);
+        j = threadIdx.x < nw ? sj[threadIdx.x] : 0x7fffffff;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+            if (ov < v || (ov == v && oj < j)) {
+                v = ov;
+                j = oj;
+            }
+        }
+        if (threadIdx.x == 0) {
+            sv[0] = v;
+            sj[0] = j;
+        }
+    }
+    __syncthreads();
+    bv = sv[0];
+    bj = sj[0];
+    __syncthreads();
+}
+
+template <bool SOM>
+__global__ void __launch_bounds__(1024) online_tick_kernel(const float* __restrict__ X, int d,
+                                                           const int64_t* __restrict__ sample, int B,
+                                                           float* __restrict__ hi_f32, const float* __restrict__ lo,
+                                                           int g, double sigma, double alpha, double* __restrict__ hi) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* x = reinterpret_cast<double*>(smem_raw);   // d
+    double* ah = x + d;                                  // g  (alpha * h_j)
+    __shared__ double red_v[32];
+    __shared__ int red_j[32];
+    const int64_t gd = (int64_t)g * d;
+    for (int64_t e = threadIdx.x; e < gd; e += blockDim.x) hi[e] = (double)hi_f32[e];
+    const double denom = 2.0 * sigma * sigma;
+    __syncthreads();
+    for (int s = 0; s < B; ++s) {
+        const float* xs = X + sample[s] * d;
+        for (int c = threadIdx.x; c < d; c += blockDim.x) x[c] = (double)xs[c];
+        __syncthreads();
+        double bv = __longlong_as_double(0x7ff0000000000000ll);
+        int bj = 0x7fffffff;
+        for (int j = threadIdx.x; j < g; j += blockDim.x) {
+            const double* hj = hi + (int64_t)j * d;
+            double acc = 0.0;
+            for (int c = 0; c < d; ++c) {
+                const double t = __dsub_rn(hj[c], x[c]);
+                acc = __dadd_rn(acc, __dmul_rn(t, t));
+            }
+            if (acc < bv || (acc == bv && j < bj)) {
+                bv = acc;
+                bj = j;
+            }
+        }
+        int b;
+        double dummy;
+        block_argmin(bv, bj, red_v, red_j, dummy, b);
+        if (SOM) {
+            const double lbx = (double)lo[2 * b], lby = (double)lo[2 * b + 1];
+            for (int j = threadIdx.x; j < g; j += blockDim.x) {
+                const double dx = __dsub_rn((double)lo[2 * j], lbx), dy = __dsub_rn((double)lo[2 * j + 1], lby);
+                const double l2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+                ah[j] = __dmul_rn(alpha, exp(__ddiv_rn(-l2, denom)));
+            }
+            __syncthreads();
+            for (int64_t e = threadIdx.x; e < gd; e += blockDim.x) {
+                const int j = (int)(e / d), c = (int)(e % d);
+                hi[e] = __dadd_rn(hi[e], __dmul_rn(ah[j], __dsub_rn(x[c], hi[e])));
+            }
+        } else {
+            for (int c = threadIdx.x; c < d; c += blockDim.x) {
+                double* hb = hi + (int64_t)b * d;
+                hb[c] = __dadd_rn(hb[c], __dmul_rn(alpha, __dsub_rn(x[c], hb[c])));
+            }
+        }
+        __syncthreads();
+    }
+    for (int64_t e = threadIdx.x; e < gd; e += blockDim.x) hi_f32[e] = (float)hi[e];
+}
+
+// ---------------------------------------------------------------------------
+// Batch-SOM update (NEW).  One CTA per landmark j:
+//   H_jb = exp(-|lo_j - lo_b|^2 / (2 sigma^2)),  num_j = sum_b H_jb S_b,
+//   den_j = sum_b H_jb C_b;  mode 0: hi_j += (alpha/B)(num_j - den_j hi_j)
+//   mode 1: hi_j = num_j / den_j (den_j > 0).
+// ---------------------------------------------------------------------------
+__global__ void batch_update_kernel(const double* __restrict__ S, const double* __restrict__ C,
+                                    const float* __restrict__ lo, int g, int d, double sigma, double alpha, int mode,
+                                    float* __restrict__ hi) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* h = reinterpret_cast<double*>(smem_raw);  // g
+    __shared__ double red[32];
+    const double denom = 2.0 * sigma * sigma;
+    for (int j = blockIdx.x; j < g; j += gridDim.x) {
+        const double ljx = lo[2 * j], ljy = lo[2 * j + 1];
+        double den_p = 0.0, b_p = 0.0;
+        for (int b = threadIdx.x; b < g; b += blockDim.x) {
+            const double dx = ljx - (double)lo[2 * b], dy = ljy - (double)lo[2 * b + 1];
+            const double cb = C[b];
+            const double hv = cb > 0.0 ? exp(-(dx * dx + dy * dy) / denom) : 0.0;
+            h[b] = hv;
+            den_p += hv * cb;
+            b_p += cb;
+        }
+        // block reduce den, B
+        for (int o = 16; o > 0; o >>= 1) {
+            den_p += __shfl_xor_sync(0xffffffffu, den_p, o);
+            b_p += __shfl_xor_sync(0xffffffffu, b_p, o);
+        }
+        const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+            red[w] = den_p;
+            red[16 + w] = b_p;
+        }
+        __syncthreads();
+        double den = 0.0, Btot = 0.0;
+        for (int q = 0; q < nw; ++q) {
+            den += red[q];
+            Btot += red[16 + q];
+        }
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+            double num = 0.0;
+            for (int b = 0; b < g; ++b) num = fma(h[b], S[(int64_t)b * d + c], num);
+            float* hj = hi + (int64_t)j * d + c;
+            if (mode == 1) {
+                if (den > 0.0) *hj = (float)(num / den);
+            } else if (Btot > 0.0) {
+                const double h0 = (double)*hj;
+                *hj = (float)(h0 + (alpha / Btot) * (num - den * h0));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int kp_for(int k) {
+    if (k <= 4) return 4;
+    if (k <= 8) return 8;
+    if (k <= 16) return 16;
+    if (k <= 32) return 32;
+    if (k <= 64) return 64;
+    return 0;
+}
+
+struct Plan {
+    int dp, dc, nch, ntiles, kp;
+    size_t tile_bytes;
+};
+
+Plan make_plan(int d, int g, int k) {
+    Plan p;
+    p.dp = round_dp(d);
+    if (p.dp <= 64) {
+        p.dc = p.dp <= 4 ? 4 : p.dp <= 8 ? 8 : p.dp <= 16 ? 16 : p.dp <= 32 ? 32 : 64;
+        p.dp = p.dc;
+        p.nch = 1;
+    } else {
+        p.dc = 32;
+        p.dp = (d + 31) / 32 * 32;
+        p.nch = p.dp / 32;
+    }
+    p.ntiles = (g + kTile - 1) / kTile;
+    p.kp = kp_for(k);
+    p.tile_bytes = (size_t)p.dp * kTile * 4;
+    return p;
+}
+
+template <int MODE>
+int launch_scan(const Plan& p, ScanArgs a, cudaStream_t st) {
+#define ESOM_CASE(DCV, KPV)                                  \
+    if (p.dc == DCV && p.kp == KPV) return launch_scan_t<DCV, KPV, MODE>(a, st);
+#define ESOM_KPS(DCV)                                                                                 \
+    if (MODE == 2) {                                                                                  \
+        ESOM_CASE(DCV, 4)                                                                             \
+    } else {                                                                                          \
+        ESOM_CASE(DCV, 4) ESOM_CASE(DCV, 8) ESOM_CASE(DCV, 16) ESOM_CASE(DCV, 32) ESOM_CASE(DCV, 64) \
+    }
+    ESOM_KPS(4)
+    ESOM_KPS(8)
+    ESOM_KPS(16)
+    ESOM_KPS(32)
+    ESOM_KPS(64)
+#undef ESOM_KPS
+#undef ESOM_CASE
+    return set_err(ESOM_ERR_UNSUPPORTED, "no scan kernel for this (d, k)%s", "");
+}
+
+int grid_for(int64_t work, int threads) {
+    int64_t b = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms() * 16;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int esom_version(void) { return ESOM_ABI_VERSION; }
+
+const char* esom_last_error(void) { return g_err; }
+
+size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs) {
+    (void)k;
+    const Plan p = make_plan(d, g, k < 1 ? 1 : k);
+    size_t bytes = (size_t)p.ntiles * p.tile_bytes;
+    bytes = (bytes + 255) / 256 * 256;
+    if (with_pairs) bytes += (size_t)g * g * 4;
+    return bytes + 256;
+}
+
+int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, int32_t k, int32_t* idx,
+             float* sqd, int32_t* nonfinite_flag, void* workspace, size_t ws_bytes, cudaStream_t stream) {
+    if (n < 0 || d < 1 || g < 1) return set_err(ESOM_ERR_PARAM, "bad shape%s n=%lld d=%lld", "", n, d);
+    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
+    if (n == 0) return ESOM_OK;
+    if (k > 64 || d > 2048) {
+        int gpow = 1;
+        while (gpow < g) gpow <<= 1;
+        const size_t smem = (size_t)gpow * 8;
+        if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g too large for k > 64%s", "");
+        cudaFuncSetAttribute(knn_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int grid = (int)(n < (int64_t)num_sms() * 8 ? n : (int64_t)num_sms() * 8);
+        knn_sort_kernel<<<grid, 256, smem, stream>>>(X, n, d, L, g, gpow, k, idx, sqd, nonfinite_flag);
+        // landmarks' finiteness (the scan path checks them while packing)
+        if (int e = cuda_check("knn_sort_kernel")) return e;
+        check_finite_kernel<<<grid_for((int64_t)g * d, 256), 256, 0, stream>>>(L, (int64_t)g * d, nonfinite_flag);
+        return cuda_check("check_finite");
+    }
+    const Plan p = make_plan(d, g, k);
+    if (ws_bytes < esom_workspace_bytes(g, d, k, 0)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    float* Lt = reinterpret_cast<float*>(workspace);
+    pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(L, g, d, p.dp, p.ntiles,
+                                                                                                   Lt, nonfinite_flag);
+    if (int e = cuda_check("pack_landmarks")) return e;
+    ScanArgs a{};
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.dp = p.dp;
+    a.nch = p.nch;
+    a.Lt = Lt;
+    a.g = g;
+    a.ntiles = p.ntiles;
+    a.k = k;
+    a.out_idx = idx;
+    a.out_sqd = sqd;
+    a.flag = nonfinite_flag;
+    a.nz = -0.0f;
+    return launch_scan<0>(p, a, stream);
+}
+
+int esom_scores(const float* sqd, int64_t n, int32_t k, double* out, cudaStream_t stream) {
+    if (k < 1) return set_err(ESOM_ERR_PARAM, "k must be >= 1%s", "");
+    if (n == 0) return ESOM_OK;
+    scores_kernel<<<grid_for(n, 128), 128, 0, stream>>>(sqd, n, k, out);
+    return cuda_check("scores_kernel");
+}
+
+int esom_project(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g,
+                 const int32_t* idx, const double* scores, int32_t k, float* xy, cudaStream_t stream) {
+    (void)g;
+    if (k < 1 || d < 1) return set_err(ESOM_ERR_PARAM, "bad k/d%s", "");
+    if (n == 0) return ESOM_OK;
+    project_kernel<<<grid_for(n, 128), 128, 0, stream>>>(X, n, d, hi, lo, idx, scores, k, xy);
+    return cuda_check("project_kernel");
+}
+
+int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* workspace, size_t ws_bytes,
+                       int32_t* nonfinite_flag, cudaStream_t stream) {
+    if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64 (got %lld)%s", "", k);
+    const Plan p = make_plan(d, g, k);
+    if (ws_bytes < esom_workspace_bytes(g, d, k, 1)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    float* Lt = reinterpret_cast<float*>(workspace);
+    const size_t lt_bytes = ((size_t)p.ntiles * p.tile_bytes + 255) / 256 * 256;
+    float* T = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + lt_bytes);
+    pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
+                                                                                                   Lt, nonfinite_flag);
+    if (int e = cuda_check("pack_landmarks")) return e;
+    pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T);
+    return cuda_check("pair_table");
+}
+
+int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
+                        const void* workspace, float* xy, int32_t* bmu, double* acc_S, double* acc_C,
+                        double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
+    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
+    if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64%s", "");
+    if (n == 0) return ESOM_OK;
+    const Plan p = make_plan(d, g, k);
+    const size_t lt_bytes = ((size_t)p.ntiles * p.tile_bytes + 255) / 256 * 256;
+    ScanArgs a{};
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.dp = p.dp;
+    a.nch = p.nch;
+    a.Lt = reinterpret_cast<const float*>(workspace);
+    a.T = reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + lt_bytes);
+    a.g = g;
+    a.ntiles = p.ntiles;
+    a.k = k;
+    a.hi = hi;
+    a.lo = lo;
+    a.xy = xy;
+    a.bmu = bmu;
+    a.accS = acc_S;
+    a.accC = acc_C;
+    a.qe_sum = qe_sum;
+    a.flag = nonfinite_flag;
+    a.nz = -0.0f;
+    return launch_scan<1>(p, a, stream);
+}
+
+int esom_embed(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
+               void* workspace, size_t ws_bytes, float* xy, int32_t* bmu, double* acc_S, double* acc_C,
+               double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
+    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
+    if (int e = esom_prepare_model(hi, g, d, k, workspace, ws_bytes, nonfinite_flag, stream)) return e;
+    return esom_embed_prepared(X, n, d, hi, lo, g, k, workspace, xy, bmu, acc_S, acc_C, qe_sum, nonfinite_flag,
+                               stream);
+}
+
+int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, int32_t g, void* workspace,
+                        size_t ws_bytes, int32_t* bmu, double* acc_S, double* acc_C, double* qe_sum,
+                        int32_t* nonfinite_flag, cudaStream_t stream) {
+    if (n < 0 || d < 1 || g < 1) return set_err(ESOM_ERR_PARAM, "bad shape%s", "");
+    if (n == 0) return ESOM_OK;
+    const Plan p = make_plan(d, g, 1);
+    if (ws_bytes < esom_workspace_bytes(g, d, 1, 0)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    float* Lt = reinterpret_cast<float*>(workspace);
+    pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
+                                                                                                   Lt, nonfinite_flag);
+    if (int e = cuda_check("pack_landmarks")) return e;
+    ScanArgs a{};
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.dp = p.dp;
+    a.nch = p.nch;
+    a.Lt = Lt;
+    a.g = g;
+    a.ntiles = p.ntiles;
+    a.k = 1;
+    a.bmu = bmu;
+    a.accS = acc_S;
+    a.accC = acc_C;
+    a.qe_sum = qe_sum;
+    a.flag = nonfinite_flag;
+    a.nz = -0.0f;
+    return launch_scan<2>(p, a, stream);
+}
+
+size_t esom_tick_workspace_bytes(int32_t g, int32_t d) { return (size_t)g * d * 8 + 256; }
+
+static int online_tick(bool som, const float* X, int32_t d, const int64_t* sample_idx, int32_t B, float* hi_inout,
+                       const float* lo, int32_t g, double sigma, double alpha, void* ws, size_t ws_bytes,
+                       cudaStream_t stream) {
+    if (B < 0 || g < 1 || d < 1) return set_err(ESOM_ERR_PARAM, "bad tick shape%s", "");
+    if (ws_bytes < esom_tick_workspace_bytes(g, d)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    const size_t smem = ((size_t)d + g) * 8;
+    if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g + d too large%s", "");
+    auto kern = som ? online_tick_kernel<true> : online_tick_kernel<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<1, 1024, smem, stream>>>(X, d, sample_idx, B, hi_inout, lo, g, sigma, alpha, reinterpret_cast<double*>(ws));
+    return cuda_check("online_tick_kernel");
+}
+
+int esom_som_tick(const float* X, int32_t d, const int64_t* sample_idx, int32_t B, float* hi_inout, const float* lo,
+                  int32_t g, double sigma, double alpha, void* ws, size_t ws_bytes, cudaStream_t stream) {
+    if (!(sigma > 0)) return set_err(ESOM_ERR_PARAM, "sigma must be > 0%s", "");
+    return online_tick(true, X, d, sample_idx, B, hi_inout, lo, g, sigma, alpha, ws, ws_bytes, stream);
+}
+
+int esom_kmeans_tick(const float* X, int32_t d, const int64_t* sample_idx, int32_t B, float* hi_inout, int32_t g,
+                     double alpha_km, void* ws, size_t ws_bytes, cudaStream_t stream) {
+    return online_tick(false, X, d, sample_idx, B, hi_inout, nullptr, g, 1.0, alpha_km, ws, ws_bytes, stream);
+}
+
+int esom_batch_som_update(const double* acc_S, const double* acc_C, const float* lo, int32_t g, int32_t d,
+                          double sigma, double alpha, int32_t mode, float* hi_inout, cudaStream_t stream) {
+    if (!(sigma > 0)) return set_err(ESOM_ERR_PARAM, "sigma must be > 0%s", "");
+    const size_t smem = (size_t)g * 8;
+    if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g too large%s", "");
+    cudaFuncSetAttribute(batch_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int threads = d >= 256 ? 256 : 128;
+    batch_update_kernel<<<g < num_sms() * 4 ? g : num_sms() * 4, threads, smem, stream>>>(acc_S, acc_C, lo, g, d, sigma,
+                                                                                          alpha, mode, hi_inout);
+    return cuda_check("batch_update_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol of
+include/esom.h, host-side validation mirrors the reference (raises before
+any device work), the multi-rank statistics path (gloo, world size 2), and
+the reference arm of bench.py."""
+import json
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "esom.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*\*?\s*(esom_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2201_00701_b200 import _lib
+
+    lib = _lib.load()
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert lib.esom_version() == 1
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    for s in syms:
+        assert re.search(rf"\bT {s}\b", out), f"{s} not exported"
+    # every ctypes signature corresponds to a declared symbol
+    assert set(_lib.SIGNATURES) | set(_lib.HELPERS) == set(syms)
+
+
+def test_library_is_sm100a():
+    from paper_2201_00701_b200 import _lib
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "FFMA2" in sass and "FADD2" in sass  # packed f32x2 distance arithmetic
+    assert "UBLKCP" in sass                     # TMA bulk copies staging the landmark tiles
+
+
+def test_host_validation_matches_reference():
+    import paper_2201_00701_b200 as esom
+
+    with pytest.raises(esom.ParameterError, match="violates"):
+        esom.knn_base(np.ones((2, 2)), np.ones((3, 2)), 4)
+    with pytest.raises(esom.ParameterError, match="power-of-two"):
+        esom.knn_bitonic(np.ones((4, 2)), np.ones((32, 2)), 12)
+    with pytest.raises(esom.ParameterError, match="unknown knn backend"):
+        esom.knn(np.ones((4, 2)), np.ones((8, 2)), 4, backend="carrier-pigeon")
+    with pytest.raises(esom.InputError, match="dimension mismatch"):
+        esom.knn(np.ones((4, 3)), np.ones((8, 2)), 4)
+    with pytest.raises(esom.ParameterError):
+        esom.scores([1.0, 2.0])
+    with pytest.raises(esom.InputError):
+        esom.scores([1.0, 0.5, 2.0])
+    model = esom.LandmarkModel.create(np.ones((8, 4), np.float32), np.zeros((8, 2), np.float32))
+    with pytest.raises(esom.ParameterError):
+        esom.embed(np.ones((3, 4)), model, esom.EmbedParams(k=16))
+    with pytest.raises(esom.InputError):
+        esom.embed(np.ones((3, 5)), model, esom.EmbedParams(k=4))
+    with pytest.raises(esom.ParameterError):
+        esom.SomConfig(sigma=0.0)
+    with pytest.raises(esom.ParameterError):
+        esom.KmeansConfig(alpha_km=0.0)
+    with pytest.raises(esom.InputError):
+        esom.Dataset.from_points(np.array([[np.nan]]))
+
+
+def test_rng_matches_reference_stream(golden):
+    from paper_2201_00701_b200.core import Rng
+
+    assert np.array_equal(Rng(7).integers(0, 1 << 20, size=256), golden["c3_som_sample"])
+
+
+def _gloo_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle
+    from paper_2201_00701_b200.batch_som import _allreduce_
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = np.load(ROOT / "tests" / "golden" / "golden.npz")
+    pts, hi, lo = g["small_points"], g["small_hi0"], g["small_lo"]
+    shard = np.array_split(np.arange(pts.shape[0]), world)[rank]
+    S, C = oracle.batch_som_accumulate(pts[shard], hi)
+    acc = torch.from_numpy(np.concatenate([S.ravel(), C.astype(np.float64)]))
+    _allreduce_(acc)  # the same call the device FrameLoop issues (NCCL there)
+    gd = hi.size
+    new_hi = oracle.batch_som_update(acc[:gd].numpy().reshape(hi.shape), acc[gd:].numpy().astype(np.int64),
+                                     lo, hi, 0.9, 0.3)
+    if rank == 0:
+        np.save(result_path, new_hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_batch_som_gloo_world2(tmp_path, golden):
+    import torch.multiprocessing as mp
+    from oracle import oracle
+
+    port = 29500 + (os.getpid() % 1000)
+    out = tmp_path / "hi.npy"
+    mp.spawn(_gloo_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    sharded = np.load(out)
+    full = oracle.batch_som_step(golden["small_points"], golden["small_hi0"], golden["small_lo"], 0.9, 0.3)
+    np.testing.assert_allclose(sharded, full, rtol=1e-6, atol=1e-7)
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stderr
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0

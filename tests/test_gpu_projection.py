@@ -1,0 +1,201 @@
+"""Scores / projection / fused embed parity on the B200.
+
+Tolerances (north_star): embeddings within max |xy - xy_ref| <= 1e-4 x the
+embedding extent.  The faithful kernels are additionally held to bit-exact
+on inputs that involve no exp (project_point with given scores) and report
+the exact-row fraction where CUDA's exp may differ from glibc's by 1 ulp.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import c1_inputs, c2_inputs
+from oracle import oracle
+import paper_2201_00701_b200 as esom
+from paper_2201_00701_b200 import datagen
+from paper_2201_00701_b200.projection import ScoreVector
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # x extent
+
+
+def extent(lo):
+    lo = np.asarray(lo, np.float64)
+    return float(max(lo[:, 0].max() - lo[:, 0].min(), lo[:, 1].max() - lo[:, 1].min(), 1e-30))
+
+
+def assert_xy_close(got, want, lo, what=""):
+    err = float(np.abs(got.astype(np.float64) - want.astype(np.float64)).max()) if len(got) else 0.0
+    assert err <= TOL * extent(lo), f"{what}: max err {err:.3e} > {TOL} x extent {extent(lo):.3g}"
+    return err / extent(lo)
+
+
+def test_scores_rows(golden):
+    worst = 0.0
+    exact = 0
+    cnt = int(golden["scores_count"][0])
+    for i in range(cnt):
+        got = esom.scores(golden[f"scores_in_{i}"]).scores
+        want = golden[f"scores_out_{i}"]
+        exact += int(np.array_equal(got, want))
+        worst = max(worst, float(np.max(np.abs(got - want))))
+    assert worst <= 1e-15, worst
+    assert exact >= cnt * 0.5
+    s = esom.scores(np.array([0.0, 1.0, 4.0])).scores
+    np.testing.assert_allclose(s, [1 - math.exp(-2), math.exp(-0.5) - math.exp(-2), 0.0], rtol=1e-12)
+    np.testing.assert_array_equal(esom.scores(np.full(5, 2.0)).scores, [1, 1, 1, 1, 0])
+    with pytest.raises(esom.InputError):
+        esom.scores(np.array([1.0, 0.5, 2.0]))
+
+
+def test_project_point_bit_exact(golden):
+    # scores are given -> no exp involved -> the faithful kernel is bit-exact
+    for t in range(golden["proj_x"].shape[0]):
+        model = esom.LandmarkModel.create(golden["proj_hi"][t], golden["proj_lo"][t])
+        out = esom.project_point(golden["proj_x"][t], model, golden["proj_idx"][t],
+                                 ScoreVector(scores=golden["proj_scores"][t]))
+        assert np.array_equal(out, golden["proj_out"][t]), t
+
+
+def test_c1_embed(golden):
+    pts, hi, lo = c1_inputs()
+    model = esom.LandmarkModel.create(hi, lo)
+    fast = esom.embed(pts, model, esom.EmbedParams(k=8))
+    rel = assert_xy_close(fast, golden["c1_xy"], lo, "c1 fast")
+    faithful = esom.embed(pts, model, esom.EmbedParams(k=8), mode="faithful")
+    assert_xy_close(faithful, golden["c1_xy"], lo, "c1 faithful")
+    exact_rows = np.mean(np.all(faithful == golden["c1_xy"], axis=1))
+    assert exact_rows > 0.9, exact_rows
+    print(f"c1: fast max err/extent {rel:.2e}; faithful exact rows {exact_rows:.4f}")
+
+
+def test_degenerate_layout_and_finite(golden):
+    model = esom.LandmarkModel.create(golden["degen_hi"], golden["degen_lo"])
+    for mode in ("fast", "faithful"):
+        xy = esom.embed(golden["degen_points"], model, esom.EmbedParams(k=8), mode=mode)
+        assert np.all(np.isfinite(xy))
+        assert_xy_close(xy, golden["degen_xy"], golden["degen_lo"], mode)
+
+
+def test_coincident_layout_falls_back_exactly(rng_np):
+    hi = rng_np.random((8, 4)).astype(np.float32)
+    lo = np.tile(np.float32([0.25, 0.75]), (8, 1))
+    model = esom.LandmarkModel.create(hi, lo)
+    x = rng_np.random((50, 4)).astype(np.float32)
+    for mode in ("fast", "faithful"):
+        xy = esom.embed(x, model, esom.EmbedParams(k=4), mode=mode)
+        assert np.array_equal(xy, np.tile(lo[0], (50, 1))), mode
+
+
+def test_fixed_point_c02():
+    # tests:test_acceptance.py:70-77
+    gen = np.random.default_rng(7)
+    lo = gen.random((64, 2)).astype(np.float32)
+    model = esom.LandmarkModel.create(lo, lo)
+    pts = gen.random((1000, 2)).astype(np.float32)
+    for mode in ("fast", "faithful"):
+        out = esom.embed(pts, model, esom.EmbedParams(k=16), mode=mode)
+        assert float(np.abs(out - pts).max()) <= 1e-4, mode
+
+
+def test_equivariance_c04():
+    # tests:test_acceptance.py:124-163, through the device project_point
+    gen = np.random.default_rng(53)
+    worst = dict(scale=0.0, trans=0.0, rot=0.0)
+    for _ in range(30):
+        hi = gen.normal(size=(24, 6)).astype(np.float32)
+        lo = gen.random((24, 2)).astype(np.float32)
+        model = esom.LandmarkModel.create(hi, lo)
+        x = gen.normal(size=6).astype(np.float32)
+        nb = esom.knn_base(x.reshape(1, -1), hi, 8)
+        s = esom.scores(nb.sqdists[0])
+        base = esom.project_point(x, model, nb.indices[0], s)
+        c = float(gen.uniform(0.1, 10.0))
+        worst["scale"] = max(worst["scale"], float(np.abs(
+            esom.project_point(x, model, nb.indices[0], ScoreVector(scores=s.scores * c)) - base).max()))
+        t = gen.normal(size=2).astype(np.float32)
+        worst["trans"] = max(worst["trans"], float(np.abs(
+            esom.project_point(x, model.with_lo(lo + t), nb.indices[0], s) - (base + t)).max()))
+        th = float(gen.uniform(0, 2 * np.pi))
+        rot = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+        rl = (lo.astype(np.float64) @ rot.T).astype(np.float32)
+        worst["rot"] = max(worst["rot"], float(np.abs(
+            esom.project_point(x, model.with_lo(rl), nb.indices[0], s) - base @ rot.T).max()))
+    assert worst["scale"] <= 1e-6 and worst["trans"] <= 1e-5 and worst["rot"] <= 1e-5, worst
+
+
+def test_chunking_and_backends_bit_identical(rng_np):
+    pts = rng_np.random((10_000, 16)).astype(np.float32)
+    hi = rng_np.normal(size=(256, 16)).astype(np.float32)
+    lo = rng_np.random((256, 2)).astype(np.float32)
+    model = esom.LandmarkModel.create(hi, lo)
+    whole = esom.embed(pts, model, esom.EmbedParams(k=16))
+    chunked = esom.embed(pts, model, esom.EmbedParams(k=16), chunk_size=1429)
+    assert np.array_equal(whole, chunked)
+    base = esom.embed(pts, model, esom.EmbedParams(k=16), backend="base")
+    assert np.array_equal(whole, base)
+    dup = esom.embed(np.tile(pts[:1], (5, 1)), model, esom.EmbedParams(k=16))
+    assert np.all(dup == dup[0])
+    want = oracle.embed(pts, hi, lo, 16)
+    assert_xy_close(whole, want, lo, "random 10k")
+
+
+@pytest.mark.parametrize("k", [3, 5, 8, 16, 32, 64])
+def test_embed_k_sweep_vs_oracle(k):
+    gen = np.random.default_rng(k)
+    pts, _ = datagen.gaussians(6, 3000, 8, seed=k)
+    hi = pts[gen.choice(3000, 100, replace=False)]
+    lo = datagen.lattice(10, 10)
+    model = esom.LandmarkModel.create(hi, lo)
+    want = oracle.embed(pts, hi, lo, k)
+    got = esom.embed(pts, model, esom.EmbedParams(k=k), backend="base")
+    assert_xy_close(got, want, lo, f"k={k}")
+
+
+def test_outliers_far_from_landmarks():
+    # law-of-cosines guard: points 10..1000x farther than the landmark spacing
+    gen = np.random.default_rng(11)
+    hi = gen.normal(size=(64, 16)).astype(np.float32)
+    lo = datagen.lattice(8, 8)
+    far = (gen.normal(size=(2000, 16)) * np.repeat([10.0, 100.0, 1000.0, 1.0], 500)[:, None]).astype(np.float32)
+    model = esom.LandmarkModel.create(hi, lo)
+    want = oracle.embed(far, hi, lo, 16)
+    got = esom.embed(far, model, esom.EmbedParams(k=16))
+    assert_xy_close(got, want, lo, "outliers")
+
+
+def test_c2_full_size_embed(golden):
+    pts, hi, lo = c2_inputs()
+    model = esom.LandmarkModel.create(hi, lo)
+    xy = esom.embed(torch.from_numpy(pts).cuda(), model, esom.EmbedParams(k=16)).cpu().numpy()
+    assert np.all(np.isfinite(xy))
+    assert_xy_close(xy[:4096], golden["c2_xy"], lo, "c2 head vs reference")
+    rows = np.arange(0, pts.shape[0], 211)
+    want = oracle.embed(pts[rows], hi, lo, 16)
+    assert_xy_close(xy[rows], want, lo, "c2 sample vs oracle")
+
+
+def test_c4_c5_heads_embed(golden):
+    model4 = esom.LandmarkModel.create(golden["c4_hi"], golden["c4_lo"])
+    xy4 = esom.embed(golden["c4_points"], model4, esom.EmbedParams(k=16))
+    assert_xy_close(xy4, golden["c4_xy"], golden["c4_lo"], "c4 head")
+    from test_gpu_knn import _c5_model
+    hi5, lo5 = _c5_model()
+    xy5 = esom.embed(golden["c5_points"], esom.LandmarkModel.create(hi5, lo5), esom.EmbedParams(k=32))
+    assert_xy_close(xy5, golden["c5_xy"], lo5, "c5 head")
+
+
+def test_embed_errors(rng_np):
+    model = esom.LandmarkModel.create(rng_np.normal(size=(8, 4)).astype(np.float32),
+                                      rng_np.random((8, 2)).astype(np.float32))
+    with pytest.raises(esom.ParameterError):
+        esom.embed(rng_np.random((3, 4)), model, esom.EmbedParams(k=16), backend="bitonic")
+    with pytest.raises(esom.InputError):
+        esom.embed(rng_np.random((3, 5)), model, esom.EmbedParams(k=4))
+    bad = rng_np.random((3, 4)).astype(np.float32)
+    bad[1, 2] = np.nan
+    with pytest.raises(esom.InputError):
+        esom.embed(bad, model, esom.EmbedParams(k=4))

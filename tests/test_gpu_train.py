@@ -1,0 +1,124 @@
+"""Landmark training on the B200: online SOM / k-means vs the reference's
+goldens (f64 internally; only exp ulps and exact BMU near-ties may differ),
+batch SOM vs the oracle restatement, and the reference's trainer properties."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import c2_inputs
+from oracle import oracle
+import paper_2201_00701_b200 as esom
+from paper_2201_00701_b200 import datagen
+from paper_2201_00701_b200.batch_som import BatchSomConfig, FrameLoop, batch_som_step
+from paper_2201_00701_b200.core import Rng
+
+pytestmark = pytest.mark.gpu
+
+
+def close(got, want, what):
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-6, err_msg=what)
+    return float(np.mean(got == want))
+
+
+def test_som_and_kmeans_small_vs_reference(golden):
+    pts, hi0, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+    model = esom.LandmarkModel.create(hi0, lo)
+    rng = Rng(2)
+    for t in range(5):
+        model = model.with_hi(esom.som_tick(esom.Dataset.from_points(pts), model,
+                                            esom.SomConfig(sigma=0.8, alpha=0.2, batch_size=64), rng))
+        close(model.hi, golden["small_som_his"][t], f"som tick {t}")
+    model = esom.LandmarkModel.create(hi0, lo)
+    rng = Rng(3)
+    for t in range(5):
+        model = model.with_hi(esom.kmeans_tick(esom.Dataset.from_points(pts), model,
+                                               esom.KmeansConfig(alpha_km=0.3, batch_size=64), rng))
+        close(model.hi, golden["small_km_his"][t], f"kmeans tick {t}")
+
+
+def test_c3_online_ticks_vs_reference(golden):
+    pts, hi, lo = c2_inputs()
+    model = esom.LandmarkModel.create(hi, lo)
+    X = torch.from_numpy(pts).cuda()
+    got = esom.som_tick(X, model, esom.SomConfig(sigma=1.0, alpha=0.1), Rng(7)).cpu().numpy()
+    assert close(got, golden["c3_som_hi"], "c3 som") > 0.9
+    got = esom.kmeans_tick(X, model, esom.KmeansConfig(), Rng(8)).cpu().numpy()
+    assert close(got, golden["c3_km_hi"], "c3 kmeans") > 0.99
+
+
+def test_som_properties(golden):
+    pts, hi0, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+    ds = esom.Dataset.from_points(pts)
+    model = esom.LandmarkModel.create(hi0, lo)
+    out = esom.som_tick(ds, model, esom.SomConfig(sigma=1.0, alpha=0.0), Rng(3))
+    assert np.array_equal(out, model.hi)                       # tests:test_som.py:40-44
+    before = model.lo.copy()
+    esom.som_tick(ds, model, esom.SomConfig(), Rng(6))
+    assert np.array_equal(model.lo, before)                    # tests:test_som.py:105-109
+    one = esom.LandmarkModel.create(np.zeros((1, 5), np.float32), np.zeros((1, 2), np.float32))
+    s = int(Rng(9).integers(0, 500, size=1)[0])
+    out = esom.som_tick(ds, one, esom.SomConfig(sigma=1.0, alpha=1.0, batch_size=1), Rng(9))
+    np.testing.assert_array_equal(out[0], pts[s])              # tests:test_som.py:46-54
+    big = esom.som_tick(ds, model, esom.SomConfig(sigma=2.0, alpha=0.3, batch_size=1), Rng(8))
+    small = esom.som_tick(ds, model, esom.SomConfig(sigma=0.5, alpha=0.3, batch_size=1), Rng(8))
+    assert np.all(np.linalg.norm(small - model.hi, axis=1) <= np.linalg.norm(big - model.hi, axis=1) + 1e-12)
+
+
+def test_quantization_error(golden):
+    pts, hi0 = golden["small_points"], golden["small_hi0"]
+    qe = esom.quantization_error(esom.Dataset.from_points(pts), hi0)
+    assert qe == pytest.approx(float(golden["small_qe"][0]), rel=1e-6)
+
+
+def test_som_efficacy_c06():
+    # tests:test_acceptance.py:203-221 on the device trainer
+    ds = esom.Dataset.from_points(datagen.extruded_s(10_000, seed=5))
+    rng = Rng(2)
+    hi = ds.points[rng.choice_distinct(ds.n, 256)]
+    model = esom.LandmarkModel.create(hi, datagen.lattice(16, 16))
+    before = esom.quantization_error(ds, model.hi)
+    for t in range(50):
+        cfg = esom.SomConfig(sigma=1.5 + (0.2 - 1.5) * t / 49, alpha=0.1)
+        model = model.with_hi(esom.som_tick(ds, model, cfg, rng))
+    assert esom.quantization_error(ds, model.hi) <= 0.7 * before
+
+
+def test_batch_som_vs_oracle(golden):
+    pts, hi0, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+    model = esom.LandmarkModel.create(hi0, lo)
+    for mode, m in (("mean_field", 0), ("kohonen", 1)):
+        got = batch_som_step(pts, model, BatchSomConfig(sigma=0.9, alpha=0.3, mode=mode))
+        want = oracle.batch_som_step(pts, hi0, lo, 0.9, 0.3, m)
+        close(got, want, mode)
+    pts2, hi2, lo2 = c2_inputs()
+    sub = pts2[: 1 << 17]
+    got = batch_som_step(torch.from_numpy(sub).cuda(), esom.LandmarkModel.create(hi2, lo2),
+                         BatchSomConfig(sigma=1.0, alpha=0.1)).cpu().numpy()
+    want = oracle.batch_som_step(sub, hi2, lo2, 1.0, 0.1)
+    close(got, want, "c3 batch")
+
+
+def test_batch_som_b1_equals_online(golden):
+    pts, hi0, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+    model = esom.LandmarkModel.create(hi0, lo)
+    for s in (3, 77, 401):
+        batch = batch_som_step(pts[s:s + 1], model, BatchSomConfig(sigma=0.8, alpha=0.4))
+        online = oracle.som_tick(pts, hi0, lo, np.array([s]), 0.8, 0.4)
+        np.testing.assert_allclose(batch, online, rtol=1e-6, atol=1e-7)
+
+
+def test_frame_loop_trains_and_embeds():
+    pts, hi, lo = c2_inputs()
+    X = torch.from_numpy(pts).cuda()
+    loop = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=1.5, alpha=0.5))
+    qes = []
+    for _ in range(5):
+        loop.frame()
+        qes.append(float(loop.qe.item()) / pts.shape[0])
+    assert qes[-1] < qes[0]
+    assert torch.isfinite(loop.xy).all()
+    # the frame's embedding equals a standalone embed under the same landmarks
+    hi_now = loop.model.hi.clone()
+    xy_loop = loop.frame().clone()
+    xy_ref = esom.embed(X, esom.LandmarkModel.create(hi_now.cpu().numpy(), lo), esom.EmbedParams(k=16))
+    assert torch.equal(xy_loop, xy_ref)
