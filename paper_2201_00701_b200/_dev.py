@@ -9,9 +9,13 @@ device) so concurrent callers on different streams never share scratch.
 from __future__ import annotations
 
 import threading
+import warnings
 
 import numpy as np
 import torch
+
+# read-only inputs (the reference's frozen core arrays) are only ever read
+warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
 
 from .core import InputError
 

@@ -102,29 +102,39 @@ def test_fixed_point_c02():
 
 
 def test_equivariance_c04():
-    # tests:test_acceptance.py:124-163, through the device project_point
+    # tests:test_acceptance.py:104-163 -- the reference's own instance stream
+    # (default_rng(53), same draw order) through the device knn/scores/project_point
     gen = np.random.default_rng(53)
-    worst = dict(scale=0.0, trans=0.0, rot=0.0)
-    for _ in range(30):
+    worst = dict(scale=0.0, trans=0.0, rot=0.0, iso=0.0)
+    for _ in range(100):
         hi = gen.normal(size=(24, 6)).astype(np.float32)
         lo = gen.random((24, 2)).astype(np.float32)
         model = esom.LandmarkModel.create(hi, lo)
         x = gen.normal(size=6).astype(np.float32)
-        nb = esom.knn_base(x.reshape(1, -1), hi, 8)
-        s = esom.scores(nb.sqdists[0])
-        base = esom.project_point(x, model, nb.indices[0], s)
+        nb = esom.knn_base(x.reshape(1, -1), model.hi, 8)
+        idx, s = nb.indices[0], esom.scores(nb.sqdists[0])
+        base = esom.project_point(x, model, idx, s)
         c = float(gen.uniform(0.1, 10.0))
         worst["scale"] = max(worst["scale"], float(np.abs(
-            esom.project_point(x, model, nb.indices[0], ScoreVector(scores=s.scores * c)) - base).max()))
+            esom.project_point(x, model, idx, ScoreVector(scores=s.scores * c)) - base).max()))
         t = gen.normal(size=2).astype(np.float32)
         worst["trans"] = max(worst["trans"], float(np.abs(
-            esom.project_point(x, model.with_lo(lo + t), nb.indices[0], s) - (base + t)).max()))
+            esom.project_point(x, model.with_lo(model.lo + t), idx, s) - (base + t)).max()))
         th = float(gen.uniform(0, 2 * np.pi))
         rot = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
-        rl = (lo.astype(np.float64) @ rot.T).astype(np.float32)
+        rl = (model.lo.astype(np.float64) @ rot.T).astype(np.float32)
         worst["rot"] = max(worst["rot"], float(np.abs(
-            esom.project_point(x, model.with_lo(rl), nb.indices[0], s) - base @ rot.T).max()))
-    assert worst["scale"] <= 1e-6 and worst["trans"] <= 1e-5 and worst["rot"] <= 1e-5, worst
+            esom.project_point(x, model.with_lo(rl), idx, s) - base @ rot.T).max()))
+        q, _ = np.linalg.qr(gen.normal(size=(6, 6)))
+        shift = gen.normal(size=6)
+        hi2 = (model.hi.astype(np.float64) @ q.T + shift).astype(np.float32)
+        x2 = (x.astype(np.float64) @ q.T + shift).astype(np.float32)
+        moved = model.with_hi(hi2)
+        nb2 = esom.knn_base(x2.reshape(1, -1), moved.hi, 8)
+        iso = esom.project_point(x2, moved, nb2.indices[0], esom.scores(nb2.sqdists[0]))
+        worst["iso"] = max(worst["iso"], float(np.abs(iso - base).max()))
+    ok = worst["scale"] <= 1e-6 and worst["trans"] <= 1e-5 and worst["rot"] <= 1e-5 and worst["iso"] <= 1e-4
+    assert ok, worst
 
 
 def test_chunking_and_backends_bit_identical(rng_np):
