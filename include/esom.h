@@ -44,8 +44,9 @@ typedef esom_stream_t cudaStream_t;
 int esom_version(void);
 const char *esom_last_error(void);
 
-/* Bytes of scratch for esom_knn (with_pairs = 0) or for esom_prepare_model /
- * esom_embed (with_pairs = 1: packed landmark tiles + g×g pair table). */
+/* Bytes of scratch for esom_knn / esom_bmu_accumulate (with_pairs = 0) or
+ * for a prepared model (with_pairs = 1: packed landmark tiles + the packed
+ * upper-triangular pair table). */
 size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs);
 
 /* Exact k nearest landmarks per point, rows ascending by (sqdist, index).
@@ -71,17 +72,25 @@ int esom_project(const float *X, int64_t n, int32_t d, const float *hi, const fl
 int esom_prepare_model(const float *hi, int32_t g, int32_t d, int32_t k, void *workspace,
                        size_t ws_bytes, int32_t *nonfinite_flag, cudaStream_t stream);
 
-/* Fused embed on a prepared workspace: k-NN + scores + projection -> xy
- * (n×2 f32).  Replaces embed (ref: projection.py:220-245).  Optional
- * outputs (NULL to skip): bmu (n int32 = idx[:,0]); batch-SOM statistics
- * acc_S (g×d f64 += x_i per BMU) and acc_C (g f64 += 1); qe_sum (f64 +=
- * nearest squared distance, ref: som.py:71-79).  k <= 64. */
+/* Per-call scratch of esom_embed_prepared for n points: the neighbour rows
+ * of one L2-resident chunk of points (scan -> projection). */
+size_t esom_point_workspace_bytes(int64_t n, int32_t k);
+
+/* Embed on a prepared model: exact k-NN scan + scores + projection -> xy
+ * (n×2 f32), two kernels per chunk.  Replaces embed (ref:
+ * projection.py:220-245).  Optional outputs (NULL to skip): bmu (n int32 =
+ * idx[:,0]); batch-SOM statistics acc_S (g×d f64 += x_i per BMU) and acc_C
+ * (g f64 += 1); qe_sum (f64 += nearest squared distance, ref: som.py:71-79).
+ * k <= 64. */
 int esom_embed_prepared(const float *X, int64_t n, int32_t d, const float *hi, const float *lo,
-                        int32_t g, int32_t k, const void *workspace, float *xy, int32_t *bmu,
-                        double *acc_S, double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
+                        int32_t g, int32_t k, const void *model_ws, void *point_ws,
+                        size_t point_ws_bytes, float *xy, int32_t *bmu, double *acc_S,
+                        double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
                         cudaStream_t stream);
 
-/* esom_prepare_model + esom_embed_prepared. */
+/* esom_prepare_model + esom_embed_prepared in one workspace of
+ * esom_embed_workspace_bytes(n, g, d, k) bytes. */
+size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k);
 int esom_embed(const float *X, int64_t n, int32_t d, const float *hi, const float *lo, int32_t g,
                int32_t k, void *workspace, size_t ws_bytes, float *xy, int32_t *bmu,
                double *acc_S, double *acc_C, double *qe_sum, int32_t *nonfinite_flag,

@@ -29,7 +29,8 @@ SIGNATURES = {
     "esom_scores": [_vp, _i64, _i32, _vp, _vp],
     "esom_project": [_vp, _i64, _i32, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp],
     "esom_prepare_model": [_vp, _i32, _i32, _i32, _vp, _sz, _vp, _vp],
-    "esom_embed_prepared": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "esom_embed_prepared": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp,
+                            _vp],
     "esom_embed": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "esom_bmu_accumulate": [_vp, _i64, _i32, _vp, _i32, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp],
     "esom_som_tick": [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _f64, _f64, _vp, _sz, _vp],
@@ -41,6 +42,8 @@ HELPERS = {
     "esom_last_error": ([], C.c_char_p),
     "esom_workspace_bytes": ([_i32, _i32, _i32, _i32], C.c_size_t),
     "esom_tick_workspace_bytes": ([_i32, _i32], C.c_size_t),
+    "esom_point_workspace_bytes": ([_i64, _i32], C.c_size_t),
+    "esom_embed_workspace_bytes": ([_i64, _i32, _i32, _i32], C.c_size_t),
 }
 
 

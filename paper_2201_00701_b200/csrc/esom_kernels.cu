@@ -2,9 +2,11 @@
 // declared in include/esom.h.
 //
 //   pack_landmarks_kernel   hi (g×d) -> Lt[tile][c][32], padded   (prep for TMA staging)
-//   pair_table_kernel       g×g f32 table 0.5/hd2 (faithful hd2 test)    ref: projection.py:332-340
-//   scan_kernel<DC,KP,MODE> fused distance + top-k (+ scores + projection + batch-SOM stats)
-//                            ref: knn.py:65-92 / 148-184, projection.py:220-245
+//   pair_table_kernel       packed triangle 0.5/hd2 (faithful hd2 test)  ref: projection.py:332-340
+//   knn_scan_kernel<DC,KP>  exact distance tiles + top-k (+ BMU statistics)   esom_scan.cuh
+//                            ref: knn.py:65-92 / 148-184
+//   project_fast_kernel<KP> scores + law-of-cosines projection              esom_project.cuh
+//                            ref: projection.py:38-121; embed = scan + project (projection.py:220-245)
 //   knn_sort_kernel         k > 64 fallback: block-per-point full sort    ref: knn.py:201-214
 //   scores_kernel           ref: projection.py:38-65
 //   project_kernel          faithful mixed-precision pair loop            ref: projection.py:68-121
@@ -113,13 +115,15 @@ __global__ void check_finite_kernel(const float* __restrict__ v, int64_t count, 
     flag_nonfinite(flag, bad);
 }
 
-// T[u*g+v] = 0.5 / hd2(u,v) as f32 when the reference keeps the pair
-// (hd2 >= 1e-12 with hd2 = sum_c (f64)(e*e), e = hi[v,c] - hi[u,c] in f32,
-// ref: projection.py:332-340), else -1.
+// Packed upper triangle T[tri(u,v)] (u < v) = 0.5 / hd2(u,v) as f32 when the
+// reference keeps the pair (hd2 >= 1e-12 with hd2 = sum_c (f64)(e*e), e =
+// hi[v,c] - hi[u,c] in f32, ref: projection.py:332-340), else -1.  hd2 is
+// symmetric (f32 subtraction is sign-symmetric), so one triangle suffices.
 __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, float* __restrict__ T) {
     const int64_t total = (int64_t)g * g;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int u = (int)(e / g), v = (int)(e % g);
+        if (v <= u) continue;
         const float* hu = hi + (int64_t)u * d;
         const float* hv = hi + (int64_t)v * d;
         double hd2 = 0.0;
@@ -127,7 +131,7 @@ __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, fl
             const float df = __fsub_rn(hv[c], hu[c]);
             hd2 = __dadd_rn(hd2, (double)__fmul_rn(df, df));
         }
-        T[e] = hd2 < kPairEps ? -1.0f : (float)(0.5 / hd2);
+        T[(int64_t)u * (2 * (int64_t)g - u - 1) / 2 + (v - u - 1)] = hd2 < kPairEps ? -1.0f : (float)(0.5 / hd2);
     }
 }
 
@@ -472,16 +476,10 @@ Plan make_plan(int d, int g, int k) {
     return p;
 }
 
-template <int MODE>
-int launch_scan(const Plan& p, ScanArgs a, cudaStream_t st) {
-#define ESOM_CASE(DCV, KPV)                                  \
-    if (p.dc == DCV && p.kp == KPV) return launch_scan_t<DCV, KPV, MODE>(a, st);
-#define ESOM_KPS(DCV)                                                                                 \
-    if (MODE == 2) {                                                                                  \
-        ESOM_CASE(DCV, 4)                                                                             \
-    } else {                                                                                          \
-        ESOM_CASE(DCV, 4) ESOM_CASE(DCV, 8) ESOM_CASE(DCV, 16) ESOM_CASE(DCV, 32) ESOM_CASE(DCV, 64) \
-    }
+int dispatch_scan(const Plan& p, ScanArgs a, cudaStream_t st) {
+#define ESOM_CASE(DCV, KPV) \
+    if (p.dc == DCV && p.kp == KPV) return launch_scan_t<DCV, KPV>(a, st);
+#define ESOM_KPS(DCV) ESOM_CASE(DCV, 4) ESOM_CASE(DCV, 8) ESOM_CASE(DCV, 16) ESOM_CASE(DCV, 32) ESOM_CASE(DCV, 64)
     ESOM_KPS(4)
     ESOM_KPS(8)
     ESOM_KPS(16)
@@ -490,6 +488,17 @@ int launch_scan(const Plan& p, ScanArgs a, cudaStream_t st) {
 #undef ESOM_KPS
 #undef ESOM_CASE
     return set_err(ESOM_ERR_UNSUPPORTED, "no scan kernel for this (d, k)%s", "");
+}
+
+int dispatch_project(int kp, ProjArgs a, cudaStream_t st) {
+    switch (kp) {
+        case 4: return launch_project_t<4>(a, st);
+        case 8: return launch_project_t<8>(a, st);
+        case 16: return launch_project_t<16>(a, st);
+        case 32: return launch_project_t<32>(a, st);
+        case 64: return launch_project_t<64>(a, st);
+    }
+    return set_err(ESOM_ERR_UNSUPPORTED, "no projection kernel for k%s", "");
 }
 
 int grid_for(int64_t work, int threads) {
@@ -511,13 +520,44 @@ int esom_version(void) { return ESOM_ABI_VERSION; }
 
 const char* esom_last_error(void) { return g_err; }
 
+static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
 size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs) {
-    (void)k;
     const Plan p = make_plan(d, g, k < 1 ? 1 : k);
-    size_t bytes = (size_t)p.ntiles * p.tile_bytes;
-    bytes = (bytes + 255) / 256 * 256;
-    if (with_pairs) bytes += (size_t)g * g * 4;
+    size_t bytes = align256((size_t)p.ntiles * p.tile_bytes);
+    if (with_pairs) bytes += align256((size_t)g * (g > 1 ? g - 1 : 1) / 2 * 4);
     return bytes + 256;
+}
+
+// points per embed chunk: the chunk's neighbour rows stay L2-resident between
+// the k-NN scan and the projection kernel
+static int64_t embed_chunk(int32_t k) {
+    const char* e = getenv("ESOM_EMBED_CHUNK");
+    const int64_t c = e ? atoll(e) : (int64_t)(24u << 20) / (8 * (int64_t)k);
+    return c < 1024 ? 1024 : c;
+}
+
+size_t esom_point_workspace_bytes(int64_t n, int32_t k) {
+    const int64_t c = n < embed_chunk(k) ? n : embed_chunk(k);
+    return align256((size_t)(c > 0 ? c : 1) * k * 4) * 2 + 256;
+}
+
+static ScanArgs scan_args(const Plan& p, const float* X, int64_t n, int32_t d, const float* L, int32_t g, int32_t k,
+                          const float* Lt, int32_t* flag) {
+    ScanArgs a{};
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.dp = p.dp;
+    a.nch = p.nch;
+    a.Lt = Lt;
+    a.L = L;
+    a.g = g;
+    a.ntiles = p.ntiles;
+    a.k = k;
+    a.flag = flag;
+    a.nz = -0.0f;
+    return a;
 }
 
 int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, int32_t k, int32_t* idx,
@@ -533,7 +573,6 @@ int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, in
         cudaFuncSetAttribute(knn_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int grid = (int)(n < (int64_t)num_sms() * 8 ? n : (int64_t)num_sms() * 8);
         knn_sort_kernel<<<grid, 256, smem, stream>>>(X, n, d, L, g, gpow, k, idx, sqd, nonfinite_flag);
-        // landmarks' finiteness (the scan path checks them while packing)
         if (int e = cuda_check("knn_sort_kernel")) return e;
         check_finite_kernel<<<grid_for((int64_t)g * d, 256), 256, 0, stream>>>(L, (int64_t)g * d, nonfinite_flag);
         return cuda_check("check_finite");
@@ -544,21 +583,10 @@ int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, in
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(L, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
-    ScanArgs a{};
-    a.X = X;
-    a.n = n;
-    a.d = d;
-    a.dp = p.dp;
-    a.nch = p.nch;
-    a.Lt = Lt;
-    a.g = g;
-    a.ntiles = p.ntiles;
-    a.k = k;
+    ScanArgs a = scan_args(p, X, n, d, L, g, k, Lt, nonfinite_flag);
     a.out_idx = idx;
     a.out_sqd = sqd;
-    a.flag = nonfinite_flag;
-    a.nz = -0.0f;
-    return launch_scan<0>(p, a, stream);
+    return dispatch_scan(p, a, stream);
 }
 
 int esom_scores(const float* sqd, int64_t n, int32_t k, double* out, cudaStream_t stream) {
@@ -583,8 +611,7 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     const Plan p = make_plan(d, g, k);
     if (ws_bytes < esom_workspace_bytes(g, d, k, 1)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
     float* Lt = reinterpret_cast<float*>(workspace);
-    const size_t lt_bytes = ((size_t)p.ntiles * p.tile_bytes + 255) / 256 * 256;
-    float* T = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + lt_bytes);
+    float* T = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align256((size_t)p.ntiles * p.tile_bytes));
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
@@ -593,43 +620,60 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
 }
 
 int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
-                        const void* workspace, float* xy, int32_t* bmu, double* acc_S, double* acc_C,
-                        double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
+                        const void* model_ws, void* point_ws, size_t point_ws_bytes, float* xy, int32_t* bmu,
+                        double* acc_S, double* acc_C, double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
     if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64%s", "");
     if (n == 0) return ESOM_OK;
+    if (point_ws_bytes < esom_point_workspace_bytes(n, k))
+        return set_err(ESOM_ERR_PARAM, "point workspace too small%s", "");
     const Plan p = make_plan(d, g, k);
-    const size_t lt_bytes = ((size_t)p.ntiles * p.tile_bytes + 255) / 256 * 256;
-    ScanArgs a{};
-    a.X = X;
-    a.n = n;
-    a.d = d;
-    a.dp = p.dp;
-    a.nch = p.nch;
-    a.Lt = reinterpret_cast<const float*>(workspace);
-    a.T = reinterpret_cast<const float*>(reinterpret_cast<const char*>(workspace) + lt_bytes);
-    a.g = g;
-    a.ntiles = p.ntiles;
-    a.k = k;
-    a.hi = hi;
-    a.lo = lo;
-    a.xy = xy;
-    a.bmu = bmu;
-    a.accS = acc_S;
-    a.accC = acc_C;
-    a.qe_sum = qe_sum;
-    a.flag = nonfinite_flag;
-    a.nz = -0.0f;
-    return launch_scan<1>(p, a, stream);
+    const float* Lt = reinterpret_cast<const float*>(model_ws);
+    const float* T = reinterpret_cast<const float*>(reinterpret_cast<const char*>(model_ws) +
+                                                    align256((size_t)p.ntiles * p.tile_bytes));
+    const int64_t chunk = n < embed_chunk(k) ? n : embed_chunk(k);
+    int32_t* idx = reinterpret_cast<int32_t*>(point_ws);
+    float* sqd = reinterpret_cast<float*>(reinterpret_cast<char*>(point_ws) + align256((size_t)chunk * k * 4));
+    for (int64_t s = 0; s < n; s += chunk) {
+        const int64_t m = n - s < chunk ? n - s : chunk;
+        ScanArgs a = scan_args(p, X + s * d, m, d, hi, g, k, Lt, nonfinite_flag);
+        a.out_idx = idx;
+        a.out_sqd = sqd;
+        a.bmu = bmu ? bmu + s : nullptr;
+        a.accS = acc_S;
+        a.accC = acc_C;
+        a.qe_sum = qe_sum;
+        if (int e = dispatch_scan(p, a, stream)) return e;
+        ProjArgs q{};
+        q.idx = idx;
+        q.sqd = sqd;
+        q.n = m;
+        q.k = k;
+        q.g = g;
+        q.lo = lo;
+        q.T = T;
+        q.xy = xy + 2 * s;
+        q.X = X + s * d;
+        q.hi = hi;
+        q.d = d;
+        if (int e = dispatch_project(p.kp, q, stream)) return e;
+    }
+    return ESOM_OK;
+}
+
+size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k) {
+    return esom_workspace_bytes(g, d, k, 1) + esom_point_workspace_bytes(n, k);
 }
 
 int esom_embed(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
                void* workspace, size_t ws_bytes, float* xy, int32_t* bmu, double* acc_S, double* acc_C,
                double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
     if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
-    if (int e = esom_prepare_model(hi, g, d, k, workspace, ws_bytes, nonfinite_flag, stream)) return e;
-    return esom_embed_prepared(X, n, d, hi, lo, g, k, workspace, xy, bmu, acc_S, acc_C, qe_sum, nonfinite_flag,
-                               stream);
+    const size_t mb = esom_workspace_bytes(g, d, k, 1);
+    if (ws_bytes < esom_embed_workspace_bytes(n, g, d, k)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    if (int e = esom_prepare_model(hi, g, d, k, workspace, mb, nonfinite_flag, stream)) return e;
+    return esom_embed_prepared(X, n, d, hi, lo, g, k, workspace, reinterpret_cast<char*>(workspace) + mb,
+                               ws_bytes - mb, xy, bmu, acc_S, acc_C, qe_sum, nonfinite_flag, stream);
 }
 
 int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, int32_t g, void* workspace,
@@ -643,23 +687,12 @@ int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, i
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
-    ScanArgs a{};
-    a.X = X;
-    a.n = n;
-    a.d = d;
-    a.dp = p.dp;
-    a.nch = p.nch;
-    a.Lt = Lt;
-    a.g = g;
-    a.ntiles = p.ntiles;
-    a.k = 1;
+    ScanArgs a = scan_args(p, X, n, d, hi, g, 1, Lt, nonfinite_flag);
     a.bmu = bmu;
     a.accS = acc_S;
     a.accC = acc_C;
     a.qe_sum = qe_sum;
-    a.flag = nonfinite_flag;
-    a.nz = -0.0f;
-    return launch_scan<2>(p, a, stream);
+    return dispatch_scan(p, a, stream);
 }
 
 size_t esom_tick_workspace_bytes(int32_t g, int32_t d) { return (size_t)g * d * 8 + 256; }

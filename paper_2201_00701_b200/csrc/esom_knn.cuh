@@ -1,4 +1,5 @@
-// esom_knn.cuh -- fused exact f32 distance scan + register top-k selection.
+// esom_knn.cuh -- exact f32 distance tiles and the register/shared-memory
+// top-k selection of the k-NN scan kernel.
 //
 // One thread owns one point (ref: knn.py:65-92 `_knn_base_kernel` walks the
 // landmarks of one point in ascending j).  Landmarks sit in shared memory as
@@ -7,12 +8,17 @@
 // packed f32x2 lanes for two landmarks; the point's coordinates stay in
 // registers.  Per tile each thread produces 32 exact squared distances.
 //
-// Selection keeps a sorted (dist, idx) list of KP >= k entries in registers.
-// Because j only grows, a new candidate precedes an equal-distance entry
-// never (lexicographic key (s, j), ref: knn.py:79,85,96-97), so insertion
-// uses strict '<'.  Candidates that beat the current k-th key are parked in
-// a per-thread shared-memory slot row and inserted in a divergent loop whose
-// trip count is the warp's max candidate count (not the tile size).
+// Selection (exact, equal to the reference's lexicographic (dist, index)
+// order, ref: knn.py:79,85,96-97):
+//  * a VALUES-ONLY sorted list vd[KP] in registers (min/max insertion, two
+//    FMNMX per slot, no index bookkeeping) gives the running k-th distance tau;
+//  * every landmark that beats tau when scanned is appended, in index order,
+//    to a per-thread candidate log in shared memory (value, index);
+//  * at the end the final set is {log entries with v < tau_f} plus the
+//    lowest-index entries with v == tau_f, ranked by (v, j).
+// A landmark that is not logged had v >= tau at scan time, and tau only
+// decreases, so it cannot be in the top k (ties go to lower indices, which
+// were scanned earlier) -- the selection is exact, ties included.
 #pragma once
 #include "esom_common.cuh"
 
@@ -35,7 +41,7 @@ __device__ __forceinline__ void tile_accumulate(const float (&x)[DC], const floa
             f2 s0 = f2_sq(t0, nz);
             f2 s1 = f2_sq(t1, nz);
             if (first && c == 0) {
-                acc[2 * q] = s0;          // 0 + t^2 == t^2 exactly
+                acc[2 * q] = s0;  // 0 + t^2 == t^2 exactly
                 acc[2 * q + 1] = s1;
             } else {
                 acc[2 * q] = f2_add(acc[2 * q], s0);
@@ -45,87 +51,30 @@ __device__ __forceinline__ void tile_accumulate(const float (&x)[DC], const floa
     }
 }
 
-// Insert (v, j) into the sorted register list; j exceeds every held index.
-template <int KP>
-__device__ __forceinline__ void topk_insert(float (&td)[KP], int (&ti)[KP], float v, int j) {
-#pragma unroll
-    for (int q = KP - 1; q > 0; --q) {
-        const bool gp = td[q - 1] > v;
-        const bool gc = td[q] > v;
-        td[q] = gp ? td[q - 1] : (gc ? v : td[q]);
-        ti[q] = gp ? ti[q - 1] : (gc ? j : ti[q]);
-    }
-    if (td[0] > v) {
-        td[0] = v;
-        ti[0] = j;
-    }
-}
+constexpr float kInf = __builtin_huge_valf();
 
-// Exact lexicographic insertion, only needed when v == +inf (an overflowed
-// distance competing with the (+inf, g) sentinels of still-empty slots).
+// Live slots of the values list are [KP-k, KP); slots below hold -inf and
+// never move, so the k-th smallest value is always vd[KP-1].
 template <int KP>
-__device__ __forceinline__ void topk_insert_lex(float (&td)[KP], int (&ti)[KP], float v, int j) {
+__device__ __forceinline__ void vlist_init(float (&vd)[KP], int k) {
 #pragma unroll
-    for (int q = KP - 1; q > 0; --q) {
-        const bool gp = td[q - 1] > v || (td[q - 1] == v && ti[q - 1] > j);
-        const bool gc = td[q] > v || (td[q] == v && ti[q] > j);
-        td[q] = gp ? td[q - 1] : (gc ? v : td[q]);
-        ti[q] = gp ? ti[q - 1] : (gc ? j : ti[q]);
-    }
-    if (td[0] > v || (td[0] == v && ti[0] > j)) {
-        td[0] = v;
-        ti[0] = j;
-    }
-}
-
-// The live list occupies slots [KP-k, KP); slots below hold -inf and never
-// move, so the k-th key is always td[KP-1] (a static register).
-template <int KP>
-__device__ __forceinline__ void topk_init(float (&td)[KP], int (&ti)[KP], int k, int sentinel) {
-#pragma unroll
-    for (int q = 0; q < KP; ++q) {
-        td[q] = q >= KP - k ? __int_as_float(0x7f800000) : __int_as_float(0xff800000);
-        ti[q] = sentinel;
-    }
+    for (int q = 0; q < KP; ++q) vd[q] = q >= KP - k ? kInf : -kInf;
 }
 
 template <int KP>
-__device__ __forceinline__ float topk_tau(const float (&td)[KP], int) {
-    return td[KP - 1];
+__device__ __forceinline__ void vlist_insert(float (&vd)[KP], float v) {
+#pragma unroll
+    for (int q = KP - 1; q > 0; --q) vd[q] = fmaxf(vd[q - 1], fminf(vd[q], v));
+    vd[0] = fminf(vd[0], v);
 }
 
-// Merge one tile's 32 distances into the top-k list.
+// number of values (live or -inf padding) strictly below v
 template <int KP>
-__device__ __forceinline__ void topk_tile(float (&td)[KP], int (&ti)[KP], const f2 (&acc)[16], int jbase,
-                                          int k, float* __restrict__ cbuf, int tid) {
-    float tau = topk_tau<KP>(td, k);
-    const bool open = tau == __int_as_float(0x7f800000);  // k-th slot still empty
-    uint32_t m = 0;
+__device__ __forceinline__ int vlist_count_lt(const float (&vd)[KP], float v) {
+    int c = 0;
 #pragma unroll
-    for (int p = 0; p < 16; ++p) {
-        float a, b;
-        f2_unpack(acc[p], a, b);
-        if (a < tau || (open && a == tau)) {
-            m |= 1u << (2 * p);
-            cbuf[(2 * p) * kThreads + tid] = a;
-        }
-        if (b < tau || (open && b == tau)) {
-            m |= 1u << (2 * p + 1);
-            cbuf[(2 * p + 1) * kThreads + tid] = b;
-        }
-    }
-    while (m) {
-        const int t = __ffs(m) - 1;
-        m &= m - 1;
-        const float v = cbuf[t * kThreads + tid];
-        if (v < tau) {
-            topk_insert<KP>(td, ti, v, jbase + t);
-            tau = topk_tau<KP>(td, k);
-        } else if (v == tau && tau == __int_as_float(0x7f800000) && jbase + t < 0x7fffffff) {
-            topk_insert_lex<KP>(td, ti, v, jbase + t);
-            tau = topk_tau<KP>(td, k);
-        }
-    }
+    for (int q = 0; q < KP; ++q) c += vd[q] < v ? 1 : 0;
+    return c;
 }
 
 }  // namespace esom

@@ -1,6 +1,9 @@
-// esom_scan.cuh -- the fused scan kernel (distance + top-k [+ scores +
-// projection | + BMU statistics]) and its launcher template.  Instantiated
-// per (DC, KP, MODE) in inst/*.cu so the library builds in parallel.
+// esom_scan.cuh -- the exact k-NN scan kernel (distance tiles + selection,
+// optional batch-SOM statistics) and its launcher template.  Instantiated
+// per (DC, KP) in inst/*.cu so the library builds in parallel.
+//
+//   ref: knn.py:56-62 (_sqdist_f32), 65-92 (_knn_base_kernel),
+//        148-184 (_knn_bitonic_kernel; identical output), 201-243 (API)
 #pragma once
 #include "esom_common.cuh"
 #include "esom_host.h"
@@ -8,23 +11,6 @@
 #include "esom_scan_args.h"
 
 namespace esom {
-
-
-// ---------------------------------------------------------------------------
-// Fused scan kernel.
-//
-// MODE 0: k-NN only -> idx/sqd rows.
-// MODE 1: embed -> scores + fast projection -> xy; optional batch-SOM stats
-//         (BMU = idx[0]) and the quantization-error sum.
-//
-// Fast projection ("law of cosines"): for a kept pair,
-//   dnum = (x - h_u).(h_v - h_u) = (sqd_u - sqd_v + hd2) / 2
-// so h = dnum/hd2 + g.lo_u = 0.5 + (sqd_u - sqd_v) * T[u,v] + g.lo_u with
-// T = 0.5/hd2 from pair_table_kernel.  Its absolute error is bounded by
-// ~u*sqrt(d)*(sqd_u + sqd_v)/hd2; points whose kappa = max (sqd_u+sqd_v)/hd2
-// exceeds kKappaMax (far outliers) are redone with the exact f64 pair loop.
-// ---------------------------------------------------------------------------
-
 
 template <int DC>
 __device__ __forceinline__ bool load_x(const float* __restrict__ X, int64_t i, int64_t n, int d, int c0,
@@ -44,52 +30,49 @@ __device__ __forceinline__ bool load_x(const float* __restrict__ X, int64_t i, i
     return bad;
 }
 
-// Exact (f64, x-based) pair accumulation for one point: used for outliers.
-static __device__ __noinline__ void pairs_exact(const float* __restrict__ X, int64_t i, int d, const float* __restrict__ hi,
-                            const float* __restrict__ lo, int k, const int* sj, const float* ss, int tid,
-                            double& a11, double& a12, double& a22, double& c1, double& c2) {
-    a11 = a12 = a22 = c1 = c2 = 0.0;
-    const float* x = X + i * d;
-    for (int u = 0; u < k; ++u) {
-        const float su = ss[u * kThreads + tid];
-        if (su <= 0.0f) continue;
-        const int ju = sj[u * kThreads + tid];
-        const float* hu = hi + (int64_t)ju * d;
-        for (int v = u + 1; v < k; ++v) {
-            const float sv = ss[v * kThreads + tid];
-            const double w = (double)su * (double)sv;
-            if (!(w > 0.0)) continue;
-            const int jv = sj[v * kThreads + tid];
-            const float* hv = hi + (int64_t)jv * d;
-            double hd2 = 0.0, hd2f = 0.0, dnum = 0.0;
-            for (int c = 0; c < d; ++c) {
-                const double hu_c = hu[c];
-                const double e = (double)hv[c] - hu_c;
-                const float ef = __fsub_rn(hv[c], hu[c]);
-                hd2f = __dadd_rn(hd2f, (double)__fmul_rn(ef, ef));
-                hd2 = fma(e, e, hd2);
-                dnum = fma((double)x[c] - hu_c, e, dnum);
-            }
-            if (hd2f < kPairEps) continue;
-            const float lux = lo[2 * ju], luy = lo[2 * ju + 1];
-            const float ex = __fsub_rn(lo[2 * jv], lux);
-            const float ey = __fsub_rn(lo[2 * jv + 1], luy);
-            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-            if ((double)ld2 < kPairEps) continue;
-            const double G1 = (double)ex / (double)ld2, G2 = (double)ey / (double)ld2;
-            const double h = dnum / hd2 + G1 * (double)lux + G2 * (double)luy;
-            const double wg1 = w * G1, wg2 = w * G2, wh = w * h;
-            a11 = fma(wg1, G1, a11);
-            a12 = fma(wg1, G2, a12);
-            a22 = fma(wg2, G2, a22);
-            c1 = fma(wh, G1, c1);
-            c2 = fma(wh, G2, c2);
+// Rare exact fallback for one point whose candidate log overflowed (massive
+// exact ties / overflowing distances): the reference's own insertion scan
+// (ref: knn.py:65-92) over row-major landmarks, writing rank-ordered rows.
+static __device__ __noinline__ void knn_point_slow(const float* __restrict__ x, int d, const float* __restrict__ L,
+                                                   int g, int k, int32_t* oi, float* od, int* b0, float* d0) {
+    float bd[64];
+    int bi[64];
+    int cnt = 0;
+    for (int j = 0; j < g; ++j) {
+        const float* l = L + (int64_t)j * d;
+        float s = 0.0f;
+        for (int c = 0; c < d; ++c) {
+            const float t = __fsub_rn(x[c], l[c]);
+            s = __fadd_rn(s, __fmul_rn(t, t));
+        }
+        int p;
+        if (cnt < k) {
+            p = cnt++;
+        } else {
+            if (s > bd[k - 1] || (s == bd[k - 1] && j > bi[k - 1])) continue;
+            p = k - 1;
+        }
+        while (p > 0 && (s < bd[p - 1] || (s == bd[p - 1] && j < bi[p - 1]))) {
+            bd[p] = bd[p - 1];
+            bi[p] = bi[p - 1];
+            --p;
+        }
+        bd[p] = s;
+        bi[p] = j;
+    }
+    for (int q = 0; q < k; ++q) {
+        if (oi) {
+            oi[q] = bi[q];
+            od[q] = bd[q];
         }
     }
+    *b0 = bi[0];
+    *d0 = bd[0];
 }
 
-template <int DC, int KP, int MODE>
-__global__ void __launch_bounds__(kThreads) scan_kernel(ScanArgs a) {
+template <int DC, int KP>
+__global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
+    constexpr int LOGCAP = KP + kTile;  // one tile of appends on top of a compacted log
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];  // TMA completion barriers
     const int tid = threadIdx.x;
@@ -97,15 +80,13 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(ScanArgs a) {
     const uint32_t tile_bytes = (uint32_t)tile_floats * 4u;
     const int nbuf = a.res_tiles ? a.res_tiles : 2;
     float* tiles = reinterpret_cast<float*>(smem_raw);
-    float* cbuf = tiles + (size_t)nbuf * tile_floats;              // [32][kThreads] candidates
-    // MODE 1 per-thread neighbour rows [KP][kThreads], aliasing cbuf (the
-    // candidate rows are dead once the tile loop of a point block is done)
-    int* sj = reinterpret_cast<int*>(cbuf);
-    float* ssq = reinterpret_cast<float*>(sj + KP * kThreads);
-    float* ssc = ssq + KP * kThreads;
+    float* logv = tiles + (size_t)nbuf * tile_floats;            // [LOGCAP][kThreads]
+    int* logj = reinterpret_cast<int*>(logv + LOGCAP * kThreads);  // [LOGCAP][kThreads]
 
     const f2 nz = f2_pack(a.nz, a.nz);
     const bool stream = a.res_tiles == 0;
+    const int k = a.k;
+    const int off = KP - k;
     uint32_t uses0 = 0, uses1 = 0;
 
     if (tid == 0) {
@@ -128,15 +109,16 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(ScanArgs a) {
     double qe_local = 0.0;
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         const int64_t i = blk * kThreads + tid;
+        const bool valid = i < a.n;
         float x[DC];
         if (a.nch == 1) bad |= load_x<DC>(a.X, i, a.n, a.d, 0, x);
 
-        float td[KP];
-        int ti[KP];
-        topk_init<KP>(td, ti, a.k, a.g);
-        const int off = KP - a.k;  // live slots are [off, KP)
+        float vd[KP];
+        vlist_init<KP>(vd, k);
+        int cnt = 0;
+        bool ovf = false;
+
         if (stream && tid == 0) {
-            // prefetch tiles 0 and 1 of this block's pass
             for (int b = 0; b < 2 && b < a.ntiles; ++b) {
                 mbar_expect_tx(&bars[b], tile_bytes);
                 tma_bulk_g2s(tiles + (size_t)b * tile_floats, a.Lt + (size_t)b * tile_floats, tile_bytes, &bars[b]);
@@ -158,7 +140,46 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(ScanArgs a) {
                 if (a.nch > 1) bad |= load_x<DC>(a.X, i, a.n, a.d, ch * DC, x);
                 tile_accumulate<DC>(x, tl + ch * DC * kTile, nz, acc, ch == 0);
             }
-            topk_tile<KP>(td, ti, acc, t * kTile, a.k, cbuf, tid);
+            if (!ovf) {
+                const float tau = vd[KP - 1];
+                const bool open = tau == kInf;
+                const int jb = t * kTile;
+                const int cnt0 = cnt;
+#pragma unroll
+                for (int p = 0; p < 16; ++p) {
+                    float va, vb;
+                    f2_unpack(acc[p], va, vb);
+                    const int ja = jb + 2 * p;
+                    if (va < tau || (open && ja < a.g)) {
+                        logv[cnt * kThreads + tid] = va;
+                        logj[cnt * kThreads + tid] = ja;
+                        ++cnt;
+                    }
+                    if (vb < tau || (open && ja + 1 < a.g)) {
+                        logv[cnt * kThreads + tid] = vb;
+                        logj[cnt * kThreads + tid] = ja + 1;
+                        ++cnt;
+                    }
+                }
+                for (int e = cnt0; e < cnt; ++e) {
+                    const float v = logv[e * kThreads + tid];
+                    if (v < vd[KP - 1]) vlist_insert<KP>(vd, v);
+                }
+                if (cnt > LOGCAP - kTile) {  // compact: keep what can still make the top k
+                    const float tf = vd[KP - 1];
+                    int w = 0;
+                    for (int e = 0; e < cnt; ++e) {
+                        const float v = logv[e * kThreads + tid];
+                        if (v <= tf) {
+                            logj[w * kThreads + tid] = logj[e * kThreads + tid];
+                            logv[w * kThreads + tid] = v;
+                            ++w;
+                        }
+                    }
+                    cnt = w;
+                    ovf = cnt > LOGCAP - kTile;
+                }
+            }
             if (stream) {
                 __syncthreads();  // everyone done with buffer (t & 1)
                 if (tid == 0 && t + 2 < a.ntiles) {
@@ -170,145 +191,73 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(ScanArgs a) {
                 }
             }
         }
+        if (!valid) continue;
 
-        const bool valid = i < a.n;
-        if (MODE == 0) {
-            if (valid) {
-                int32_t* oi = a.out_idx + i * a.k;
-                float* od = a.out_sqd + i * a.k;
+        // ---- final selection: rank the logged candidates by (v, j) ----
+        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+        int b0 = 0;
+        float d0 = 0.0f;
+        if (ovf) {
+            knn_point_slow(a.X + i * a.d, a.d, a.L, a.g, k, oi, od, &b0, &d0);
+        } else {
+            const float tf = vd[KP - 1];
+            int quota = k - (vlist_count_lt<KP>(vd, tf) - off);  // entries == tf still admitted
+            for (int e = 0; e < cnt; ++e) {
+                const float v = logv[e * kThreads + tid];
+                int r;
+                if (v < tf) {
+                    r = vlist_count_lt<KP>(vd, v) - off;
+                    // exact duplicates below tf: earlier-index copies rank first
+                    int le = 0;
 #pragma unroll
-                for (int q = 0; q < KP; ++q) {
-                    if (q >= off) {
-                        oi[q - off] = ti[q];
-                        od[q - off] = td[q];
+                    for (int q = 0; q < KP; ++q) le += vd[q] <= v ? 1 : 0;
+                    if (le - off - r > 1) {
+                        for (int e2 = 0; e2 < e; ++e2) r += logv[e2 * kThreads + tid] == v ? 1 : 0;
                     }
+                } else if (v == tf && quota > 0) {
+                    r = k - quota;  // ties at the k-th value: lowest indices, in log (= index) order
+                    --quota;
+                } else {
+                    continue;
+                }
+                const int j = logj[e * kThreads + tid];
+                if (oi) {
+                    oi[r] = j;
+                    od[r] = v;
+                }
+                if (r == 0) {
+                    b0 = j;
+                    d0 = v;
                 }
             }
-            continue;
         }
-
-        // ---------------- MODE 1/2: BMU statistics ----------------
-        const int k = a.k;
-        float d0 = td[KP - 1];
-        int b0 = ti[KP - 1];
-#pragma unroll
-        for (int q = KP - 1; q >= 0; --q) {
-            if (q >= off) {
-                d0 = td[q];
-                b0 = ti[q];
-            }
-        }
-        if (valid && a.qe_sum) qe_local += (double)d0;
-        if (valid && a.bmu) a.bmu[i] = b0;
-        if (valid && a.accS) {
-            const int b = b0;
-            atomicAdd(a.accC + b, 1.0);
+        if (a.bmu) a.bmu[i] = b0;
+        if (a.qe_sum) qe_local += (double)d0;
+        if (a.accS) {
+            atomicAdd(a.accC + b0, 1.0);
             if (a.nch == 1) {
 #pragma unroll
                 for (int c = 0; c < DC; ++c)
-                    if (c < a.d) atomicAdd(a.accS + (int64_t)b * a.d + c, (double)x[c]);
+                    if (c < a.d) atomicAdd(a.accS + (int64_t)b0 * a.d + c, (double)x[c]);
             } else {
-                for (int c = 0; c < a.d; ++c) atomicAdd(a.accS + (int64_t)b * a.d + c, (double)a.X[i * a.d + c]);
+                for (int c = 0; c < a.d; ++c) atomicAdd(a.accS + (int64_t)b0 * a.d + c, (double)a.X[i * a.d + c]);
             }
         }
-        if (MODE == 2) continue;
-        // ---------------- MODE 1: scores + projection ----------------
-        // scores (f64 like the reference; ref: projection.py:38-59), parked in
-        // smem with the neighbour rows: [q][kThreads], q = rank 0..k-1
-        {
-            double sigma = 0.0;
-            const double dk = (double)__fsqrt_rn(td[KP - 1]);
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                if (q >= off) {
-                    sigma += (double)__fsqrt_rn(td[q]);
-                    sj[(q - off) * kThreads + tid] = ti[q];
-                    ssq[(q - off) * kThreads + tid] = td[q];
-                }
-            }
-            sigma /= (double)k;
-            bool uniform = sigma < kScoreEps;
-            if (!uniform) {
-                const double inv = -1.0 / (2.0 * sigma * sigma);
-                const double tail = exp(dk * dk * inv);
-#pragma unroll
-                for (int q = 0; q < KP; ++q) {
-                    if (q >= off) {
-                        const double dq = (double)__fsqrt_rn(td[q]);
-                        const double v = exp(dq * dq * inv) - tail;
-                        const float sv = v > 0.0 ? (float)v : 0.0f;
-                        ssc[(q - off) * kThreads + tid] = sv;
-                        if (q == off) uniform = v < kScoreEps;
-                    }
-                }
-            }
-            if (uniform) {
-                for (int q = 0; q < k; ++q) ssc[q * kThreads + tid] = q == k - 1 ? 0.0f : 1.0f;
-            }
-        }
-        if (!valid) continue;
-        double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-        float kappa = 0.0f;
-        for (int u = 0; u + 1 < k; ++u) {
-            const float su = ssc[u * kThreads + tid];
-            if (su <= 0.0f) continue;
-            const int ju = sj[u * kThreads + tid];
-            const float squ = ssq[u * kThreads + tid];
-            const float2 lou = __ldg(reinterpret_cast<const float2*>(a.lo) + ju);
-            const float* Trow = a.T + (int64_t)ju * a.g;
-            for (int v = u + 1; v < k; ++v) {
-                const float sv = ssc[v * kThreads + tid];
-                const float wf = su * sv;
-                if (!(wf > 0.0f)) continue;
-                const int jv = sj[v * kThreads + tid];
-                const float tv = __ldg(Trow + jv);
-                if (tv < 0.0f) continue;  // hd2 < 1e-12: reference skips the pair
-                const float2 lov = __ldg(reinterpret_cast<const float2*>(a.lo) + jv);
-                const float ex = __fsub_rn(lov.x, lou.x);
-                const float ey = __fsub_rn(lov.y, lou.y);
-                const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-                if ((double)ld2 < kPairEps) continue;
-                const float sqv = ssq[v * kThreads + tid];
-                kappa = fmaxf(kappa, (squ + sqv) * tv);
-                const float r = __frcp_rn(ld2);
-                const double G1 = (double)(ex * r), G2 = (double)(ey * r);
-                const double h = fma((double)(squ - sqv), (double)tv, 0.5) + G1 * (double)lou.x + G2 * (double)lou.y;
-                const double w = (double)wf;
-                const double wg1 = w * G1, wg2 = w * G2, wh = w * h;
-                a11 = fma(wg1, G1, a11);
-                a12 = fma(wg1, G2, a12);
-                a22 = fma(wg2, G2, a22);
-                c1 = fma(wh, G1, c1);
-                c2 = fma(wh, G2, c2);
-            }
-        }
-        if (kappa > (float)(2.0 * kKappaMax))  // kappa here is (sqd_u+sqd_v)*0.5/hd2
-            pairs_exact(a.X, i, a.d, a.hi, a.lo, k, sj, ssc, tid, a11, a12, a22, c1, c2);
-        const double det = a11 * a22 - a12 * a12;
-        const double tr = a11 + a22;
-        float2 out;
-        if (det < kDetRel * tr * tr + kDetAbs) {
-            out = __ldg(reinterpret_cast<const float2*>(a.lo) + b0);
-        } else {
-            out.x = (float)((c1 * a22 - c2 * a12) / det);
-            out.y = (float)((a11 * c2 - a12 * c1) / det);
-        }
-        reinterpret_cast<float2*>(a.xy)[i] = out;
     }
     flag_nonfinite(a.flag, bad);
-    if (MODE != 0 && a.qe_sum) {
+    if (a.qe_sum) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) qe_local += __shfl_xor_sync(0xffffffffu, qe_local, o);
         if ((tid & 31) == 0 && qe_local != 0.0) atomicAdd(a.qe_sum, qe_local);
     }
 }
 
-
-template <int DC, int KP, int MODE>
+template <int DC, int KP>
 int launch_scan_t(ScanArgs a, cudaStream_t st) {
+    constexpr int LOGCAP = KP + kTile;
     const size_t tile_bytes = (size_t)a.dp * kTile * 4;
-    size_t extra = (size_t)kTile * kThreads * 4;
-    if (MODE == 1 && (size_t)KP * kThreads * 12 > extra) extra = (size_t)KP * kThreads * 12;
+    const size_t extra = (size_t)LOGCAP * kThreads * 8;
     const size_t cap = (size_t)esom_host::max_smem_optin() - 2048;
     size_t smem;
     if ((size_t)a.ntiles * tile_bytes + extra <= cap && (size_t)a.ntiles * tile_bytes <= esom_host::resident_limit()) {
@@ -319,7 +268,7 @@ int launch_scan_t(ScanArgs a, cudaStream_t st) {
         smem = 2 * tile_bytes + extra;
         if (smem > cap) return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "dimension too large for smem tiles%s", "");
     }
-    auto kern = scan_kernel<DC, KP, MODE>;
+    auto kern = knn_scan_kernel<DC, KP>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
@@ -329,8 +278,7 @@ int launch_scan_t(ScanArgs a, cudaStream_t st) {
     if (grid > nblk) grid = nblk;
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
-    return esom_host::cuda_check("scan_kernel");
+    return esom_host::cuda_check("knn_scan_kernel");
 }
-
 
 }  // namespace esom

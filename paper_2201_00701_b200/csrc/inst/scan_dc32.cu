@@ -1,0 +1,9 @@
+// generated: explicit instantiations of the k-NN scan kernel
+#include "../esom_scan.cuh"
+namespace esom {
+template int launch_scan_t<32, 4>(ScanArgs, cudaStream_t);
+template int launch_scan_t<32, 8>(ScanArgs, cudaStream_t);
+template int launch_scan_t<32, 16>(ScanArgs, cudaStream_t);
+template int launch_scan_t<32, 32>(ScanArgs, cudaStream_t);
+template int launch_scan_t<32, 64>(ScanArgs, cudaStream_t);
+}

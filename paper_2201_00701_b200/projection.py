@@ -168,14 +168,23 @@ class PreparedModel:
                       self.ws.numel(), _dev.ptr(self.flag), _dev.stream_handle(dev))
         return self
 
+    def point_workspace(self, n: int) -> torch.Tensor:
+        nbytes = _lib.load().esom_point_workspace_bytes(n, self.k)
+        pws = getattr(self, "pws", None)
+        if pws is None or pws.numel() < nbytes:
+            self.pws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.pws
+
     def embed_into(self, X: torch.Tensor, xy: torch.Tensor, *, bmu=None, acc_S=None, acc_C=None, qe_sum=None,
                    flag=None, stream=None) -> None:
-        """Asynchronous fused embed of device points X (n×d f32) into xy (n×2 f32)."""
+        """Asynchronous embed of device points X (n×d f32) into xy (n×2 f32):
+        k-NN scan + projection kernels per L2-resident chunk."""
         n, d = X.shape
         st = stream if stream is not None else _dev.stream_handle(self.device)
+        pws = self.point_workspace(n)
         _lib.call("esom_embed_prepared", _dev.ptr(X), n, d, _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.k,
-                  _dev.ptr(self.ws), _dev.ptr(xy), _dev.ptr(bmu), _dev.ptr(acc_S), _dev.ptr(acc_C), _dev.ptr(qe_sum),
-                  _dev.ptr(flag if flag is not None else self.flag), st)
+                  _dev.ptr(self.ws), _dev.ptr(pws), pws.numel(), _dev.ptr(xy), _dev.ptr(bmu), _dev.ptr(acc_S),
+                  _dev.ptr(acc_C), _dev.ptr(qe_sum), _dev.ptr(flag if flag is not None else self.flag), st)
 
 
 def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_size: int | None = None,
