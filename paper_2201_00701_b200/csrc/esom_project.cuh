@@ -22,20 +22,15 @@
 
 namespace esom {
 
-// threads per CTA: 256 for k <= 16 (per-thread rows fit next to a smem pair
-// table), fewer for larger k so the per-thread rows still fit
+// threads per CTA: 384 for k <= 16 (per-thread rows fit next to a smem pair
+// table of g <= 256), fewer for larger k so the per-thread rows still fit
 template <int KP>
-__host__ __device__ constexpr int proj_threads() { return KP <= 16 ? 256 : (KP <= 32 ? 128 : 64); }
-
-__device__ __forceinline__ int64_t tri_index(int a, int b, int g) {
-    // a < b; row a holds pairs (a, a+1..g-1)
-    return (int64_t)a * (2 * (int64_t)g - a - 1) / 2 + (b - a - 1);
-}
+__host__ __device__ constexpr int proj_threads() { return KP <= 16 ? 384 : (KP <= 32 ? 256 : 128); }
 
 // Exact f64 pair accumulation from x and the landmark rows (outlier path).
 static __device__ __noinline__ void pairs_exact_f64(const float* __restrict__ x, int d,
                                                     const float* __restrict__ hi, const float* __restrict__ lo,
-                                                    int k, const int* J, const double* S, int stride, double* out5) {
+                                                    int k, const int* J, const float* S, int stride, double* out5) {
     double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
     for (int u = 0; u < k; ++u) {
         const double su = S[u * stride];
@@ -43,7 +38,7 @@ static __device__ __noinline__ void pairs_exact_f64(const float* __restrict__ x,
         const int ju = J[u * stride];
         const float* hu = hi + (int64_t)ju * d;
         for (int v = u + 1; v < k; ++v) {
-            const double w = su * S[v * stride];
+            const double w = su * (double)S[v * stride];
             if (!(w > 0.0)) continue;
             const int jv = J[v * stride];
             const float* hv = hi + (int64_t)jv * d;
@@ -56,10 +51,11 @@ static __device__ __noinline__ void pairs_exact_f64(const float* __restrict__ x,
                 dnum = fma((double)x[c] - (double)hu[c], e, dnum);
             }
             if (hd2f < kPairEps) continue;
-            const double ex = (double)lo[2 * jv] - (double)lo[2 * ju];
-            const double ey = (double)lo[2 * jv + 1] - (double)lo[2 * ju + 1];
-            const double ld2 = ex * ex + ey * ey;
-            if (ld2 < kPairEps) continue;
+            const float exf = __fsub_rn(lo[2 * jv], lo[2 * ju]);
+            const float eyf = __fsub_rn(lo[2 * jv + 1], lo[2 * ju + 1]);
+            const float ld2f = __fadd_rn(__fmul_rn(exf, exf), __fmul_rn(eyf, eyf));
+            if ((double)ld2f < kPairEps) continue;
+            const double ex = exf, ey = eyf, ld2 = (double)ld2f;
             const double g1 = ex / ld2, g2 = ey / ld2;
             const double h = dnum / hd2 + g1 * (double)lo[2 * ju] + g2 * (double)lo[2 * ju + 1];
             const double wg1 = w * g1, wg2 = w * g2, wh = w * h;
@@ -77,40 +73,49 @@ static __device__ __noinline__ void pairs_exact_f64(const float* __restrict__ x,
     out5[4] = c2;
 }
 
+// smallest f32 value v with (double)v >= 1e-12: ld2 (f32, as the reference
+// computes it) is skipped iff ld2 < kLd2Min  (ref: projection.py:346)
+constexpr float kLd2Min = 1.000000104e-12f;  // 0x2b8cbccd
+
 template <int KP>
 __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjArgs a) {
-    constexpr int kProjThreads = proj_threads<KP>();
+    constexpr int PT = proj_threads<KP>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
-    // layout: lo64 [g] double2 | J [KP][T] int | Q [KP][T] double | S [KP][T] double | (T table)
-    double2* lo64 = reinterpret_cast<double2*>(smem_raw);
-    int* J = reinterpret_cast<int*>(lo64 + g);
-    double* Q = reinterpret_cast<double*>(J + KP * kProjThreads);
-    double* S = Q + KP * kProjThreads;
+    // layout: lo [g] float2 | RB [g] int | J [KP][PT] int | S [KP][PT] f32 | Q [KP][PT] f32 | (T table)
+    float2* LO = reinterpret_cast<float2*>(smem_raw);
+    int* RB = reinterpret_cast<int*>(LO + g);
+    int* J = RB + g;
+    float* S = reinterpret_cast<float*>(J + KP * PT);
+    float* Q = S + KP * PT;
     const float* Ts = a.T;
     if (a.t_smem) {
-        float* tsm = reinterpret_cast<float*>(S + KP * kProjThreads);
-        const int64_t ntri = (int64_t)g * (g - 1) / 2;
-        for (int64_t e = tid; e < ntri; e += kProjThreads) tsm[e] = a.T[e];
+        float* tsm = Q + KP * PT;
+        const int ntri = g * (g - 1) / 2;
+        const float4* src = reinterpret_cast<const float4*>(a.T);
+        float4* dst = reinterpret_cast<float4*>(tsm);
+        for (int e = tid; e < ntri / 4; e += PT) dst[e] = src[e];
+        for (int e = (ntri / 4) * 4 + tid; e < ntri; e += PT) tsm[e] = a.T[e];
         Ts = tsm;
     }
-    for (int j = tid; j < g; j += kProjThreads)
-        lo64[j] = make_double2((double)a.lo[2 * j], (double)a.lo[2 * j + 1]);
+    for (int j = tid; j < g; j += PT) {
+        LO[j] = make_float2(a.lo[2 * j], a.lo[2 * j + 1]);
+        RB[j] = j * (2 * g - j - 1) / 2 - j - 1;  // tri(j, b) = RB[j] + b for b > j
+    }
     __syncthreads();
 
-    for (int64_t i = blockIdx.x * (int64_t)kProjThreads + tid; i < a.n; i += (int64_t)gridDim.x * kProjThreads) {
+    for (int64_t i = blockIdx.x * (int64_t)PT + tid; i < a.n; i += (int64_t)gridDim.x * PT) {
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
-        // scores (f64; ref: projection.py:38-59)
+        // scores (f64 like the reference; ref: projection.py:38-59), parked as f32 weights
         double sigma = 0.0, dk = 0.0;
         for (int q = 0; q < k; ++q) {
             const float sq = __ldg(drow + q);
             const double dq = (double)__fsqrt_rn(sq);
             sigma += dq;
-            J[q * kProjThreads + tid] = __ldg(irow + q);
-            Q[q * kProjThreads + tid] = (double)sq;
-            S[q * kProjThreads + tid] = dq;  // distances for now
+            J[q * PT + tid] = __ldg(irow + q);
+            Q[q * PT + tid] = sq;
             dk = dq;
         }
         sigma /= (double)k;
@@ -119,39 +124,43 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
             const double inv = -1.0 / (2.0 * sigma * sigma);
             const double tail = exp(dk * dk * inv);
             for (int q = 0; q < k; ++q) {
-                const double dq = S[q * kProjThreads + tid];
+                const double dq = (double)__fsqrt_rn(Q[q * PT + tid]);
                 const double v = exp(dq * dq * inv) - tail;
-                S[q * kProjThreads + tid] = v > 0.0 ? v : 0.0;
+                S[q * PT + tid] = v > 0.0 ? (float)v : 0.0f;
                 if (q == 0) uniform = v < kScoreEps;
             }
         }
         if (uniform)
-            for (int q = 0; q < k; ++q) S[q * kProjThreads + tid] = q == k - 1 ? 0.0 : 1.0;
+            for (int q = 0; q < k; ++q) S[q * PT + tid] = q == k - 1 ? 0.0f : 1.0f;
 
         double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-        double kappa = 0.0;
+        float kappa = 0.0f;
         for (int u = 0; u + 1 < k; ++u) {
-            const double su = S[u * kProjThreads + tid];
-            if (!(su > 0.0)) continue;
-            const int ju = J[u * kProjThreads + tid];
-            const double squ = Q[u * kProjThreads + tid];
-            const double2 lu = lo64[ju];
+            const float su = S[u * PT + tid];
+            if (!(su > 0.0f)) continue;
+            const int ju = J[u * PT + tid];
+            const float squ = Q[u * PT + tid];
+            const float2 lu = LO[ju];
+            const int rbu = RB[ju];
+            const double lux = lu.x, luy = lu.y;
+#pragma unroll 2
             for (int v = u + 1; v < k; ++v) {
-                const double w = su * S[v * kProjThreads + tid];
-                if (!(w > 0.0)) continue;
-                const int jv = J[v * kProjThreads + tid];
-                const float tv = ju < jv ? Ts[tri_index(ju, jv, g)] : Ts[tri_index(jv, ju, g)];
-                if (tv < 0.0f) continue;  // hd2 < 1e-12: the reference skips the pair
-                const double2 lv = lo64[jv];
-                const double ex = lv.x - lu.x, ey = lv.y - lu.y;
-                const double ld2 = fma(ex, ex, ey * ey);
-                if (ld2 < kPairEps) continue;
-                const double t = (double)tv;
-                const double sqv = Q[v * kProjThreads + tid];
-                kappa = fmax(kappa, (squ + sqv) * t);
-                const double r = __drcp_rn(ld2);
-                const double g1 = ex * r, g2 = ey * r;
-                const double h = fma(squ - sqv, t, 0.5) + fma(g1, lu.x, g2 * lu.y);
+                const float sv = S[v * PT + tid];
+                const int jv = J[v * PT + tid];
+                const float sqv = Q[v * PT + tid];
+                const int ti = ju < jv ? rbu + jv : RB[jv] + ju;
+                const float tv = Ts[ti];
+                const float2 lv = LO[jv];
+                // layout terms in f32 exactly as the reference forms them (ref: projection.py:341-348)
+                const float ex = __fsub_rn(lv.x, lu.x), ey = __fsub_rn(lv.y, lu.y);
+                const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+                const bool keep = (su * sv > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
+                kappa = keep ? fmaxf(kappa, (squ + sqv) * tv) : kappa;
+                const double w = keep ? (double)(su * sv) : 0.0;
+                const double r = keep ? 1.0 / (double)ld2 : 0.0;
+                const double g1 = (double)ex * r, g2 = (double)ey * r;
+                // dnum/hd2 by the law of cosines + g . lo_u  (f64 like the reference's h)
+                const double h = 0.5 + (double)((squ - sqv) * tv) + fma(g1, lux, g2 * luy);
                 const double wg1 = w * g1, wg2 = w * g2, wh = w * h;
                 a11 = fma(wg1, g1, a11);
                 a12 = fma(wg1, g2, a12);
@@ -160,9 +169,9 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
                 c2 = fma(wh, g2, c2);
             }
         }
-        if (kappa > kKappaMax) {
+        if (kappa > (float)kKappaMax) {
             double o5[5];
-            pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, J + tid, S + tid, kProjThreads, o5);
+            pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, J + tid, S + tid, PT, o5);
             a11 = o5[0];
             a12 = o5[1];
             a22 = o5[2];
@@ -173,8 +182,7 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         const double tr = a11 + a22;
         float2 out;
         if (det < kDetRel * tr * tr + kDetAbs) {
-            const int j0 = J[tid];
-            out = make_float2(a.lo[2 * j0], a.lo[2 * j0 + 1]);
+            out = LO[J[tid]];
         } else {
             out.x = (float)((c1 * a22 - c2 * a12) / det);
             out.y = (float)((a11 * c2 - a12 * c1) / det);
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
 template <int KP>
 int launch_project_t(ProjArgs a, cudaStream_t st) {
     constexpr int kProjThreads = proj_threads<KP>();
-    const size_t base = (size_t)a.g * 16 + (size_t)KP * kProjThreads * (4 + 8 + 8);
+    const size_t base = (size_t)a.g * 12 + (size_t)KP * kProjThreads * 12 + 64;
     const size_t tbytes = (size_t)a.g * (a.g - 1) / 2 * 4;
     const size_t cap = (size_t)esom_host::max_smem_optin() - 1024;
     if (base > cap) return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "g too large for the projection kernel%s", "");

@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
     const uint32_t tile_bytes = (uint32_t)tile_floats * 4u;
     const int nbuf = a.res_tiles ? a.res_tiles : 2;
     float* tiles = reinterpret_cast<float*>(smem_raw);
-    float* logv = tiles + (size_t)nbuf * tile_floats;            // [LOGCAP][kThreads]
-    int* logj = reinterpret_cast<int*>(logv + LOGCAP * kThreads);  // [LOGCAP][kThreads]
+    float* logv = tiles + (size_t)nbuf * tile_floats;                                // [LOGCAP][kThreads]
+    unsigned short* logj = reinterpret_cast<unsigned short*>(logv + LOGCAP * kThreads);  // [LOGCAP][kThreads], g < 65536
 
     const f2 nz = f2_pack(a.nz, a.nz);
     const bool stream = a.res_tiles == 0;
@@ -152,12 +152,12 @@ __global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
                     const int ja = jb + 2 * p;
                     if (va < tau || (open && ja < a.g)) {
                         logv[cnt * kThreads + tid] = va;
-                        logj[cnt * kThreads + tid] = ja;
+                        logj[cnt * kThreads + tid] = (unsigned short)ja;
                         ++cnt;
                     }
                     if (vb < tau || (open && ja + 1 < a.g)) {
                         logv[cnt * kThreads + tid] = vb;
-                        logj[cnt * kThreads + tid] = ja + 1;
+                        logj[cnt * kThreads + tid] = (unsigned short)(ja + 1);
                         ++cnt;
                     }
                 }
@@ -198,9 +198,8 @@ __global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
         float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
         int b0 = 0;
         float d0 = 0.0f;
-        if (ovf) {
-            knn_point_slow(a.X + i * a.d, a.d, a.L, a.g, k, oi, od, &b0, &d0);
-        } else {
+        int written = 0;
+        if (!ovf) {
             const float tf = vd[KP - 1];
             int quota = k - (vlist_count_lt<KP>(vd, tf) - off);  // entries == tf still admitted
             for (int e = 0; e < cnt; ++e) {
@@ -230,8 +229,13 @@ __global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
                     b0 = j;
                     d0 = v;
                 }
+                ++written;
             }
         }
+        // log overflow (pathological ties) or NaN inputs (flagged as
+        // non-finite; rows must still hold valid indices): the reference's
+        // own insertion scan for this point
+        if (ovf || written != k) knn_point_slow(a.X + i * a.d, a.d, a.L, a.g, k, oi, od, &b0, &d0);
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         if (a.accS) {
@@ -257,7 +261,8 @@ template <int DC, int KP>
 int launch_scan_t(ScanArgs a, cudaStream_t st) {
     constexpr int LOGCAP = KP + kTile;
     const size_t tile_bytes = (size_t)a.dp * kTile * 4;
-    const size_t extra = (size_t)LOGCAP * kThreads * 8;
+    const size_t extra = (size_t)LOGCAP * kThreads * 6;
+    if (a.g >= 65536) return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "g >= 65536 unsupported by the scan kernel%s", "");
     const size_t cap = (size_t)esom_host::max_smem_optin() - 2048;
     size_t smem;
     if ((size_t)a.ntiles * tile_bytes + extra <= cap && (size_t)a.ntiles * tile_bytes <= esom_host::resident_limit()) {
