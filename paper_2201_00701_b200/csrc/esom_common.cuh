@@ -10,6 +10,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cuda_bf16.h>
 
 #define ESOM_OK 0
 #define ESOM_ERR_PARAM 1

@@ -135,6 +135,45 @@ __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, fl
     }
 }
 
+// Tensor-core operands of the landmarks (esom_tc.cuh): split bf16 hi/lo in
+// the canonical K-major layout (gpad rows x d16, zero padded), |l_j|^2
+// (+inf on padding rows) and max |l_j|, max |l_j|^2 for the error bound.
+__global__ void tc_prepare_kernel(const float* __restrict__ hi, int g, int d, int d16, int gpad,
+                                  uint16_t* __restrict__ Bhi, uint16_t* __restrict__ Blo, float* __restrict__ ln,
+                                  float* __restrict__ lstats) {
+    const int chunks = d16 / 8;
+    const int64_t total = (int64_t)gpad * chunks;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int row = (int)(e / chunks), c0 = (int)(e % chunks) * 8;
+        uint32_t hw[4], lw[4];
+        for (int q = 0; q < 8; q += 2) {
+            const float v0 = (row < g && c0 + q < d) ? hi[(int64_t)row * d + c0 + q] : 0.0f;
+            const float v1 = (row < g && c0 + q + 1 < d) ? hi[(int64_t)row * d + c0 + q + 1] : 0.0f;
+            const uint16_t h0 = __bfloat16_as_ushort(__float2bfloat16_rn(v0));
+            const uint16_t h1 = __bfloat16_as_ushort(__float2bfloat16_rn(v1));
+            const uint16_t l0 = __bfloat16_as_ushort(__float2bfloat16_rn(v0 - __bfloat162float(__ushort_as_bfloat16(h0))));
+            const uint16_t l1 = __bfloat16_as_ushort(__float2bfloat16_rn(v1 - __bfloat162float(__ushort_as_bfloat16(h1))));
+            hw[q >> 1] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+            lw[q >> 1] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+        }
+        const int64_t off = (((int64_t)(row >> 3) * chunks + (c0 >> 3)) << 6) + ((row & 7) << 3);  // in uint16
+        *reinterpret_cast<uint4*>(Bhi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(Blo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        if (c0 == 0) {
+            if (row < g) {
+                double s = 0.0;
+                for (int c = 0; c < d; ++c) s = fma((double)hi[(int64_t)row * d + c], (double)hi[(int64_t)row * d + c], s);
+                const float lnf = (float)(s * (1.0 + 1e-7));
+                ln[row] = lnf;
+                atomicMax(reinterpret_cast<int*>(lstats), __float_as_int((float)(sqrt(s) * (1.0 + 1e-7))));
+                atomicMax(reinterpret_cast<int*>(lstats + 1), __float_as_int(lnf));
+            } else {
+                ln[row] = __int_as_float(0x7f800000);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Scores (ref: projection.py:38-59).  numba's float(f32) stays f32, so the
 // root is sqrtf, widened; the rest is f64.  `exp` is CUDA's (<= 1 ulp from
@@ -509,6 +548,94 @@ int grid_for(int64_t work, int threads) {
     return (int)b;
 }
 
+struct ModelLayout {
+    size_t lt, tri, bhi, blo, ln, lstats, total;
+    int d16, gpad;
+};
+
+size_t a256(size_t b) { return (b + 255) / 256 * 256; }
+
+ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
+    const Plan p = make_plan(d, g, k < 1 ? 1 : k);
+    ModelLayout m{};
+    m.d16 = (d + 15) / 16 * 16;
+    m.gpad = (g + 31) / 32 * 32;
+    size_t o = 0;
+    m.lt = o;
+    o += a256((size_t)p.ntiles * p.tile_bytes);
+    m.tri = o;
+    if (with_pairs) o += a256((size_t)g * (g > 1 ? g - 1 : 1) / 2 * 4);
+    m.bhi = o;
+    o += a256((size_t)m.gpad * m.d16 * 2);
+    m.blo = o;
+    o += a256((size_t)m.gpad * m.d16 * 2);
+    m.ln = o;
+    o += a256((size_t)m.gpad * 4);
+    m.lstats = o;
+    o += 256;
+    m.total = o + 256;
+    return m;
+}
+
+bool tc_enabled() {  // ESOM_TC=0 forces the CUDA-core scan (read per call: tests toggle it)
+    const char* e = getenv("ESOM_TC");
+    return e ? atoi(e) != 0 : true;
+}
+
+// shapes the split-bf16 tensor-core screen handles (smem budget of esom_tc.cuh)
+bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1024 && d <= 32 && g <= 256 && k <= 16; }
+
+int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cudaStream_t st) {
+    cudaMemsetAsync(ws + m.lstats, 0, 8, st);
+    tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
+        hi, g, d, m.d16, m.gpad, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
+        reinterpret_cast<float*>(ws + m.ln), reinterpret_cast<float*>(ws + m.lstats));
+    return cuda_check("tc_prepare_kernel");
+}
+
+// returns ESOM_ERR_UNSUPPORTED when the shape does not fit (caller falls back)
+int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st) {
+    TcArgs a{};
+    a.X = s.X;
+    a.n = s.n;
+    a.d = s.d;
+    a.d16 = m.d16;
+    a.dp = p.dp;
+    a.g = s.g;
+    a.gpad = m.gpad;
+    a.k = s.k;
+    a.Bhi = reinterpret_cast<const uint16_t*>(ws + m.bhi);
+    a.Blo = reinterpret_cast<const uint16_t*>(ws + m.blo);
+    a.ln = reinterpret_cast<const float*>(ws + m.ln);
+    a.Lt = reinterpret_cast<const float*>(ws + m.lt);
+    a.L = s.L;
+    a.lstats = reinterpret_cast<const float*>(ws + m.lstats);
+    a.out_idx = s.out_idx;
+    a.out_sqd = s.out_sqd;
+    a.bmu = s.bmu;
+    a.accS = s.accS;
+    a.accC = s.accC;
+    a.qe_sum = s.qe_sum;
+    a.flag = s.flag;
+    a.stats = nullptr;
+    switch (p.kp) {
+        case 4: return launch_tc_t<4>(a, st);
+        case 8: return launch_tc_t<8>(a, st);
+        case 16: return launch_tc_t<16>(a, st);
+    }
+    return set_err(ESOM_ERR_UNSUPPORTED, "no tensor-core kernel for k%s", "");
+}
+
+// k-NN over a prepared model workspace: tensor-core screen when eligible, else the CUDA-core scan
+int run_knn(const Plan& p, const ModelLayout& m, ScanArgs a, const char* ws, cudaStream_t st) {
+    if (tc_eligible(a.n, a.d, a.g, a.k)) {
+        const int e = dispatch_tc(p, m, a, ws, st);
+        if (e != ESOM_ERR_UNSUPPORTED) return e;
+    }
+    return dispatch_scan(p, a, st);
+}
+
+
 }  // namespace
 
 // ===========================================================================
@@ -523,10 +650,7 @@ const char* esom_last_error(void) { return g_err; }
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs) {
-    const Plan p = make_plan(d, g, k < 1 ? 1 : k);
-    size_t bytes = align256((size_t)p.ntiles * p.tile_bytes);
-    if (with_pairs) bytes += align256((size_t)g * (g > 1 ? g - 1 : 1) / 2 * 4);
-    return bytes + 256;
+    return model_layout(g, d, k, with_pairs != 0).total;
 }
 
 // points per embed chunk: the chunk's neighbour rows stay L2-resident between
@@ -578,15 +702,19 @@ int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, in
         return cuda_check("check_finite");
     }
     const Plan p = make_plan(d, g, k);
-    if (ws_bytes < esom_workspace_bytes(g, d, k, 0)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
-    float* Lt = reinterpret_cast<float*>(workspace);
+    const ModelLayout m = model_layout(g, d, k, false);
+    if (ws_bytes < m.total) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    char* ws = reinterpret_cast<char*>(workspace);
+    float* Lt = reinterpret_cast<float*>(ws + m.lt);
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(L, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
+    if (tc_eligible(n, d, g, k))
+        if (int e = prepare_tc(L, g, d, m, ws, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, L, g, k, Lt, nonfinite_flag);
     a.out_idx = idx;
     a.out_sqd = sqd;
-    return dispatch_scan(p, a, stream);
+    return run_knn(p, m, a, ws, stream);
 }
 
 int esom_scores(const float* sqd, int64_t n, int32_t k, double* out, cudaStream_t stream) {
@@ -609,14 +737,19 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
                        int32_t* nonfinite_flag, cudaStream_t stream) {
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64 (got %lld)%s", "", k);
     const Plan p = make_plan(d, g, k);
-    if (ws_bytes < esom_workspace_bytes(g, d, k, 1)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
-    float* Lt = reinterpret_cast<float*>(workspace);
-    float* T = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align256((size_t)p.ntiles * p.tile_bytes));
+    const ModelLayout m = model_layout(g, d, k, true);
+    if (ws_bytes < m.total) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    char* ws = reinterpret_cast<char*>(workspace);
+    float* Lt = reinterpret_cast<float*>(ws + m.lt);
+    float* T = reinterpret_cast<float*>(ws + m.tri);
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
     pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T);
-    return cuda_check("pair_table");
+    if (int e = cuda_check("pair_table")) return e;
+    if (tc_eligible(1 << 20, d, g, k))
+        if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
+    return ESOM_OK;
 }
 
 int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
@@ -628,9 +761,10 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
     if (point_ws_bytes < esom_point_workspace_bytes(n, k))
         return set_err(ESOM_ERR_PARAM, "point workspace too small%s", "");
     const Plan p = make_plan(d, g, k);
-    const float* Lt = reinterpret_cast<const float*>(model_ws);
-    const float* T = reinterpret_cast<const float*>(reinterpret_cast<const char*>(model_ws) +
-                                                    align256((size_t)p.ntiles * p.tile_bytes));
+    const ModelLayout ml = model_layout(g, d, k, true);
+    const char* mws = reinterpret_cast<const char*>(model_ws);
+    const float* Lt = reinterpret_cast<const float*>(mws + ml.lt);
+    const float* T = reinterpret_cast<const float*>(mws + ml.tri);
     const int64_t chunk = n < embed_chunk(k) ? n : embed_chunk(k);
     int32_t* idx = reinterpret_cast<int32_t*>(point_ws);
     float* sqd = reinterpret_cast<float*>(reinterpret_cast<char*>(point_ws) + align256((size_t)chunk * k * 4));
@@ -643,7 +777,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         a.accS = acc_S;
         a.accC = acc_C;
         a.qe_sum = qe_sum;
-        if (int e = dispatch_scan(p, a, stream)) return e;
+        if (int e = run_knn(p, ml, a, mws, stream)) return e;
         ProjArgs q{};
         q.idx = idx;
         q.sqd = sqd;
@@ -682,17 +816,21 @@ int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, i
     if (n < 0 || d < 1 || g < 1) return set_err(ESOM_ERR_PARAM, "bad shape%s", "");
     if (n == 0) return ESOM_OK;
     const Plan p = make_plan(d, g, 1);
-    if (ws_bytes < esom_workspace_bytes(g, d, 1, 0)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
-    float* Lt = reinterpret_cast<float*>(workspace);
+    const ModelLayout m = model_layout(g, d, 1, false);
+    if (ws_bytes < m.total) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    char* ws = reinterpret_cast<char*>(workspace);
+    float* Lt = reinterpret_cast<float*>(ws + m.lt);
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
+    if (tc_eligible(n, d, g, 1))
+        if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, hi, g, 1, Lt, nonfinite_flag);
     a.bmu = bmu;
     a.accS = acc_S;
     a.accC = acc_C;
     a.qe_sum = qe_sum;
-    return dispatch_scan(p, a, stream);
+    return run_knn(p, m, a, ws, stream);
 }
 
 size_t esom_tick_workspace_bytes(int32_t g, int32_t d) { return (size_t)g * d * 8 + 256; }

@@ -37,6 +37,31 @@ struct ProjArgs {
     int d;
 };
 
+// tensor-core screened k-NN (esom_tc.cuh)
+struct TcArgs {
+    const float* X;          // n×d points
+    int64_t n;
+    int d, d16, dp;          // dims, dims padded to 16 (MMA K), dims of the exact tiles
+    int g, gpad, k;          // landmarks, landmarks padded to 32
+    const uint16_t* Bhi;     // gpad × d16 bf16, canonical K-major layout
+    const uint16_t* Blo;
+    const float* ln;         // gpad |l_j|^2 (f32; +inf for padding rows)
+    const float* Lt;         // exact tiles [tile][dp][32]
+    const float* L;          // row-major landmarks (slow path)
+    const float* lstats;     // [0] = max_j |l_j|, [1] = max_j |l_j|^2 (device)
+    int32_t* out_idx;
+    float* out_sqd;
+    int32_t* bmu;
+    double* accS;
+    double* accC;
+    double* qe_sum;
+    int32_t* flag;
+    int32_t* stats;          // [0] += candidates examined exactly (diagnostic, nullable)
+};
+
+template <int KP>
+int launch_tc_t(TcArgs a, cudaStream_t st);  // esom_tc.cuh, instantiated in inst/tc.cu
+
 template <int DC, int KP>
 int launch_scan_t(ScanArgs a, cudaStream_t st);   // esom_scan.cuh, instantiated in inst/*.cu
 

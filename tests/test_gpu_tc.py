@@ -1,0 +1,75 @@
+"""Tensor-core screened k-NN (esom_tc.cuh): bit-identical to the CUDA-core
+scan and to the reference oracle, including ties, on every eligible shape."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import c1_inputs, c2_inputs
+from oracle import oracle
+import paper_2201_00701_b200 as esom
+
+pytestmark = pytest.mark.gpu
+
+
+def run(p, l, k, tc):
+    old = os.environ.get("ESOM_TC")
+    os.environ["ESOM_TC"] = "1" if tc else "0"
+    try:
+        nb = esom.knn_base(p, l, k)
+    finally:
+        if old is None:
+            del os.environ["ESOM_TC"]
+        else:
+            os.environ["ESOM_TC"] = old
+    return nb
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "uniform16", "normal32", "ties", "wide"])
+def test_tc_equals_scan_and_oracle(case):
+    gen = np.random.default_rng(hash(case) % 2**32)
+    if case == "c1":
+        p, l, _ = c1_inputs()
+        k = 8
+    elif case == "c2":
+        p, l, _ = c2_inputs()
+        p = p[: 1 << 17]
+        k = 16
+    elif case == "uniform16":
+        p = gen.random((20000, 16)).astype(np.float32)
+        l = gen.random((200, 16)).astype(np.float32)
+        k = 16
+    elif case == "normal32":
+        p = (gen.normal(size=(20000, 32)) * 30 + 100).astype(np.float32)  # far from the origin
+        l = (gen.normal(size=(256, 32)) * 30 + 100).astype(np.float32)
+        k = 16
+    elif case == "ties":
+        p = gen.integers(0, 3, size=(20000, 8)).astype(np.float32)
+        l = gen.integers(0, 3, size=(128, 8)).astype(np.float32)
+        k = 16
+    else:
+        p = gen.normal(size=(5000, 5)).astype(np.float32) * np.float32(1e3)
+        l = gen.normal(size=(37, 5)).astype(np.float32)
+        k = 4
+    a = run(p, l, k, tc=True)
+    b = run(p, l, k, tc=False)
+    assert np.array_equal(a.indices, b.indices) and np.array_equal(a.sqdists, b.sqdists), case
+    rows = np.arange(0, p.shape[0], max(1, p.shape[0] // 4000))
+    wi, wd = oracle.knn(p[rows], l, k)
+    assert np.array_equal(a.indices[rows], wi) and np.array_equal(a.sqdists[rows], wd), case
+
+
+def test_tc_embed_and_stats_match_scan():
+    p, hi, lo = c2_inputs()
+    X = torch.from_numpy(p[: 1 << 18]).cuda()
+    model = esom.LandmarkModel.create(hi, lo)
+    os.environ["ESOM_TC"] = "1"
+    xa = esom.embed(X, model, esom.EmbedParams(k=16))
+    qa = esom.quantization_error(X, hi)
+    os.environ["ESOM_TC"] = "0"
+    xb = esom.embed(X, model, esom.EmbedParams(k=16))
+    qb = esom.quantization_error(X, hi)
+    del os.environ["ESOM_TC"]
+    assert torch.equal(xa, xb)
+    assert qa == pytest.approx(qb, rel=1e-12)
