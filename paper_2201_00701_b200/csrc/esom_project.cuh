@@ -191,8 +191,149 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
     }
 }
 
+// ---------------------------------------------------------------------------
+// k <= 16: the whole per-point state lives in registers and the k(k-1)/2 pair
+// loop is fully unrolled (static register indexing; no per-pair shared
+// loads except the pair-table entry).  Same arithmetic as above.
+// ---------------------------------------------------------------------------
+template <int KP, bool TSMEM>
+__global__ void __launch_bounds__(384) project_reg_kernel(ProjArgs a) {
+    constexpr int PT = 384;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int g = a.g, k = a.k;
+    float2* LO = reinterpret_cast<float2*>(smem_raw);
+    int* RB = reinterpret_cast<int*>(LO + g);
+    float* tsm = reinterpret_cast<float*>(RB + g + ((g & 1) ? 1 : 0));
+    if (TSMEM) {
+        const int ntri = g * (g - 1) / 2;
+        for (int e = tid; e < ntri; e += PT) tsm[e] = __ldg(a.T + e);
+    }
+    for (int j = tid; j < g; j += PT) {
+        LO[j] = make_float2(a.lo[2 * j], a.lo[2 * j + 1]);
+        RB[j] = j * (2 * g - j - 1) / 2 - j - 1;
+    }
+    __syncthreads();
+    const float* T = TSMEM ? tsm : a.T;
+
+    for (int64_t i = blockIdx.x * (int64_t)PT + tid; i < a.n; i += (int64_t)gridDim.x * PT) {
+        int jj[KP], rb[KP];
+        float sq[KP], sc[KP], lx[KP], ly[KP];
+        const int32_t* irow = a.idx + i * k;
+        const float* drow = a.sqd + i * k;
+        double sigma = 0.0;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            if (q < k) {
+                jj[q] = __ldg(irow + q);
+                sq[q] = __ldg(drow + q);
+            } else {
+                jj[q] = 0;
+                sq[q] = 0.0f;
+            }
+            const float2 l = LO[jj[q]];
+            lx[q] = l.x;
+            ly[q] = l.y;
+            rb[q] = RB[jj[q]];
+            if (q < k) sigma += (double)__fsqrt_rn(sq[q]);
+        }
+        // scores (f64 like the reference; ref: projection.py:38-59)
+        sigma /= (double)k;
+        bool uniform = sigma < kScoreEps;
+        double dk = 0.0;
+#pragma unroll
+        for (int q = 0; q < KP; ++q)
+            if (q == k - 1) dk = (double)__fsqrt_rn(sq[q]);
+        if (!uniform) {
+            const double inv = -1.0 / (2.0 * sigma * sigma);
+            const double tail = exp(dk * dk * inv);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                const double dq = (double)__fsqrt_rn(sq[q]);
+                const double v = q < k ? exp(dq * dq * inv) - tail : 0.0;
+                sc[q] = v > 0.0 ? (float)v : 0.0f;
+                if (q == 0) uniform = v < kScoreEps;
+            }
+        }
+        if (uniform) {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
+        }
+
+        double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+        float kappa = 0.0f;
+#pragma unroll
+        for (int u = 0; u < KP - 1; ++u) {
+#pragma unroll
+            for (int v = u + 1; v < KP; ++v) {
+                const float w = sc[u] * sc[v];  // 0 when v >= k (sc = 0 there) or s_{k-1} = 0
+                const int ti = jj[u] < jj[v] ? rb[u] + jj[v] : rb[v] + jj[u];
+                const float tv = w > 0.0f ? T[ti] : -1.0f;
+                const float ex = __fsub_rn(lx[v], lx[u]), ey = __fsub_rn(ly[v], ly[u]);
+                const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+                const bool keep = (tv >= 0.0f) & (ld2 >= kLd2Min);
+                kappa = keep ? fmaxf(kappa, (sq[u] + sq[v]) * tv) : kappa;
+                const float r = keep ? __frcp_rn(ld2) : 0.0f;
+                const float g1 = ex * r, g2 = ey * r;
+                // dnum/hd2 by the law of cosines + g . lo_u
+                const float h = fmaf(sq[u] - sq[v], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
+                const double W = keep ? (double)w : 0.0;
+                const double G1 = (double)g1, G2 = (double)g2;
+                const double wg1 = W * G1, wg2 = W * G2, wh = W * (double)h;
+                a11 = fma(wg1, G1, a11);
+                a12 = fma(wg1, G2, a12);
+                a22 = fma(wg2, G2, a22);
+                c1 = fma(wh, G1, c1);
+                c2 = fma(wh, G2, c2);
+            }
+        }
+        float2 out;
+        if (kappa > (float)kKappaMax) {
+            // far outlier: exact x-based f64 pair loop (rare; rows spilled to local memory)
+            double o5[5];
+            pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, sc, 1, o5);
+            a11 = o5[0];
+            a12 = o5[1];
+            a22 = o5[2];
+            c1 = o5[3];
+            c2 = o5[4];
+        }
+        const double det = a11 * a22 - a12 * a12;
+        const double tr = a11 + a22;
+        if (det < kDetRel * tr * tr + kDetAbs) {
+            out = make_float2(lx[0], ly[0]);
+        } else {
+            out.x = (float)((c1 * a22 - c2 * a12) / det);
+            out.y = (float)((a11 * c2 - a12 * c1) / det);
+        }
+        reinterpret_cast<float2*>(a.xy)[i] = out;
+    }
+}
+
+template <int KP, bool TSMEM>
+int launch_project_reg(ProjArgs a, size_t smem, cudaStream_t st) {
+    auto kern = project_reg_kernel<KP, TSMEM>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 384, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t nblk = (a.n + 383) / 384;
+    int64_t grid = (int64_t)esom_host::num_sms() * per_sm;
+    if (grid > nblk) grid = nblk;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 384, smem, st>>>(a);
+    return esom_host::cuda_check("project_reg_kernel");
+}
+
 template <int KP>
 int launch_project_t(ProjArgs a, cudaStream_t st) {
+    if constexpr (KP <= 16) {
+        const size_t base = (size_t)a.g * 12 + 256;
+        const size_t tbytes = (size_t)a.g * (a.g - 1) / 2 * 4;
+        const size_t cap = (size_t)esom_host::max_smem_optin() - 1024;
+        if (base + tbytes <= cap) return launch_project_reg<KP, true>(a, base + tbytes, st);
+        return launch_project_reg<KP, false>(a, base, st);
+    }
     constexpr int kProjThreads = proj_threads<KP>();
     const size_t base = (size_t)a.g * 12 + (size_t)KP * kProjThreads * 12 + 64;
     const size_t tbytes = (size_t)a.g * (a.g - 1) / 2 * 4;

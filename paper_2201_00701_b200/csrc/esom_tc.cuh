@@ -223,45 +223,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
         // ---- epilogue: screen with the approximate distances ----
         const float xnorm = sqrtf(xn);
         const float eps2 = 2.0f * tc_eps(xnorm, xn, lmax, lnmax, d, d16);
-        float vd[KP];
-        vlist_init<KP>(vd, k);
-        int cnt = 0;
-        bool ovf = false;
+        // pass 1: minima of the 32 landmark groups j = q (mod 32); the k-th
+        // smallest group minimum bounds the k-th smallest d~ from above (the
+        // minima belong to k distinct landmarks)
+        float gm[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) gm[q] = kInf;
         for (int c0 = 0; c0 < gpad; c0 += 32) {
             float v[32];
             tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
-            if (ovf) continue;
-            const float tau = vd[KP - 1] + eps2;
-            const int cnt0 = cnt;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) gm[q] = fminf(gm[q], fmaf(-2.0f, v[q], xn + lns[c0 + q]));
+        }
+        float vd[KP];
+        vlist_init<KP>(vd, k);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) vlist_insert<KP>(vd, gm[q]);
+        const float tcut = vd[KP - 1] + eps2;
+        // pass 2: log every landmark that can still be in the top k
+        int cnt = 0;
+        for (int c0 = 0; c0 < gpad; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
 #pragma unroll
             for (int q = 0; q < 32; ++q) {
-                const float dt = fmaf(-2.0f, v[q], xn + lns[c0 + q]);  // +inf for padding rows
-                v[q] = dt;
-                if (dt <= tau) {
-                    logv[cnt * kTcThreads + tid] = dt;
-                    logj[cnt * kTcThreads + tid] = (unsigned short)(c0 + q);
+                const float dt = fmaf(-2.0f, v[q], xn + lns[c0 + q]);  // +inf on padding rows
+                if (dt <= tcut) {
+                    if (cnt < LOGCAP) {
+                        logv[cnt * kTcThreads + tid] = dt;
+                        logj[cnt * kTcThreads + tid] = (unsigned short)(c0 + q);
+                    }
                     ++cnt;
                 }
             }
-            for (int e = cnt0; e < cnt; ++e) {
+        }
+        const bool ovf = cnt > LOGCAP;
+        // refine: the exact k-th smallest d~ among the logged candidates
+        vlist_init<KP>(vd, k);
+        if (!ovf)
+            for (int e = 0; e < cnt; ++e) {
                 const float dv = logv[e * kTcThreads + tid];
                 if (dv < vd[KP - 1]) vlist_insert<KP>(vd, dv);
             }
-            if (cnt > LOGCAP - kTile) {
-                const float tf = vd[KP - 1] + eps2;
-                int w = 0;
-                for (int e = 0; e < cnt; ++e) {
-                    const float dv = logv[e * kTcThreads + tid];
-                    if (dv <= tf) {
-                        logj[w * kTcThreads + tid] = logj[e * kTcThreads + tid];
-                        logv[w * kTcThreads + tid] = dv;
-                        ++w;
-                    }
-                }
-                cnt = w;
-                ovf = cnt > LOGCAP - kTile;
-            }
-        }
         tc_fence_before();
         __syncthreads();  // TMEM and the A tiles may be overwritten by the next block
 

@@ -207,6 +207,11 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
     k = params.k
     want_numpy = not _dev.is_device_tensor(points)
     dev = _dev.cuda_device(points)
+    if (isinstance(points, torch.Tensor) and not points.is_cuda and points.is_pinned() and mode == "fast"
+            and k <= 64 and points.dtype == torch.float32 and points.is_contiguous() and ps[0] >= 2 * PIPE_CHUNK
+            and not chunk_size):
+        with torch.cuda.device(dev):
+            return _embed_host_pipelined(points, model, k, dev)
     with torch.cuda.device(dev):
         X = _dev.to_f32(points, dev)
         n = X.shape[0]
@@ -230,3 +235,47 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
         _dev.raise_if_nonfinite(flag)
         _dev.raise_if_nonfinite(pm.flag)
         return _dev.out_like(xy, want_numpy)
+
+
+PIPE_CHUNK = 1 << 17  # points per H2D/compute/D2H stage of the host pipeline
+
+
+def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
+    """embed() for pinned host points: chunked H2D on a copy stream overlapped
+    with the kernels on the compute stream and the D2H of finished chunks, so
+    the end-to-end time approaches max(PCIe, compute) instead of their sum."""
+    n, d = host.shape
+    pm = PreparedModel(model.hi, model.lo, k, device=dev)
+    flag = _dev.new_flag(dev)
+    out = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    c = min(PIPE_CHUNK, n)
+    Xd = [torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(2)]
+    Yd = [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(2)]
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    freed = [None, None]
+    copy.wait_stream(comp)  # model preparation precedes the first chunk
+    for it, s in enumerate(range(0, n, c)):
+        b = it & 1
+        m = min(c, n - s)
+        with torch.cuda.stream(copy):
+            if freed[b] is not None:
+                copy.wait_event(freed[b])
+            Xd[b][:m].copy_(host[s:s + m], non_blocking=True)
+            loaded[b].record(copy)
+        comp.wait_event(loaded[b])
+        pm.embed_into(Xd[b][:m], Yd[b][:m], flag=flag)
+        done[b].record(comp)
+        with torch.cuda.stream(copy):
+            copy.wait_event(done[b])
+            out[s:s + m].copy_(Yd[b][:m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            freed[b] = ev
+    copy.synchronize()
+    comp.synchronize()
+    _dev.raise_if_nonfinite(flag)
+    _dev.raise_if_nonfinite(pm.flag)
+    return out.numpy()

@@ -209,3 +209,13 @@ def test_embed_errors(rng_np):
     bad[1, 2] = np.nan
     with pytest.raises(esom.InputError):
         esom.embed(bad, model, esom.EmbedParams(k=4))
+
+
+def test_host_pipeline_equals_device():
+    # pinned host input takes the chunked H2D/compute/D2H pipeline; same rows out
+    pts, hi, lo = c2_inputs()
+    model = esom.LandmarkModel.create(hi, lo)
+    host = torch.from_numpy(pts[:600_000].copy()).pin_memory()
+    a = esom.embed(host, model, esom.EmbedParams(k=16))
+    b = esom.embed(torch.from_numpy(pts[:600_000]).cuda(), model, esom.EmbedParams(k=16)).cpu().numpy()
+    assert isinstance(a, np.ndarray) and np.array_equal(a, b)

@@ -110,7 +110,7 @@ def test_batch_som_b1_equals_online(golden):
 def test_frame_loop_trains_and_embeds():
     pts, hi, lo = c2_inputs()
     X = torch.from_numpy(pts).cuda()
-    loop = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=1.5, alpha=0.5))
+    loop = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=0.3, alpha=0.5))
     qes = []
     for _ in range(5):
         loop.frame()

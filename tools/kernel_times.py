@@ -61,11 +61,15 @@ def main(names):
         def prep():
             pm.update()
 
+        import os
+        os.environ["ESOM_TC"] = "0"
+        t_scan = timed(knn, flush)
+        os.environ["ESOM_TC"] = "1"
         t_knn = timed(knn, flush)
         t_emb = timed(embed, flush)
         t_prep = timed(prep, flush)
-        print(json.dumps({"shape": name, "n": n, "d": d, "g": g, "k": k, "knn_ms": t_knn, "embed_ms": t_emb,
-                          "projection_ms": t_emb - t_knn, "prepare_model_ms": t_prep,
+        print(json.dumps({"shape": name, "n": n, "d": d, "g": g, "k": k, "knn_scan_ms": t_scan, "knn_ms": t_knn,
+                          "embed_ms": t_emb, "projection_ms": t_emb - t_knn, "prepare_model_ms": t_prep,
                           "embed_Mpts_per_s": n / t_emb / 1e3}), flush=True)
         del X, idx, sqd, xy, pm
 
