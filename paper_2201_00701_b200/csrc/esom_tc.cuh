@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
     float* Lt = reinterpret_cast<float*>(p);  p += lt_bytes;
     float* lns = reinterpret_cast<float*>(p);  p += ((gpad * 4 + 127) / 128) * 128;
     float* xrow = reinterpret_cast<float*>(p);  p += (((size_t)kTcThreads * (d + 1) * 4 + 127) / 128) * 128;
-    float* logv = reinterpret_cast<float*>(p);  p += (size_t)LOGCAP * kTcThreads * 4;
+    float* logv = reinterpret_cast<float*>(p);  p += (size_t)(LOGCAP + 1) * kTcThreads * 4;
     unsigned short* logj = reinterpret_cast<unsigned short*>(p);
 
     if (tid == 0) {
@@ -248,13 +248,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
 #pragma unroll
             for (int q = 0; q < 32; ++q) {
                 const float dt = fmaf(-2.0f, v[q], xn + lns[c0 + q]);  // +inf on padding rows
-                if (dt <= tcut) {
-                    if (cnt < LOGCAP) {
-                        logv[cnt * kTcThreads + tid] = dt;
-                        logj[cnt * kTcThreads + tid] = (unsigned short)(c0 + q);
-                    }
-                    ++cnt;
+                const bool keep = dt <= tcut;
+                const int slot = min(cnt, LOGCAP);  // slot LOGCAP is a dump row
+                if (keep) {
+                    logv[slot * kTcThreads + tid] = dt;
+                    logj[slot * kTcThreads + tid] = (unsigned short)(c0 + q);
                 }
+                cnt += keep ? 1 : 0;
             }
         }
         const bool ovf = cnt > LOGCAP;
@@ -277,22 +277,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
         int written = 0;
         if (!ovf && !xbad) {
             const float tf = vd[KP - 1] + eps2;
+            int m = 0;  // compact the survivors of the refined threshold (index order kept)
+            for (int e = 0; e < cnt; ++e) {
+                const float dv = logv[e * kTcThreads + tid];
+                if (dv <= tf) {
+                    logj[m * kTcThreads + tid] = logj[e * kTcThreads + tid];
+                    ++m;
+                }
+            }
+            // exact f32 distances, four independent sequential chains in flight
             float ve[KP];
             vlist_init<KP>(ve, k);
-            int m = 0;
-            for (int e = 0; e < cnt; ++e) {
-                if (!(logv[e * kTcThreads + tid] <= tf)) continue;
-                const int j = logj[e * kTcThreads + tid];
-                const float* lt = Lt + (size_t)(j >> 5) * a.dp * kTile + (j & 31);
-                float s = 0.0f;
-                for (int c = 0; c < d; ++c) {
-                    const float t = __fsub_rn(myx[c], lt[c * kTile]);
-                    s = __fadd_rn(s, __fmul_rn(t, t));
+            for (int e = 0; e < m; e += 4) {
+                const float* lt[4];
+                int jq[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    jq[u] = logj[min(e + u, m - 1) * kTcThreads + tid];
+                    lt[u] = Lt + (size_t)(jq[u] >> 5) * a.dp * kTile + (jq[u] & 31);
                 }
-                logv[m * kTcThreads + tid] = s;  // compact in place: exact value, same index order
-                logj[m * kTcThreads + tid] = (unsigned short)j;
-                ++m;
-                if (s < ve[KP - 1]) vlist_insert<KP>(ve, s);
+                float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                for (int c = 0; c < d; ++c) {
+                    const float xc = myx[c];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float t = __fsub_rn(xc, lt[u][c * kTile]);
+                        s4[u] = __fadd_rn(s4[u], __fmul_rn(t, t));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (e + u < m) {
+                        logv[(e + u) * kTcThreads + tid] = s4[u];
+                        if (s4[u] < ve[KP - 1]) vlist_insert<KP>(ve, s4[u]);
+                    }
+                }
             }
             if (a.stats) atomicAdd(a.stats, m);
             const float te = ve[KP - 1];
@@ -356,7 +375,7 @@ size_t tc_smem_bytes(const TcArgs& a) {
     b += (size_t)(a.gpad / kTile) * a.dp * kTile * 4;                // exact tiles
     b += ((size_t)a.gpad * 4 + 127) / 128 * 128;                     // |l|^2
     b += (((size_t)kTcThreads * (a.d + 1) * 4 + 127) / 128) * 128;   // f32 rows
-    b += (size_t)LOGCAP * kTcThreads * 6;                            // candidate log
+    b += (size_t)(LOGCAP + 1) * kTcThreads * 6;                      // candidate log (+ dump row)
     return b + 1024;
 }
 
