@@ -196,9 +196,11 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
 // loop is fully unrolled (static register indexing; no per-pair shared
 // loads except the pair-table entry).  Same arithmetic as above.
 // ---------------------------------------------------------------------------
+constexpr int kRegThreads = 256;
+
 template <int KP, bool TSMEM>
-__global__ void __launch_bounds__(384) project_reg_kernel(ProjArgs a) {
-    constexpr int PT = 384;
+__global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
+    constexpr int PT = kRegThreads;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(384) project_reg_kernel(ProjArgs a) {
     const float* T = TSMEM ? tsm : a.T;
 
     for (int64_t i = blockIdx.x * (int64_t)PT + tid; i < a.n; i += (int64_t)gridDim.x * PT) {
-        int jj[KP], rb[KP];
+        int jj[KP];
         float sq[KP], sc[KP], lx[KP], ly[KP];
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
@@ -234,7 +236,6 @@ __global__ void __launch_bounds__(384) project_reg_kernel(ProjArgs a) {
             const float2 l = LO[jj[q]];
             lx[q] = l.x;
             ly[q] = l.y;
-            rb[q] = RB[jj[q]];
             if (q < k) sigma += (double)__fsqrt_rn(sq[q]);
         }
         // scores (f64 like the reference; ref: projection.py:38-59)
@@ -261,22 +262,59 @@ __global__ void __launch_bounds__(384) project_reg_kernel(ProjArgs a) {
         }
 
         double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-        float kappa = 0.0f;
+        float tmax = 0.0f;
+        // Ring schedule over the KP slots: round r pairs slot u with slot
+        // (u + r) mod KP, r = 1..KP/2 (the last round only u < KP/2), which
+        // visits every unordered pair exactly once.  The partner arrays are
+        // rotated by one slot per round, so the round body is static code
+        // (KP pair bodies) inside a short dynamic loop: small I-cache
+        // footprint, registers only.  A pair's contribution is symmetric in
+        // (u, v) (g flips sign together with h), so visiting (v, u) is exact
+        // up to rounding.  Slots >= k carry zero weight.
+        int pj[KP];
+        float psq[KP], psc[KP], plx[KP], ply[KP];
 #pragma unroll
-        for (int u = 0; u < KP - 1; ++u) {
+        for (int q = 0; q < KP; ++q) {
+            pj[q] = jj[q];
+            psq[q] = sq[q];
+            psc[q] = sc[q];
+            plx[q] = lx[q];
+            ply[q] = ly[q];
+        }
+        for (int r = 1; r <= KP / 2; ++r) {
+            // rotate partners by one: p[q] <- p[q + 1]
+            {
+                const int j0 = pj[0];
+                const float s0 = psq[0], c0 = psc[0], x0 = plx[0], y0 = ply[0];
 #pragma unroll
-            for (int v = u + 1; v < KP; ++v) {
-                const float w = sc[u] * sc[v];  // 0 when v >= k (sc = 0 there) or s_{k-1} = 0
-                const int ti = jj[u] < jj[v] ? rb[u] + jj[v] : rb[v] + jj[u];
+                for (int q = 0; q < KP - 1; ++q) {
+                    pj[q] = pj[q + 1];
+                    psq[q] = psq[q + 1];
+                    psc[q] = psc[q + 1];
+                    plx[q] = plx[q + 1];
+                    ply[q] = ply[q + 1];
+                }
+                pj[KP - 1] = j0;
+                psq[KP - 1] = s0;
+                psc[KP - 1] = c0;
+                plx[KP - 1] = x0;
+                ply[KP - 1] = y0;
+            }
+            const bool half = r == KP / 2;
+#pragma unroll
+            for (int u = 0; u < KP; ++u) {
+                const float w = (half && u >= KP / 2) ? 0.0f : sc[u] * psc[u];
+                const int lo_j = min(jj[u], pj[u]), hi_j = max(jj[u], pj[u]);
+                const int ti = ((lo_j * (2 * g - 1 - lo_j)) >> 1) + hi_j - lo_j - 1;  // packed upper triangle
                 const float tv = w > 0.0f ? T[ti] : -1.0f;
-                const float ex = __fsub_rn(lx[v], lx[u]), ey = __fsub_rn(ly[v], ly[u]);
+                const float ex = __fsub_rn(plx[u], lx[u]), ey = __fsub_rn(ply[u], ly[u]);
                 const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
                 const bool keep = (tv >= 0.0f) & (ld2 >= kLd2Min);
-                kappa = keep ? fmaxf(kappa, (sq[u] + sq[v]) * tv) : kappa;
-                const float r = keep ? __frcp_rn(ld2) : 0.0f;
-                const float g1 = ex * r, g2 = ey * r;
+                tmax = keep ? fmaxf(tmax, tv) : tmax;
+                const float rr = keep ? __frcp_rn(ld2) : 0.0f;
+                const float g1 = ex * rr, g2 = ey * rr;
                 // dnum/hd2 by the law of cosines + g . lo_u
-                const float h = fmaf(sq[u] - sq[v], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
+                const float h = fmaf(sq[u] - psq[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
                 const double W = keep ? (double)w : 0.0;
                 const double G1 = (double)g1, G2 = (double)g2;
                 const double wg1 = W * G1, wg2 = W * G2, wh = W * (double)h;
@@ -287,6 +325,11 @@ __global__ void __launch_bounds__(384) project_reg_kernel(ProjArgs a) {
                 c2 = fma(wh, G2, c2);
             }
         }
+        // kappa <= 2 max(sqd) max(T): exact pair-wise check only when that bound trips
+        float sqmax = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) sqmax = fmaxf(sqmax, sq[q]);
+        float kappa = 2.0f * sqmax * tmax;
         float2 out;
         if (kappa > (float)kKappaMax) {
             // far outlier: exact x-based f64 pair loop (rare; rows spilled to local memory)
@@ -315,13 +358,13 @@ int launch_project_reg(ProjArgs a, size_t smem, cudaStream_t st) {
     auto kern = project_reg_kernel<KP, TSMEM>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 384, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRegThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    const int64_t nblk = (a.n + 383) / 384;
+    const int64_t nblk = (a.n + kRegThreads - 1) / kRegThreads;
     int64_t grid = (int64_t)esom_host::num_sms() * per_sm;
     if (grid > nblk) grid = nblk;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, 384, smem, st>>>(a);
+    kern<<<(unsigned)grid, kRegThreads, smem, st>>>(a);
     return esom_host::cuda_check("project_reg_kernel");
 }
 
