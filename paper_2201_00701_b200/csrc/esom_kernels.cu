@@ -174,6 +174,51 @@ __global__ void tc_prepare_kernel(const float* __restrict__ hi, int g, int d, in
     }
 }
 
+// BMU bucket sort of a chunk's neighbour rows (counting sort on idx[:,0]):
+// the projection visits points grouped by nearest landmark, so the pair-table
+// gathers of a warp coalesce when the table does not fit in shared memory.
+__global__ void bmu_hist_kernel(const int32_t* __restrict__ idx, int64_t n, int k, int g, int32_t* __restrict__ cnt) {
+    extern __shared__ int32_t h[];
+    for (int b = threadIdx.x; b < g; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[__ldg(idx + i * k)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < g; b += blockDim.x)
+        if (h[b]) atomicAdd(cnt + b, h[b]);
+}
+
+__global__ void bmu_scan_kernel(int32_t* __restrict__ cnt, int g) {  // one CTA: exclusive scan in place
+    __shared__ int32_t part[1024];
+    const int per = (g + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per;
+    int s = 0;
+    for (int b = b0; b < b0 + per && b < g; ++b) s += cnt[b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            const int v = part[t];
+            part[t] = acc;
+            acc += v;
+        }
+    }
+    __syncthreads();
+    int acc = part[threadIdx.x];
+    for (int b = b0; b < b0 + per && b < g; ++b) {
+        const int v = cnt[b];
+        cnt[b] = acc;
+        acc += v;
+    }
+}
+
+__global__ void bmu_scatter_kernel(const int32_t* __restrict__ idx, int64_t n, int k, int32_t* __restrict__ cursor,
+                                   int32_t* __restrict__ perm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        perm[atomicAdd(cursor + __ldg(idx + i * k), 1)] = (int32_t)i;
+}
+
 // ---------------------------------------------------------------------------
 // Scores (ref: projection.py:38-59).  numba's float(f32) stays f32, so the
 // root is sqrtf, widened; the rest is f64.  `exp` is CUDA's (<= 1 ulp from
@@ -583,7 +628,7 @@ bool tc_enabled() {  // ESOM_TC=0 forces the CUDA-core scan (read per call: test
 }
 
 // shapes the split-bf16 tensor-core screen handles (smem budget of esom_tc.cuh)
-bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1024 && d <= 32 && g <= 256 && k <= 16; }
+bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1024 && d <= 32 && g <= 4096 && k <= 16; }
 
 int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cudaStream_t st) {
     cudaMemsetAsync(ws + m.lstats, 0, 8, st);
@@ -607,7 +652,7 @@ int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const ch
     a.Bhi = reinterpret_cast<const uint16_t*>(ws + m.bhi);
     a.Blo = reinterpret_cast<const uint16_t*>(ws + m.blo);
     a.ln = reinterpret_cast<const float*>(ws + m.ln);
-    a.Lt = reinterpret_cast<const float*>(ws + m.lt);
+    a.Lt = m.gpad <= 256 ? reinterpret_cast<const float*>(ws + m.lt) : nullptr;  // resident exact tiles
     a.L = s.L;
     a.lstats = reinterpret_cast<const float*>(ws + m.lstats);
     a.out_idx = s.out_idx;
@@ -663,7 +708,8 @@ static int64_t embed_chunk(int32_t k) {
 
 size_t esom_point_workspace_bytes(int64_t n, int32_t k) {
     const int64_t c = n < embed_chunk(k) ? n : embed_chunk(k);
-    return align256((size_t)(c > 0 ? c : 1) * k * 4) * 2 + 256;
+    const size_t rows = align256((size_t)(c > 0 ? c : 1) * k * 4) * 2;
+    return rows + align256((size_t)(c > 0 ? c : 1) * 4) + align256(65536 * 4) + 256;  // + perm + bucket counts
 }
 
 static ScanArgs scan_args(const Plan& p, const float* X, int64_t n, int32_t d, const float* L, int32_t g, int32_t k,
@@ -779,6 +825,19 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         a.qe_sum = qe_sum;
         if (int e = run_knn(p, ml, a, mws, stream)) return e;
         ProjArgs q{};
+        const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
+        if (tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192) {
+            // pair table stays in L2: visit points grouped by BMU
+            char* base = reinterpret_cast<char*>(point_ws) + 2 * align256((size_t)chunk * k * 4);
+            int32_t* perm = reinterpret_cast<int32_t*>(base);
+            int32_t* cntb = reinterpret_cast<int32_t*>(base + align256((size_t)chunk * 4));
+            cudaMemsetAsync(cntb, 0, (size_t)g * 4, stream);
+            bmu_hist_kernel<<<num_sms() * 2, 512, (size_t)g * 4, stream>>>(idx, m, k, g, cntb);
+            bmu_scan_kernel<<<1, 1024, 0, stream>>>(cntb, g);
+            bmu_scatter_kernel<<<grid_for(m, 256), 256, 0, stream>>>(idx, m, k, cntb, perm);
+            if (int e = cuda_check("bmu_sort")) return e;
+            q.perm = perm;
+        }
         q.idx = idx;
         q.sqd = sqd;
         q.n = m;

@@ -198,6 +198,12 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
 // ---------------------------------------------------------------------------
 constexpr int kRegThreads = 256;
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 template <int KP, bool TSMEM>
 __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
     constexpr int PT = kRegThreads;
@@ -218,7 +224,10 @@ __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
     __syncthreads();
     const float* T = TSMEM ? tsm : a.T;
 
-    for (int64_t i = blockIdx.x * (int64_t)PT + tid; i < a.n; i += (int64_t)gridDim.x * PT) {
+    for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
+        // optional BMU-sorted visiting order: lanes of a warp then share
+        // neighbour sets, so their pair-table reads hit the same L1 lines
+        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
         int jj[KP];
         float sq[KP], sc[KP], lx[KP], ly[KP];
         const int32_t* irow = a.idx + i * k;
@@ -311,7 +320,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
                 const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
                 const bool keep = (tv >= 0.0f) & (ld2 >= kLd2Min);
                 tmax = keep ? fmaxf(tmax, tv) : tmax;
-                const float rr = keep ? __frcp_rn(ld2) : 0.0f;
+                const float rr = keep ? rcp_approx(ld2) : 0.0f;  // MUFU.RCP (<= 1 ulp); ld2 >= 1e-12
                 const float g1 = ex * rr, g2 = ey * rr;
                 // dnum/hd2 by the law of cosines + g . lo_u
                 const float h = fmaf(sq[u] - psq[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);

@@ -35,6 +35,7 @@ struct ProjArgs {
     const float* X;          // outlier exact path
     const float* hi;
     int d;
+    const int32_t* perm;     // optional visiting order (nullable)
 };
 
 // tensor-core screened k-NN (esom_tc.cuh)

@@ -108,22 +108,25 @@ template <int KP>
 __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
     constexpr int LOGCAP = KP + kTile;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bar_load, bar_mma;
+    __shared__ __align__(8) uint64_t bar_load, bar_mma, bar_b[2];
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int d = a.d, d16 = a.d16, gpad = a.gpad, k = a.k;
     const int off = KP - k;
-    const uint32_t a_bytes = 128u * d16 * 2u;            // one operand tile (hi or lo), bytes
-    const uint32_t b_bytes = (uint32_t)gpad * d16 * 2u;
-    const uint32_t lt_bytes = (uint32_t)(gpad / kTile) * a.dp * kTile * 4u;
+    const int R = (gpad + 255) >> 8;           // landmark rounds of <= 256 TMEM columns
+    const bool streamB = R > 1;                // B streamed round by round (double buffered)
+    const bool lt_res = a.Lt != nullptr;       // exact tiles resident in smem (else rows from L2)
+    const uint32_t a_bytes = 128u * d16 * 2u;  // one operand tile (hi or lo), bytes
+    const uint32_t b_bytes = (uint32_t)(streamB ? 256 : gpad) * d16 * 2u;
+    const uint32_t lt_bytes = lt_res ? (uint32_t)(gpad / kTile) * a.dp * kTile * 4u : 0u;
     // ---- shared memory carve-up (all 128-byte aligned) ----
     unsigned char* p = smem_raw;
-    unsigned char* Ahi = p;  p += 2 * a_bytes;            // [tile 0 | tile 1]
+    unsigned char* Ahi = p;  p += 2 * a_bytes;  // [tile 0 | tile 1]
     unsigned char* Alo = p;  p += 2 * a_bytes;
-    unsigned char* Bhi = p;  p += b_bytes;
-    unsigned char* Blo = p;  p += b_bytes;
+    unsigned char* Bhi = p;  p += (streamB ? 2 : 1) * b_bytes;
+    unsigned char* Blo = p;  p += (streamB ? 2 : 1) * b_bytes;
     float* Lt = reinterpret_cast<float*>(p);  p += lt_bytes;
     float* lns = reinterpret_cast<float*>(p);  p += ((gpad * 4 + 127) / 128) * 128;
     float* xrow = reinterpret_cast<float*>(p);  p += (((size_t)kTcThreads * (d + 1) * 4 + 127) / 128) * 128;
@@ -133,9 +136,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
     if (tid == 0) {
         mbar_init(&bar_load, 1);
         mbar_init(&bar_mma, 1);
+        mbar_init(&bar_b[0], 1);
+        mbar_init(&bar_b[1], 1);
         fence_mbar_init();
     }
-    if (warp == 0) {  // 512 TMEM columns: tile t accumulates in columns [256 t, 256 t + gpad)
+    if (warp == 0) {  // 512 TMEM columns: tile t accumulates in columns [256 t, 256 t + 256)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -145,24 +150,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
     const float lmax = __ldg(a.lstats), lnmax = __ldg(a.lstats + 1);
+    const int64_t nblk = (a.n + kTcThreads - 1) / kTcThreads;
+
+    // B round v (of the periodic visit sequence: two passes x R rounds per block)
+    auto load_round = [&](int64_t v) {
+        const int b = (int)(v & 1), r = (int)(v % R);
+        const int rows = min(256, gpad - 256 * r);
+        const uint32_t bytes = (uint32_t)rows * d16 * 2u;
+        const size_t off_el = (size_t)256 * r * d16;
+        mbar_expect_tx(&bar_b[b], 2 * bytes);
+        tma_bulk_g2s(Bhi + b * b_bytes, a.Bhi + off_el, bytes, &bar_b[b]);
+        tma_bulk_g2s(Blo + b * b_bytes, a.Blo + off_el, bytes, &bar_b[b]);
+    };
     if (tid == 0) {
-        mbar_expect_tx(&bar_load, 2 * b_bytes + lt_bytes + (uint32_t)gpad * 4u);
-        tma_bulk_g2s(Bhi, a.Bhi, b_bytes, &bar_load);
-        tma_bulk_g2s(Blo, a.Blo, b_bytes, &bar_load);
-        tma_bulk_g2s(Lt, a.Lt, lt_bytes, &bar_load);
+        mbar_expect_tx(&bar_load, (streamB ? 0u : 2 * b_bytes) + lt_bytes + (uint32_t)gpad * 4u);
+        if (!streamB) {
+            tma_bulk_g2s(Bhi, a.Bhi, b_bytes, &bar_load);
+            tma_bulk_g2s(Blo, a.Blo, b_bytes, &bar_load);
+        }
+        if (lt_res) tma_bulk_g2s(Lt, a.Lt, lt_bytes, &bar_load);
         tma_bulk_g2s(lns, a.ln, (uint32_t)gpad * 4u, &bar_load);
+        if (streamB && blockIdx.x < nblk) {
+            load_round(0);
+            load_round(1);
+        }
     }
     mbar_wait(&bar_load, 0);
 
     const int tile = tid >> 7, row = tid & 127;
-    const uint32_t idesc = umma_idesc_bf16(128, gpad);
     const uint32_t sbo = (uint32_t)(d16 >> 3) << 7, lbo = 128;
     const uint32_t lane_col = ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * tile);
     float* myx = xrow + (size_t)tid * (d + 1);
-    uint32_t mma_phase = 0;
+    uint32_t mma_phase = 0, bph0 = 0, bph1 = 0;
+    int64_t visit = 0;
     bool bad = false;
     double qe_local = 0.0;
-    const int64_t nblk = (a.n + kTcThreads - 1) / kTcThreads;
 
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         const int64_t i = blk * kTcThreads + tid;
@@ -200,74 +222,97 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
         fence_proxy_async();  // generic smem writes -> visible to the tensor core (async proxy)
         tc_fence_before();
         __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            for (int t = 0; t < 2; ++t) {
-                const uint32_t abase_h = smem_u32(Ahi + t * a_bytes), abase_l = smem_u32(Alo + t * a_bytes);
-                const uint32_t bbase_h = smem_u32(Bhi), bbase_l = smem_u32(Blo);
-                const uint32_t dcol = tmem + (uint32_t)(256 * t);
-                for (int ks = 0; ks < (d16 >> 4); ++ks) {
-                    const uint32_t ko = (uint32_t)ks * 256u;  // two 16-byte K chunks per MMA
-                    umma_bf16(dcol, umma_desc(abase_h + ko, lbo, sbo), umma_desc(bbase_h + ko, lbo, sbo), idesc,
-                              ks > 0);
-                    umma_bf16(dcol, umma_desc(abase_h + ko, lbo, sbo), umma_desc(bbase_l + ko, lbo, sbo), idesc, 1);
-                    umma_bf16(dcol, umma_desc(abase_l + ko, lbo, sbo), umma_desc(bbase_h + ko, lbo, sbo), idesc, 1);
-                }
-            }
-            umma_commit(&bar_mma);
-        }
-        mbar_wait(&bar_mma, mma_phase);
-        mma_phase ^= 1u;
-        tc_fence_after();
 
-        // ---- epilogue: screen with the approximate distances ----
         const float xnorm = sqrtf(xn);
         const float eps2 = 2.0f * tc_eps(xnorm, xn, lmax, lnmax, d, d16);
-        // pass 1: minima of the 32 landmark groups j = q (mod 32); the k-th
-        // smallest group minimum bounds the k-th smallest d~ from above (the
-        // minima belong to k distinct landmarks)
         float gm[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) gm[q] = kInf;
-        for (int c0 = 0; c0 < gpad; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) gm[q] = fminf(gm[q], fmaf(-2.0f, v[q], xn + lns[c0 + q]));
-        }
-        float vd[KP];
-        vlist_init<KP>(vd, k);
-#pragma unroll
-        for (int q = 0; q < 32; ++q) vlist_insert<KP>(vd, gm[q]);
-        const float tcut = vd[KP - 1] + eps2;
-        // pass 2: log every landmark that can still be in the top k
+        float tcut = kInf;
         int cnt = 0;
-        for (int c0 = 0; c0 < gpad; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const float dt = fmaf(-2.0f, v[q], xn + lns[c0 + q]);  // +inf on padding rows
-                const bool keep = dt <= tcut;
-                const int slot = min(cnt, LOGCAP);  // slot LOGCAP is a dump row
-                if (keep) {
-                    logv[slot * kTcThreads + tid] = dt;
-                    logj[slot * kTcThreads + tid] = (unsigned short)(c0 + q);
+        // two passes over the R landmark rounds: pass 0 builds the bound, pass 1 logs candidates
+        for (int s2 = 0; s2 < 2 * R; ++s2, ++visit) {
+            const int r = s2 % R, pass = s2 / R;
+            const int nr = min(256, gpad - 256 * r);
+            const int bb = streamB ? (int)(visit & 1) : 0;
+            if (tid == 0) {
+                if (streamB) {
+                    mbar_wait(&bar_b[bb], bb ? bph1 : bph0);
                 }
-                cnt += keep ? 1 : 0;
+                tc_fence_after();
+                const uint32_t idesc = umma_idesc_bf16(128, nr);
+                const uint32_t bbase_h = smem_u32(Bhi + bb * b_bytes), bbase_l = smem_u32(Blo + bb * b_bytes);
+                for (int t = 0; t < 2; ++t) {
+                    const uint32_t abase_h = smem_u32(Ahi + t * a_bytes), abase_l = smem_u32(Alo + t * a_bytes);
+                    const uint32_t dcol = tmem + (uint32_t)(256 * t);
+                    for (int ks = 0; ks < (d16 >> 4); ++ks) {
+                        const uint32_t ko = (uint32_t)ks * 256u;  // two 16-byte K chunks per MMA
+                        umma_bf16(dcol, umma_desc(abase_h + ko, lbo, sbo), umma_desc(bbase_h + ko, lbo, sbo), idesc,
+                                  ks > 0);
+                        umma_bf16(dcol, umma_desc(abase_h + ko, lbo, sbo), umma_desc(bbase_l + ko, lbo, sbo), idesc, 1);
+                        umma_bf16(dcol, umma_desc(abase_l + ko, lbo, sbo), umma_desc(bbase_h + ko, lbo, sbo), idesc, 1);
+                    }
+                }
+                umma_commit(&bar_mma);
             }
+            if (streamB) {
+                if (bb) bph1 ^= 1u; else bph0 ^= 1u;
+            }
+            mbar_wait(&bar_mma, mma_phase);
+            mma_phase ^= 1u;
+            tc_fence_after();
+            if (streamB && tid == 0) {
+                // buffer bb is free again: prefetch visit + 2 (next block's rounds included)
+                const bool more = s2 + 2 < 2 * R || blk + gridDim.x < nblk;
+                if (more) load_round(visit + 2);
+            }
+            const int cbase = 256 * r;
+            if (pass == 0) {
+                // minima of the 32 landmark groups j = q (mod 32): the k-th smallest
+                // group minimum bounds the k-th smallest d~ (k distinct landmarks)
+                for (int c0 = 0; c0 < nr; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) gm[q] = fminf(gm[q], fmaf(-2.0f, v[q], xn + lns[cbase + c0 + q]));
+                }
+                if (r == R - 1) {
+                    float vd[KP];
+                    vlist_init<KP>(vd, k);
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) vlist_insert<KP>(vd, gm[q]);
+                    tcut = vd[KP - 1] + eps2;
+                }
+            } else {
+                // log every landmark that can still be in the top k
+                for (int c0 = 0; c0 < nr; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float dt = fmaf(-2.0f, v[q], xn + lns[cbase + c0 + q]);  // +inf on padding rows
+                        const bool keep = dt <= tcut;
+                        const int slot = min(cnt, LOGCAP);  // slot LOGCAP is a dump row
+                        if (keep) {
+                            logv[slot * kTcThreads + tid] = dt;
+                            logj[slot * kTcThreads + tid] = (unsigned short)(cbase + c0 + q);
+                        }
+                        cnt += keep ? 1 : 0;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncthreads();  // TMEM columns are rewritten by the next visit's MMA
         }
         const bool ovf = cnt > LOGCAP;
         // refine: the exact k-th smallest d~ among the logged candidates
+        float vd[KP];
         vlist_init<KP>(vd, k);
         if (!ovf)
             for (int e = 0; e < cnt; ++e) {
                 const float dv = logv[e * kTcThreads + tid];
                 if (dv < vd[KP - 1]) vlist_insert<KP>(vd, dv);
             }
-        tc_fence_before();
-        __syncthreads();  // TMEM and the A tiles may be overwritten by the next block
-
         // ---- exact phase: reference f32 distances of the surviving candidates ----
         if (!valid) continue;
         int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
@@ -291,17 +336,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
             for (int e = 0; e < m; e += 4) {
                 const float* lt[4];
                 int jq[4];
+                int stride;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     jq[u] = logj[min(e + u, m - 1) * kTcThreads + tid];
-                    lt[u] = Lt + (size_t)(jq[u] >> 5) * a.dp * kTile + (jq[u] & 31);
+                    lt[u] = lt_res ? Lt + (size_t)(jq[u] >> 5) * a.dp * kTile + (jq[u] & 31) : a.L + (size_t)jq[u] * d;
                 }
+                stride = lt_res ? kTile : 1;
                 float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                 for (int c = 0; c < d; ++c) {
                     const float xc = myx[c];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const float t = __fsub_rn(xc, lt[u][c * kTile]);
+                        const float t = __fsub_rn(xc, lt[u][c * stride]);
                         s4[u] = __fadd_rn(s4[u], __fmul_rn(t, t));
                     }
                 }
@@ -370,9 +417,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
 template <int KP>
 size_t tc_smem_bytes(const TcArgs& a) {
     constexpr int LOGCAP = KP + kTile;
+    const bool streamB = a.gpad > 256;
     size_t b = 4 * (size_t)128 * a.d16 * 2;                          // A hi/lo, two tiles
-    b += 2 * (size_t)a.gpad * a.d16 * 2;                             // B hi/lo
-    b += (size_t)(a.gpad / kTile) * a.dp * kTile * 4;                // exact tiles
+    b += 2 * (size_t)(streamB ? 2 * 256 : a.gpad) * a.d16 * 2;       // B hi/lo (two round buffers when streamed)
+    if (a.Lt) b += (size_t)(a.gpad / kTile) * a.dp * kTile * 4;      // exact tiles (resident)
     b += ((size_t)a.gpad * 4 + 127) / 128 * 128;                     // |l|^2
     b += (((size_t)kTcThreads * (a.d + 1) * 4 + 127) / 128) * 128;   // f32 rows
     b += (size_t)(LOGCAP + 1) * kTcThreads * 6;                      // candidate log (+ dump row)

@@ -26,7 +26,8 @@ def run(p, l, k, tc):
     return nb
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "uniform16", "normal32", "ties", "wide"])
+@pytest.mark.parametrize("case", ["c1", "c2", "uniform16", "normal32", "ties", "wide", "rounds300", "c4like",
+                                  "g4096", "ties777"])
 def test_tc_equals_scan_and_oracle(case):
     gen = np.random.default_rng(hash(case) % 2**32)
     if case == "c1":
@@ -48,10 +49,27 @@ def test_tc_equals_scan_and_oracle(case):
         p = gen.integers(0, 3, size=(20000, 8)).astype(np.float32)
         l = gen.integers(0, 3, size=(128, 8)).astype(np.float32)
         k = 16
-    else:
+    elif case == "wide":
         p = gen.normal(size=(5000, 5)).astype(np.float32) * np.float32(1e3)
         l = gen.normal(size=(37, 5)).astype(np.float32)
         k = 4
+    elif case == "rounds300":  # two landmark rounds, the second partial
+        p = gen.normal(size=(20000, 24)).astype(np.float32)
+        l = gen.normal(size=(300, 24)).astype(np.float32)
+        k = 16
+    elif case == "c4like":
+        from paper_2201_00701_b200 import datagen
+        p = datagen.gaussians(16, 40000, 32, seed=3)[0]
+        l = p[gen.choice(40000, 1024, replace=False)]
+        k = 16
+    elif case == "g4096":
+        p = gen.random((8192, 16)).astype(np.float32)
+        l = gen.random((4096, 16)).astype(np.float32)
+        k = 8
+    else:  # ties777
+        p = gen.integers(0, 4, size=(10000, 6)).astype(np.float32)
+        l = gen.integers(0, 4, size=(777, 6)).astype(np.float32)
+        k = 16
     a = run(p, l, k, tc=True)
     b = run(p, l, k, tc=False)
     assert np.array_equal(a.indices, b.indices) and np.array_equal(a.sqdists, b.sqdists), case
