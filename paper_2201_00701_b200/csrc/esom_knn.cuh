@@ -68,6 +68,24 @@ __device__ __forceinline__ void vlist_insert(float (&vd)[KP], float v) {
     vd[0] = fminf(vd[0], v);
 }
 
+// Insert (v, j) into a sorted (dist, idx) register list whose held indices
+// are all smaller than j (strict '<' then realises the (dist, idx) order).
+// Slots below KP-k hold -inf and never move.
+template <int KP>
+__device__ __forceinline__ void topk_insert(float (&td)[KP], int (&ti)[KP], float v, int j) {
+#pragma unroll
+    for (int q = KP - 1; q > 0; --q) {
+        const bool gp = td[q - 1] > v;
+        const bool gc = td[q] > v;
+        td[q] = gp ? td[q - 1] : (gc ? v : td[q]);
+        ti[q] = gp ? ti[q - 1] : (gc ? j : ti[q]);
+    }
+    if (td[0] > v) {
+        td[0] = v;
+        ti[0] = j;
+    }
+}
+
 // number of values (live or -inf padding) strictly below v
 template <int KP>
 __device__ __forceinline__ int vlist_count_lt(const float (&vd)[KP], float v) {

@@ -330,9 +330,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
                     ++m;
                 }
             }
-            // exact f32 distances, four independent sequential chains in flight
-            float ve[KP];
-            vlist_init<KP>(ve, k);
+            // exact f32 distances (four independent sequential chains in flight),
+            // inserted in index order into a (dist, idx) register list
+            float td[KP];
+            int ti[KP];
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                td[q] = q >= off ? kInf : -kInf;
+                ti[q] = a.g;
+            }
             for (int e = 0; e < m; e += 4) {
                 const float* lt[4];
                 int jq[4];
@@ -353,42 +359,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (e + u < m) {
-                        logv[(e + u) * kTcThreads + tid] = s4[u];
-                        if (s4[u] < ve[KP - 1]) vlist_insert<KP>(ve, s4[u]);
-                    }
-                }
+                for (int u = 0; u < 4; ++u)
+                    if (e + u < m && s4[u] < td[KP - 1]) topk_insert<KP>(td, ti, s4[u], jq[u]);
             }
             if (a.stats) atomicAdd(a.stats, m);
-            const float te = ve[KP - 1];
-            int quota = k - (vlist_count_lt<KP>(ve, te) - off);
-            for (int e = 0; e < m; ++e) {
-                const float s = logv[e * kTcThreads + tid];
-                int r;
-                if (s < te) {
-                    r = vlist_count_lt<KP>(ve, s) - off;
-                    int le = 0;
+            written = 0;
 #pragma unroll
-                    for (int q = 0; q < KP; ++q) le += ve[q] <= s ? 1 : 0;
-                    if (le - off - r > 1)
-                        for (int e2 = 0; e2 < e; ++e2) r += logv[e2 * kTcThreads + tid] == s ? 1 : 0;
-                } else if (s == te && quota > 0) {
-                    r = k - quota;
-                    --quota;
-                } else {
-                    continue;
+            for (int q = 0; q < KP; ++q) {
+                if (q >= off) {
+                    written += ti[q] < a.g ? 1 : 0;
+                    if (oi) {
+                        oi[q - off] = ti[q];
+                        od[q - off] = td[q];
+                    }
+                    if (q == off) {
+                        b0 = ti[q];
+                        d0 = td[q];
+                    }
                 }
-                const int j = logj[e * kTcThreads + tid];
-                if (oi) {
-                    oi[r] = j;
-                    od[r] = s;
-                }
-                if (r == 0) {
-                    b0 = j;
-                    d0 = s;
-                }
-                ++written;
             }
         }
         if (written != k) {
