@@ -256,25 +256,47 @@ def run_ours(args):
     total_points = n * world
     value = total_points / (ms_max * 1e-3)
 
-    # ---- dominant kernel: the fused scan kernel, timed alone on the same stream ----
-    kern_ms = []
-    for _ in range(5):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        loop.model.embed_into(X, loop.xy, flag=loop.flag)
-        b.record(stream)
-        b.synchronize()
-        kern_ms.append(a.elapsed_time(b))
-    kern = statistics.median(kern_ms)
+    # ---- dominant kernel: the exact k-NN (tensor-core screened where eligible),
+    # timed alone over the whole shard with CUDA events on the launching stream.
+    # Algorithmic bytes of the k-NN API per point: 4d (X) + 8k (idx + sqd),
+    # SURVEY.md §8d.  The embed-level figure (4d + 8 per point) is reported too.
+    from paper_2201_00701_b200 import _dev as _d, _lib as _l
+
+    idx = torch.empty((n, k), dtype=torch.int32, device=dev)
+    sqd = torch.empty((n, k), dtype=torch.float32, device=dev)
+    wsk = torch.empty(_l.load().esom_workspace_bytes(g, d, k, 0), dtype=torch.uint8, device=dev)
+    kflag = _d.new_flag(dev)
+    sh = _d.stream_handle(dev)
+
+    def knn_call():
+        _l.call("esom_knn", _d.ptr(X), n, d, _d.ptr(loop.model.hi), g, k, _d.ptr(idx), _d.ptr(sqd), _d.ptr(kflag),
+                _d.ptr(wsk), wsk.numel(), sh)
+
+    def ev_time(fn, reps=5):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    knn_call()
+    kern = ev_time(knn_call)
+    emb = ev_time(lambda: loop.model.embed_into(X, loop.xy, flag=loop.flag))
+    del idx, sqd, wsk
     hbm_peak, bf16_peak, peak_kind = measured_peaks()
-    alg_bytes = n * (4 * d + 8)  # X read + xy write; landmarks excluded
+    alg_bytes = n * (4 * d + 8 * k)
     achieved = alg_bytes / (kern * 1e-3) / 1e9
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or 1965.0
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # lane-ops/s (T), at the sampled clock
-    fp32_ops = n * 3.0 * g * d / (kern * 1e-3) / 1e12  # exact sub/mul/add per element
-
+    exact_ops = n * 3.0 * g * d / (emb * 1e-3) / 1e12  # exact-path equivalent sub/mul/add per element
+    gemm_tflops = n * 2.0 * g * 16 * ((d + 15) // 16) * 3 / (kern * 1e-3) / 1e12  # split-bf16 screen
+    tc_used = d <= 32 and g <= 4096 and k <= 16 and os.environ.get("ESOM_TC", "1") != "0"
     # ---- end to end through the public API: pinned host points in, host xy out ----
     e2e = None
     if True:  # every rank measures; the slowest rank defines the job's e2e time
@@ -317,11 +339,16 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write outside the events); X = 128 MiB/rank"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": ncu_traffic(workload), "peak_kind": peak_kind,
-                         "kernel": "scan_kernel (fused distance+top-k+scores+projection)", "kernel_ms": kern,
-                         "alg_bytes_per_point": 4 * d + 8},
-            "compute_roofline": {"pipe": "fp32 (exact sub,mul,add per element; f32x2 packed)",
-                                 "achieved_Tops": fp32_ops, "peak_Tops_at_sampled_clock": fp32_peak,
-                                 "frac": fp32_ops / fp32_peak},
+                         "kernel": ("knn_tc_kernel (tcgen05 split-bf16 screen + exact f32 recheck)" if tc_used
+                                    else "knn_scan_kernel (exact f32, CUDA cores)"),
+                         "kernel_ms": kern, "alg_bytes_per_point": 4 * d + 8 * k,
+                         "embed_ms": emb, "embed_hbm_frac": n * (4 * d + 8) / (emb * 1e-3) / 1e9 / hbm_peak},
+            "compute_roofline": {"exact_equiv_Tops": exact_ops, "fp32_peak_Tops_at_sampled_clock": fp32_peak,
+                                 "exact_equiv_frac": exact_ops / fp32_peak,
+                                 "tensor_TFLOPs": gemm_tflops if tc_used else 0.0,
+                                 "tensor_frac_of_bf16_peak": (gemm_tflops / bf16_peak) if tc_used else 0.0,
+                                 "note": "exact_equiv = 3*g*d f32 ops per point / embed time (what the exact "
+                                         "CUDA-core path must issue); tensor = split-bf16 x.L^T MMA flops / k-NN time"},
             "clocks": clocks,
             "gpu_launches": args.steps * loop.launches_per_frame,
             "e2e": e2e,

@@ -88,6 +88,10 @@ int esom_embed_prepared(const float *X, int64_t n, int32_t d, const float *hi, c
                         double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
                         cudaStream_t stream);
 
+/* Number of kernels one esom_embed_prepared(n, ...) call launches (evidence
+ * for the benchmark's launch count). */
+int32_t esom_embed_launches(int64_t n, int32_t g, int32_t d, int32_t k);
+
 /* esom_prepare_model + esom_embed_prepared in one workspace of
  * esom_embed_workspace_bytes(n, g, d, k) bytes. */
 size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k);

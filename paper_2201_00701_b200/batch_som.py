@@ -115,8 +115,13 @@ class FrameLoop:
 
     @property
     def launches_per_frame(self) -> int:
-        # embed (+ memset acc, update, pack, pair table) -- our own kernels only
-        return 4 if self.train else 1
+        """Our own kernels per frame: the embed's k-NN + projection (per chunk),
+        plus, when training, the landmark update and the model re-preparation
+        (pack tiles, pair table, tensor-core operands)."""
+        g, d = self.model.hi.shape
+        n = self.X.shape[0]
+        embed = _lib.load().esom_embed_launches(n, g, d, self.model.k)
+        return embed + (4 if self.train else 0)
 
     def frame(self) -> torch.Tensor:
         m = self.model

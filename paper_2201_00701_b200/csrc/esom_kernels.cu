@@ -702,7 +702,7 @@ size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs)
 // the k-NN scan and the projection kernel
 static int64_t embed_chunk(int32_t k) {
     const char* e = getenv("ESOM_EMBED_CHUNK");
-    const int64_t c = e ? atoll(e) : (int64_t)(24u << 20) / (8 * (int64_t)k);
+    const int64_t c = e ? atoll(e) : (int64_t)(48u << 20) / (8 * (int64_t)k);
     return c < 1024 ? 1024 : c;
 }
 
@@ -852,6 +852,21 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         if (int e = dispatch_project(p.kp, q, stream)) return e;
     }
     return ESOM_OK;
+}
+
+int32_t esom_embed_launches(int64_t n, int32_t g, int32_t d, int32_t k) {
+    // kernels launched by one esom_embed_prepared call: per chunk the k-NN scan
+    // (or tensor-core screen) + the projection (+ 3 BMU-sort kernels when the
+    // pair table lives in L2)
+    if (n <= 0) return 0;
+    const int64_t chunk = n < embed_chunk(k) ? n : embed_chunk(k);
+    const int64_t chunks = (n + chunk - 1) / chunk;
+    const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
+    const bool sorted = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && g <= 8192;
+    (void)d;
+    int64_t per = 2 + (sorted ? 3 : 0);
+    if (sorted && chunk < 4096) per = 2;
+    return (int32_t)(chunks * per);
 }
 
 size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k) {

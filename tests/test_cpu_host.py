@@ -17,7 +17,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def declared_symbols():
     text = (ROOT / "include" / "esom.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*\*?\s*(esom_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int|size_t|const char \*)\s*\*?\s*(esom_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -44,6 +44,7 @@ def test_library_is_sm100a():
     sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "FFMA2" in sass and "FADD2" in sass  # packed f32x2 distance arithmetic
     assert "UBLKCP" in sass                     # TMA bulk copies staging the landmark tiles
+    assert "UTCHMMA" in sass and "LDTM" in sass  # tcgen05.mma (split-bf16 screen) + TMEM loads
 
 
 def test_host_validation_matches_reference():
