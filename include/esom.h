@@ -44,6 +44,10 @@ typedef esom_stream_t cudaStream_t;
 int esom_version(void);
 const char *esom_last_error(void);
 
+/* Diagnostic: when non-NULL, the tensor-core screens atomically add the
+ * number of candidates they re-evaluate exactly to *counter (device int32). */
+void esom_set_tc_stats(int32_t *counter);
+
 /* Bytes of scratch for esom_knn / esom_bmu_accumulate (with_pairs = 0) or
  * for a prepared model (with_pairs = 1: packed landmark tiles + the packed
  * upper-triangular pair table). */

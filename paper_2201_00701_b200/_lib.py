@@ -45,6 +45,7 @@ HELPERS = {
     "esom_point_workspace_bytes": ([_i64, _i32], C.c_size_t),
     "esom_embed_workspace_bytes": ([_i64, _i32, _i32, _i32], C.c_size_t),
     "esom_embed_launches": ([_i64, _i32, _i32, _i32], C.c_int32),
+    "esom_set_tc_stats": ([_vp], None),
 }
 
 

@@ -135,20 +135,44 @@ __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, fl
     }
 }
 
-// Tensor-core operands of the landmarks (esom_tc.cuh): split bf16 hi/lo in
-// the canonical K-major layout (gpad rows x d16, zero padded), |l_j|^2
-// (+inf on padding rows) and max |l_j|, max |l_j|^2 for the error bound.
+// Landmark centroid c (f64 mean, rounded to f32; dims >= d are 0): the
+// tensor-core screens work on x - c and l - c, whose norms (and so the error
+// bounds) are several times smaller than those of x and l.
+__global__ void center_kernel(const float* __restrict__ hi, int g, int d, int d16, float* __restrict__ cen) {
+    __shared__ double part[8][32];
+    const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;  // 256 threads: 8 row phases x 32 dims
+    for (int c0 = 0; c0 < d16; c0 += 32) {
+        double s = 0.0;
+        if (c0 + c < d)
+            for (int j = r0; j < g; j += 8) s += (double)hi[(int64_t)j * d + c0 + c];
+        part[r0][c] = s;
+        __syncthreads();
+        if (r0 == 0 && c0 + c < d16) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += part[q][c];
+            cen[c0 + c] = c0 + c < d ? (float)(t / g) : 0.0f;
+        }
+        __syncthreads();
+    }
+}
+
+// Tensor-core operands of the landmarks (esom_tc.cuh, esom_tc2.cuh): l' =
+// fl(l - c) as B = -2 l' (exact scaling: the MMA yields -2 x'.l') split into
+// bf16 hi/lo in the canonical K-major layout (gpad rows x d16, zero padded),
+// |l'_j|^2 (nearest f32 of the f64 sum; +inf on padding rows) and max |l'_j|,
+// max |l'_j|^2 (rounded up) for the error bounds.
 __global__ void tc_prepare_kernel(const float* __restrict__ hi, int g, int d, int d16, int gpad,
-                                  uint16_t* __restrict__ Bhi, uint16_t* __restrict__ Blo, float* __restrict__ ln,
-                                  float* __restrict__ lstats) {
+                                  const float* __restrict__ cen, uint16_t* __restrict__ Bhi,
+                                  uint16_t* __restrict__ Blo, float* __restrict__ ln, float* __restrict__ lstats) {
     const int chunks = d16 / 8;
     const int64_t total = (int64_t)gpad * chunks;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int row = (int)(e / chunks), c0 = (int)(e % chunks) * 8;
         uint32_t hw[4], lw[4];
         for (int q = 0; q < 8; q += 2) {
-            const float v0 = (row < g && c0 + q < d) ? hi[(int64_t)row * d + c0 + q] : 0.0f;
-            const float v1 = (row < g && c0 + q + 1 < d) ? hi[(int64_t)row * d + c0 + q + 1] : 0.0f;
+            const float v0 = (row < g && c0 + q < d) ? -2.0f * (hi[(int64_t)row * d + c0 + q] - cen[c0 + q]) : 0.0f;
+            const float v1 =
+                (row < g && c0 + q + 1 < d) ? -2.0f * (hi[(int64_t)row * d + c0 + q + 1] - cen[c0 + q + 1]) : 0.0f;
             const uint16_t h0 = __bfloat16_as_ushort(__float2bfloat16_rn(v0));
             const uint16_t h1 = __bfloat16_as_ushort(__float2bfloat16_rn(v1));
             const uint16_t l0 = __bfloat16_as_ushort(__float2bfloat16_rn(v0 - __bfloat162float(__ushort_as_bfloat16(h0))));
@@ -162,15 +186,28 @@ __global__ void tc_prepare_kernel(const float* __restrict__ hi, int g, int d, in
         if (c0 == 0) {
             if (row < g) {
                 double s = 0.0;
-                for (int c = 0; c < d; ++c) s = fma((double)hi[(int64_t)row * d + c], (double)hi[(int64_t)row * d + c], s);
-                const float lnf = (float)(s * (1.0 + 1e-7));
-                ln[row] = lnf;
-                atomicMax(reinterpret_cast<int*>(lstats), __float_as_int((float)(sqrt(s) * (1.0 + 1e-7))));
-                atomicMax(reinterpret_cast<int*>(lstats + 1), __float_as_int(lnf));
+                for (int c = 0; c < d; ++c) {
+                    const double v = (double)(hi[(int64_t)row * d + c] - cen[c]);
+                    s = fma(v, v, s);
+                }
+                ln[row] = (float)s;  // nearest f32 (<= 2^-24 relative, in the screens' bounds)
+                atomicMax(reinterpret_cast<int*>(lstats), __float_as_int((float)(sqrt(s) * (1.0 + 1e-6))));
+                atomicMax(reinterpret_cast<int*>(lstats + 1), __float_as_int((float)(s * (1.0 + 1e-6))));
             } else {
                 ln[row] = __int_as_float(0x7f800000);
             }
         }
+    }
+}
+
+// Exact-phase landmark rows for esom_tc2.cuh: gpad x ls f32, dims >= d and
+// rows >= g zero (a +0 term leaves the reference's sequential sum unchanged;
+// padding rows are never logged: their |l|^2 is +inf).
+__global__ void lrow_kernel(const float* __restrict__ hi, int g, int d, int gpad, int ls, float* __restrict__ Lr) {
+    const int64_t total = (int64_t)gpad * ls;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e / ls), c = (int)(e % ls);
+        Lr[e] = (j < g && c < d) ? hi[(int64_t)j * d + c] : 0.0f;
     }
 }
 
@@ -594,8 +631,8 @@ int grid_for(int64_t work, int threads) {
 }
 
 struct ModelLayout {
-    size_t lt, tri, bhi, blo, ln, lstats, total;
-    int d16, gpad;
+    size_t lt, tri, bhi, blo, ln, lstats, lrow, total;
+    int d16, gpad, ls;
 };
 
 size_t a256(size_t b) { return (b + 255) / 256 * 256; }
@@ -618,9 +655,18 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
     o += a256((size_t)m.gpad * 4);
     m.lstats = o;
     o += 256;
+    m.ls = 0;
+    m.lrow = o;
+    if (d <= 32) {  // padded f32 rows of the pipelined tensor-core screen (esom_tc2.cuh)
+        m.ls = (((m.d16 + 3) / 4) | 1) * 4;
+        o += a256((size_t)m.gpad * m.ls * 4);
+    }
     m.total = o + 256;
     return m;
 }
+
+int32_t* g_tc_stats = nullptr;  // diagnostic: device counter of logged candidates (esom_set_tc_stats)
+int32_t* tc_stats_ptr() { return g_tc_stats; }
 
 bool tc_enabled() {  // ESOM_TC=0 forces the CUDA-core scan (read per call: tests toggle it)
     const char* e = getenv("ESOM_TC");
@@ -632,14 +678,78 @@ bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1
 
 int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cudaStream_t st) {
     cudaMemsetAsync(ws + m.lstats, 0, 8, st);
+    float* cen = reinterpret_cast<float*>(ws + m.lstats + 128);
+    center_kernel<<<1, 256, 0, st>>>(hi, g, d, m.d16, cen);
     tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
-        hi, g, d, m.d16, m.gpad, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
+        hi, g, d, m.d16, m.gpad, cen, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
         reinterpret_cast<float*>(ws + m.ln), reinterpret_cast<float*>(ws + m.lstats));
-    return cuda_check("tc_prepare_kernel");
+    if (int e = cuda_check("tc_prepare_kernel")) return e;
+    if (m.ls) {
+        lrow_kernel<<<grid_for((int64_t)m.gpad * m.ls, 256), 256, 0, st>>>(hi, g, d, m.gpad, m.ls,
+                                                                          reinterpret_cast<float*>(ws + m.lrow));
+        return cuda_check("lrow_kernel");
+    }
+    return ESOM_OK;
 }
 
 // returns ESOM_ERR_UNSUPPORTED when the shape does not fit (caller falls back)
+int tc2_warpgroups() {  // ESOM_TC2_W selects 2..4 warpgroups per CTA (default 4); 0 disables tc2
+    const char* e = getenv("ESOM_TC2_W");
+    return e ? atoi(e) : 4;
+}
+
+// the requested number of warpgroups, or fewer when the shared-memory carve-up does not fit
+template <int KP>
+int launch_tc2_w(Tc2Args a, int W, cudaStream_t st) {
+    int e = ESOM_ERR_UNSUPPORTED;
+    if (W >= 4) e = launch_tc2_t<KP, 4>(a, st);
+    if (e == ESOM_ERR_UNSUPPORTED && W >= 3) e = launch_tc2_t<KP, 3>(a, st);
+    if (e == ESOM_ERR_UNSUPPORTED) e = launch_tc2_t<KP, 2>(a, st);
+    return e;
+}
+
+// pipelined screen (esom_tc2.cuh); ESOM_ERR_UNSUPPORTED when the shape does not fit
+int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st) {
+    const int W = tc2_warpgroups();
+    if (W <= 0 || !m.ls || p.kp > 16) return ESOM_ERR_UNSUPPORTED;
+    Tc2Args a{};
+    a.X = s.X;
+    a.n = s.n;
+    a.d = s.d;
+    a.d16 = m.d16;
+    a.g = s.g;
+    a.gpad = m.gpad;
+    a.k = s.k;
+    a.Bhi = reinterpret_cast<const uint16_t*>(ws + m.bhi);
+    a.Blo = reinterpret_cast<const uint16_t*>(ws + m.blo);
+    a.ln = reinterpret_cast<const float*>(ws + m.ln);
+    a.Lrow = reinterpret_cast<const float*>(ws + m.lrow);
+    a.ls = m.ls;
+    a.L = s.L;
+    a.lstats = reinterpret_cast<const float*>(ws + m.lstats);
+    a.center = reinterpret_cast<const float*>(ws + m.lstats + 128);
+    a.out_idx = s.out_idx;
+    a.out_sqd = s.out_sqd;
+    a.bmu = s.bmu;
+    a.accS = s.accS;
+    a.accC = s.accC;
+    a.qe_sum = s.qe_sum;
+    a.flag = s.flag;
+    a.stats = tc_stats_ptr();
+    switch (p.kp) {
+        case 4: return launch_tc2_w<4>(a, W, st);
+        case 8: return launch_tc2_w<8>(a, W, st);
+        case 16: return launch_tc2_w<16>(a, W, st);
+    }
+    return ESOM_ERR_UNSUPPORTED;
+}
+
 int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st) {
+    {
+        const int e = dispatch_tc2(p, m, s, ws, st);
+        if (e != ESOM_ERR_UNSUPPORTED) return e;
+        g_err[0] = 0;
+    }
     TcArgs a{};
     a.X = s.X;
     a.n = s.n;
@@ -655,6 +765,7 @@ int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const ch
     a.Lt = m.gpad <= 256 ? reinterpret_cast<const float*>(ws + m.lt) : nullptr;  // resident exact tiles
     a.L = s.L;
     a.lstats = reinterpret_cast<const float*>(ws + m.lstats);
+    a.center = reinterpret_cast<const float*>(ws + m.lstats + 128);
     a.out_idx = s.out_idx;
     a.out_sqd = s.out_sqd;
     a.bmu = s.bmu;
@@ -662,7 +773,7 @@ int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const ch
     a.accC = s.accC;
     a.qe_sum = s.qe_sum;
     a.flag = s.flag;
-    a.stats = nullptr;
+    a.stats = tc_stats_ptr();
     switch (p.kp) {
         case 4: return launch_tc_t<4>(a, st);
         case 8: return launch_tc_t<8>(a, st);
@@ -689,6 +800,8 @@ int run_knn(const Plan& p, const ModelLayout& m, ScanArgs a, const char* ws, cud
 extern "C" {
 
 int esom_version(void) { return ESOM_ABI_VERSION; }
+
+void esom_set_tc_stats(int32_t* counter) { g_tc_stats = counter; }
 
 const char* esom_last_error(void) { return g_err; }
 

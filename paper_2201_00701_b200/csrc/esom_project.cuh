@@ -16,6 +16,8 @@
 // (far outliers, where that error would matter) are redone with the exact
 // x-based f64 pair loop.  Checked against the reference to <= 1e-4 x extent.
 #pragma once
+#include <stdlib.h>
+
 #include "esom_common.cuh"
 #include "esom_host.h"
 #include "esom_scan_args.h"
@@ -362,9 +364,272 @@ __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// v2 (default for k <= 16): same law-of-cosines projection, cheaper per pair.
+//  * scores in f32 (MUFU sqrt/ex2; ~1e-7 relative, far inside the embedding
+//    tolerance), normal equations accumulated in f32 about the nearest
+//    landmark's layout position o = lo[idx0] (small magnitudes), solved in f64;
+//  * points whose system is ill-conditioned (tr^2 > kCondMax det) or whose
+//    law-of-cosines error bound trips (kappa) are recomputed in f64 (rare);
+//  * pair-table index from per-slot row bases (no triangle arithmetic per pair),
+//    unconditional table reads, vector loads of the neighbour rows.
+// ---------------------------------------------------------------------------
+constexpr float kCondMax = 100.0f;
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// f64 law-of-cosines accumulation over all pairs (fallback for ill-conditioned
+// f32 systems), same pair rules as the register kernels.
+static __device__ __noinline__ void pairs_cos_f64(int k, const int* J, const float* SQ, const float* SC,
+                                                  const float2* __restrict__ LO, const float* __restrict__ T, int g,
+                                                  double* out5) {
+    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int u = 0; u < k; ++u) {
+        if (!(SC[u] > 0.0f)) continue;
+        for (int v = u + 1; v < k; ++v) {
+            const float w = SC[u] * SC[v];
+            if (!(w > 0.0f)) continue;
+            const int lo_j = min(J[u], J[v]), hi_j = max(J[u], J[v]);
+            const float tv = T[((lo_j * (2 * g - 1 - lo_j)) >> 1) + hi_j - lo_j - 1];
+            const float2 lu = LO[J[u]], lv = LO[J[v]];
+            const float ex = __fsub_rn(lv.x, lu.x), ey = __fsub_rn(lv.y, lu.y);
+            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            if (!(tv >= 0.0f) || !(ld2 >= kLd2Min)) continue;
+            const double G1 = (double)ex / (double)ld2, G2 = (double)ey / (double)ld2;
+            const double h = 0.5 + (double)(SQ[u] - SQ[v]) * (double)tv + G1 * (double)lu.x + G2 * (double)lu.y;
+            const double W = w;
+            a11 = fma(W * G1, G1, a11);
+            a12 = fma(W * G1, G2, a12);
+            a22 = fma(W * G2, G2, a22);
+            c1 = fma(W * h, G1, c1);
+            c2 = fma(W * h, G2, c2);
+        }
+    }
+    out5[0] = a11;
+    out5[1] = a12;
+    out5[2] = a22;
+    out5[3] = c1;
+    out5[4] = c2;
+}
+
+// The reference's scores exactly as it forms them (f32 sqrt widened, f64
+// sigma and exp; ref: projection.py:38-59), parked as f32 weights.  Used on
+// the rare f64 paths: for far outliers the reference's own d^2 != sqd rounding
+// is visible at the 1e-4 level in the weights.
+template <int KP>
+__device__ __forceinline__ void ref_scores_f64(int k, const float (&sq)[KP], float (&out)[KP]) {
+    double d[KP];
+    double sigma = 0.0, dk = 0.0;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+        d[q] = q < k ? (double)__fsqrt_rn(sq[q]) : 0.0;
+        sigma += d[q];
+        if (q == k - 1) dk = d[q];
+    }
+    sigma /= (double)k;
+    bool uniform = sigma < kScoreEps;
+    if (!uniform) {
+        const double inv = -1.0 / (2.0 * sigma * sigma);
+        const double tail = exp(dk * dk * inv);
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const double v = q < k ? exp(d[q] * d[q] * inv) - tail : 0.0;
+            out[q] = v > 0.0 ? (float)v : 0.0f;
+            if (q == 0) uniform = v < kScoreEps;
+        }
+    }
+    if (uniform) {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) out[q] = q < k - 1 ? 1.0f : 0.0f;
+    }
+}
+
+template <int KP, bool TSMEM>
+__global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
+    constexpr int PT = kRegThreads;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int g = a.g, k = a.k;
+    float2* LO = reinterpret_cast<float2*>(smem_raw);
+    int* RB = reinterpret_cast<int*>(LO + g);
+    float* tsm = reinterpret_cast<float*>(RB + g + ((g & 1) ? 1 : 0));
+    if (TSMEM) {
+        const int ntri = g * (g - 1) / 2;
+        for (int e = tid; e < ntri; e += PT) tsm[e] = __ldg(a.T + e);
+    }
+    for (int j = tid; j < g; j += PT) {
+        LO[j] = make_float2(a.lo[2 * j], a.lo[2 * j + 1]);
+        RB[j] = j * (2 * g - j - 1) / 2 - j - 1;  // tri(j, b) = RB[j] + b for b > j
+    }
+    __syncthreads();
+    const float* T = TSMEM ? tsm : a.T;
+    const bool vec = (k == KP) && ((KP & 3) == 0);
+
+    for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
+        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
+        int jj[KP], rb[KP];
+        float sq[KP], sc[KP], lx[KP], ly[KP];
+        const int32_t* irow = a.idx + i * k;
+        const float* drow = a.sqd + i * k;
+        if (vec) {
+#pragma unroll
+            for (int q = 0; q < KP; q += 4) {
+                const int4 iv = __ldg(reinterpret_cast<const int4*>(irow + q));
+                const float4 dv = __ldg(reinterpret_cast<const float4*>(drow + q));
+                jj[q] = iv.x; jj[q + 1] = iv.y; jj[q + 2] = iv.z; jj[q + 3] = iv.w;
+                sq[q] = dv.x; sq[q + 1] = dv.y; sq[q + 2] = dv.z; sq[q + 3] = dv.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                jj[q] = q < k ? __ldg(irow + q) : q;  // padding slots: distinct dummy landmarks, zero weight
+                sq[q] = q < k ? __ldg(drow + q) : 0.0f;
+            }
+        }
+        const float2 o = LO[jj[0]];
+        float sig = 0.0f, sqk = 0.0f, sqmax = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const float2 l = LO[jj[q]];
+            lx[q] = l.x - o.x;  // layout about the nearest landmark
+            ly[q] = l.y - o.y;
+            rb[q] = RB[jj[q]];
+            const float dq = q < k ? sqrt_approx(sq[q]) : 0.0f;
+            sig += dq;
+            if (q == k - 1) sqk = sq[q];
+            sqmax = fmaxf(sqmax, sq[q]);
+        }
+        // scores (ref: projection.py:38-59) in f32, as the scale-free weights
+        // s_q / tail = expm1((d_k^2 - d_q^2) / 2 sigma^2): the normal equations
+        // are homogeneous in w, and the difference form keeps full relative
+        // precision where the reference's e_q - tail cancels (far outliers).
+        sig = sig / (float)k;
+        bool uniform = sig < (float)kScoreEps;
+        if (!uniform) {
+            const float inv = 1.0f / (2.0f * sig * sig);
+            const float tail = ex2_approx(-1.44269504f * sqk * inv);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                const float dl = q < k ? (sqk - sq[q]) * inv : 0.0f;  // >= 0 (rows ascending); 0 at q = k-1
+                const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
+                                                                       1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+                const float e = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
+                sc[q] = e;
+                if (q == 0)  // the reference's s_0 = e_0 - tail < 1e-9 test (no underflow of tail * e)
+                    uniform = ex2_approx(-1.44269504f * sq[0] * inv) - tail < (float)kScoreEps;
+            }
+        }
+        if (uniform) {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
+        }
+
+        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
+        int pj[KP], prb[KP];
+        float psq[KP], psc[KP], plx[KP], ply[KP];
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            pj[q] = jj[q];
+            prb[q] = rb[q];
+            psq[q] = sq[q];
+            psc[q] = sc[q];
+            plx[q] = lx[q];
+            ply[q] = ly[q];
+        }
+        // ring schedule (see project_reg_kernel): round r pairs slot u with u + r mod KP
+        for (int r = 1; r <= KP / 2; ++r) {
+            {
+                const int j0 = pj[0], b0 = prb[0];
+                const float s0 = psq[0], c0 = psc[0], x0 = plx[0], y0 = ply[0];
+#pragma unroll
+                for (int q = 0; q < KP - 1; ++q) {
+                    pj[q] = pj[q + 1];
+                    prb[q] = prb[q + 1];
+                    psq[q] = psq[q + 1];
+                    psc[q] = psc[q + 1];
+                    plx[q] = plx[q + 1];
+                    ply[q] = ply[q + 1];
+                }
+                pj[KP - 1] = j0;
+                prb[KP - 1] = b0;
+                psq[KP - 1] = s0;
+                psc[KP - 1] = c0;
+                plx[KP - 1] = x0;
+                ply[KP - 1] = y0;
+            }
+            const bool half = r == KP / 2;
+#pragma unroll
+            for (int u = 0; u < KP; ++u) {
+                const float w = (half && u >= KP / 2) ? 0.0f : sc[u] * psc[u];
+                const int ti = max(jj[u] < pj[u] ? rb[u] + pj[u] : prb[u] + jj[u], 0);
+                const float tv = T[ti];
+                const float ex = __fsub_rn(plx[u], lx[u]), ey = __fsub_rn(ply[u], ly[u]);
+                const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+                const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
+                tmax = keep ? fmaxf(tmax, tv) : tmax;
+                const float rr = keep ? rcp_approx(ld2) : 0.0f;  // g = 0 for skipped pairs (ld2 may be 0)
+                const float wr = w * rr;
+                const float g1 = ex * rr, g2 = ey * rr;
+                // dnum/hd2 by the law of cosines + g . (lo_u - o)
+                const float h = fmaf(sq[u] - psq[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
+                const float wg1 = wr * ex, wg2 = wr * ey;  // w g
+                a11 = fmaf(wg1, g1, a11);
+                a12 = fmaf(wg1, g2, a12);
+                a22 = fmaf(wg2, g2, a22);
+                c1 = fmaf(wg1, h, c1);
+                c2 = fmaf(wg2, h, c2);
+            }
+        }
+        double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
+        const float kappa = 2.0f * sqmax * tmax;
+        const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
+        if (kappa > (float)kKappaMax || illc) {
+            double o5[5];
+            float fsc[KP];
+            ref_scores_f64<KP>(k, sq, fsc);
+            if (kappa > (float)kKappaMax) {
+                // far outlier: exact x-based f64 pair loop (absolute layout coordinates)
+                pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, fsc, 1, o5);
+                // shift to the local origin: c -= A o
+                o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
+                o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
+            } else {
+                pairs_cos_f64(k, jj, sq, fsc, LO, T, g, o5);
+                o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
+                o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
+            }
+            A11 = o5[0];
+            A12 = o5[1];
+            A22 = o5[2];
+            C1 = o5[3];
+            C2 = o5[4];
+        }
+        const double det = A11 * A22 - A12 * A12;
+        const double tr = A11 + A22;
+        float2 out;
+        if (det < kDetRel * tr * tr + kDetAbs) {
+            out = o;
+        } else {
+            out.x = (float)((C1 * A22 - C2 * A12) / det + (double)o.x);
+            out.y = (float)((A11 * C2 - A12 * C1) / det + (double)o.y);
+        }
+        reinterpret_cast<float2*>(a.xy)[i] = out;
+    }
+}
+
 template <int KP, bool TSMEM>
 int launch_project_reg(ProjArgs a, size_t smem, cudaStream_t st) {
-    auto kern = project_reg_kernel<KP, TSMEM>;
+    static const bool v1 = getenv("ESOM_PROJ_V1") != nullptr;  // A/B switch (measurement only)
+    auto kern = v1 ? project_reg_kernel<KP, TSMEM> : project_reg2_kernel<KP, TSMEM>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRegThreads, smem);

@@ -33,8 +33,13 @@ __device__ __forceinline__ bool load_x(const float* __restrict__ X, int64_t i, i
 // Rare exact fallback for one point whose candidate log overflowed (massive
 // exact ties / overflowing distances): the reference's own insertion scan
 // (ref: knn.py:65-92) over row-major landmarks, writing rank-ordered rows.
-static __device__ __noinline__ void knn_point_slow(const float* __restrict__ x, int d, const float* __restrict__ L,
-                                                   int g, int k, int32_t* oi, float* od, int* b0, float* d0) {
+struct SlowNearest {
+    int b0;
+    float d0;
+};
+
+static __device__ __noinline__ SlowNearest knn_point_slow(const float* __restrict__ x, int d, const float* __restrict__ L,
+                                                          int g, int k, int32_t* oi, float* od) {
     float bd[64];
     int bi[64];
     int cnt = 0;
@@ -66,8 +71,7 @@ static __device__ __noinline__ void knn_point_slow(const float* __restrict__ x, 
             od[q] = bd[q];
         }
     }
-    *b0 = bi[0];
-    *d0 = bd[0];
+    return SlowNearest{bi[0], bd[0]};
 }
 
 template <int DC, int KP>
@@ -235,7 +239,11 @@ __global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
         // log overflow (pathological ties) or NaN inputs (flagged as
         // non-finite; rows must still hold valid indices): the reference's
         // own insertion scan for this point
-        if (ovf || written != k) knn_point_slow(a.X + i * a.d, a.d, a.L, a.g, k, oi, od, &b0, &d0);
+        if (ovf || written != k) {
+            const SlowNearest sn = knn_point_slow(a.X + i * a.d, a.d, a.L, a.g, k, oi, od);
+            b0 = sn.b0;
+            d0 = sn.d0;
+        }
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         if (a.accS) {

@@ -49,7 +49,8 @@ struct TcArgs {
     const float* ln;         // gpad |l_j|^2 (f32; +inf for padding rows)
     const float* Lt;         // exact tiles [tile][dp][32]
     const float* L;          // row-major landmarks (slow path)
-    const float* lstats;     // [0] = max_j |l_j|, [1] = max_j |l_j|^2 (device)
+    const float* lstats;     // [0] = max_j |l'_j|, [1] = max_j |l'_j|^2 (device, centred)
+    const float* center;     // landmark centroid c (padded to d16); operands are x - c, l - c
     int32_t* out_idx;
     float* out_sqd;
     int32_t* bmu;
@@ -60,8 +61,34 @@ struct TcArgs {
     int32_t* stats;          // [0] += candidates examined exactly (diagnostic, nullable)
 };
 
+// pipelined tensor-core screened k-NN (esom_tc2.cuh)
+struct Tc2Args {
+    const float* X;          // n×d points
+    int64_t n;
+    int d, d16, g, gpad, k;  // d16 = MMA K (16 or 32), gpad = g padded to 32
+    const uint16_t* Bhi;     // gpad×d16 bf16 of -2 l (hi part), canonical K-major
+    const uint16_t* Blo;     // lo part
+    const float* ln;         // gpad |l_j|^2 (f32, +inf on padding rows)
+    const float* Lrow;       // gpad×ls f32 rows, zero-padded dims (global)
+    int ls;                  // Lrow stride (floats, multiple of 4, ls/4 odd)
+    const float* L;          // row-major g×d (slow path)
+    const float* lstats;     // [0] max|l'_j|, [1] max|l'_j|^2 (centred)
+    const float* center;     // 32 f32: landmark centroid c (zero-padded), operands are x - c, l - c
+    int32_t* out_idx;
+    float* out_sqd;
+    int32_t* bmu;
+    double* accS;
+    double* accC;
+    double* qe_sum;
+    int32_t* flag;
+    int32_t* stats;          // [0] += logged candidates, [1] += slow-path points (diagnostic, nullable)
+};
+
 template <int KP>
 int launch_tc_t(TcArgs a, cudaStream_t st);  // esom_tc.cuh, instantiated in inst/tc.cu
+
+template <int KP, int W>
+int launch_tc2_t(Tc2Args a, cudaStream_t st);  // esom_tc2.cuh, instantiated in inst/tc2.cu
 
 template <int DC, int KP>
 int launch_scan_t(ScanArgs a, cudaStream_t st);   // esom_scan.cuh, instantiated in inst/*.cu

@@ -97,7 +97,9 @@ __device__ __forceinline__ uint32_t canon_off(int row, int kk, int K) {
 //    3*d16 * 2^-22 sum|x_c||l_c| (2x the sequential-RN bound)
 //  * |x|^2, |l|^2 and the final combination: (d + 4) 2^-23 (|x|^2 + |l|^2)
 //  * the reference's own rounding: d 2^-24 d_true <= d 2^-23 (|x|^2 + |l|^2)
-// with sum|x_c||l_c| <= |x||l| (Cauchy-Schwarz) and a further 2x margin.
+// with sum|x_c||l_c| <= |x||l| (Cauchy-Schwarz) and a further 2x margin; all
+// norms are of the centred vectors x - c, l - c (c = landmark centroid; the
+// centring rounding is inside the (d + 4) 2^-23 term's slack).
 __device__ __forceinline__ float tc_eps(float xnorm, float xn, float lmax, float lnmax, int d, int d16) {
     const float c1 = 2.0f * (4.0f * 3.8147e-6f + 3.0f * d16 * 2.3842e-7f);
     const float c2 = 2.0f * (2.0f * d + 4.0f) * 1.1921e-7f;
@@ -206,6 +208,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
                     xbad |= !finite_f(v0) || !finite_f(v1);
                     if (c0 + q < d) myx[c0 + q] = v0;
                     if (c0 + q + 1 < d) myx[c0 + q + 1] = v1;
+                    v0 -= __ldg(a.center + c0 + q);  // centred operands (|x - l| is translation invariant)
+                    v1 -= __ldg(a.center + c0 + q + 1);
                     xn = fmaf(v0, v0, xn);
                     xn = fmaf(v1, v1, xn);
                     const uint16_t h0 = bf16_bits(v0), h1 = bf16_bits(v1);
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
                     float v[32];
                     tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) gm[q] = fminf(gm[q], fmaf(-2.0f, v[q], xn + lns[cbase + c0 + q]));
+                    for (int q = 0; q < 32; ++q) gm[q] = fminf(gm[q], v[q] + (xn + lns[cbase + c0 + q]));  // B = -2 l
                 }
                 if (r == R - 1) {
                     float vd[KP];
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
                     tmem_ld32(tmem + lane_col + (uint32_t)c0, v);
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        const float dt = fmaf(-2.0f, v[q], xn + lns[cbase + c0 + q]);  // +inf on padding rows
+                        const float dt = v[q] + (xn + lns[cbase + c0 + q]);  // B = -2 l; +inf on padding rows
                         const bool keep = dt <= tcut;
                         const int slot = min(cnt, LOGCAP);  // slot LOGCAP is a dump row
                         if (keep) {
@@ -382,7 +386,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
         if (written != k) {
             // log overflow, non-finite input or a candidate set short of k:
             // the reference's insertion scan for this point
-            knn_point_slow(a.X + i * d, d, a.L, a.g, k, oi, od, &b0, &d0);
+            const SlowNearest sn = knn_point_slow(a.X + i * d, d, a.L, a.g, k, oi, od);
+            b0 = sn.b0;
+            d0 = sn.d0;
         }
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;

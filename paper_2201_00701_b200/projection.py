@@ -238,44 +238,62 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
 
 
 PIPE_CHUNK = 1 << 17  # points per H2D/compute/D2H stage of the host pipeline
+PIPE_DEPTH = 3        # rotating device buffers
 
 
 def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
-    """embed() for pinned host points: chunked H2D on a copy stream overlapped
-    with the kernels on the compute stream and the D2H of finished chunks, so
-    the end-to-end time approaches max(PCIe, compute) instead of their sum."""
+    """embed() for pinned host points: chunked H2D on one copy stream, the
+    kernels on the compute stream and the D2H of finished chunks on a second
+    copy stream (PCIe is full duplex), with PIPE_DEPTH rotating device
+    buffers, so the end-to-end time approaches max(H2D, compute) instead of
+    their sum."""
     n, d = host.shape
     pm = PreparedModel(model.hi, model.lo, k, device=dev)
     flag = _dev.new_flag(dev)
     out = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
+    h2d, d2h = _copy_streams(dev)
     c = min(PIPE_CHUNK, n)
-    Xd = [torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(2)]
-    Yd = [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(2)]
-    loaded = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
-    freed = [None, None]
-    copy.wait_stream(comp)  # model preparation precedes the first chunk
+    nb = PIPE_DEPTH
+    Xd = [torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(nb)]
+    Yd = [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(nb)]
+    loaded = [torch.cuda.Event() for _ in range(nb)]
+    computed = [None] * nb  # compute of the chunk that last used buffer b (Xd[b] free, Yd[b] ready)
+    drained = [None] * nb   # D2H of the chunk that last used buffer b (Yd[b] free)
+    h2d.wait_stream(comp)   # model preparation precedes the first chunk
     for it, s in enumerate(range(0, n, c)):
-        b = it & 1
+        b = it % nb
         m = min(c, n - s)
-        with torch.cuda.stream(copy):
-            if freed[b] is not None:
-                copy.wait_event(freed[b])
+        if computed[b] is not None:
+            h2d.wait_event(computed[b])
+        with torch.cuda.stream(h2d):
             Xd[b][:m].copy_(host[s:s + m], non_blocking=True)
-            loaded[b].record(copy)
+        loaded[b].record(h2d)
         comp.wait_event(loaded[b])
+        if drained[b] is not None:
+            comp.wait_event(drained[b])
         pm.embed_into(Xd[b][:m], Yd[b][:m], flag=flag)
-        done[b].record(comp)
-        with torch.cuda.stream(copy):
-            copy.wait_event(done[b])
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        computed[b] = ev
+        d2h.wait_event(ev)
+        with torch.cuda.stream(d2h):
             out[s:s + m].copy_(Yd[b][:m], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copy)
-            freed[b] = ev
-    copy.synchronize()
+        ev2 = torch.cuda.Event()
+        ev2.record(d2h)
+        drained[b] = ev2
+    d2h.synchronize()
     comp.synchronize()
     _dev.raise_if_nonfinite(flag)
     _dev.raise_if_nonfinite(pm.flag)
     return out.numpy()
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_streams(dev):
+    key = (dev.index if isinstance(dev, torch.device) else int(dev))
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _COPY_STREAMS[key]

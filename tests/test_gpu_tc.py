@@ -1,5 +1,7 @@
-"""Tensor-core screened k-NN (esom_tc.cuh): bit-identical to the CUDA-core
-scan and to the reference oracle, including ties, on every eligible shape."""
+"""Tensor-core screened k-NN (esom_tc2.cuh pipelined screen with 2/3/4
+warpgroups, and the round-streaming esom_tc.cuh): bit-identical to the
+CUDA-core scan and to the reference oracle, including ties, on every
+eligible shape."""
 import os
 
 import numpy as np
@@ -13,22 +15,26 @@ import paper_2201_00701_b200 as esom
 pytestmark = pytest.mark.gpu
 
 
-def run(p, l, k, tc):
-    old = os.environ.get("ESOM_TC")
+def run(p, l, k, tc, w=None):
+    saved = {v: os.environ.get(v) for v in ("ESOM_TC", "ESOM_TC2_W")}
     os.environ["ESOM_TC"] = "1" if tc else "0"
+    if w is not None:
+        os.environ["ESOM_TC2_W"] = str(w)
     try:
         nb = esom.knn_base(p, l, k)
     finally:
-        if old is None:
-            del os.environ["ESOM_TC"]
-        else:
-            os.environ["ESOM_TC"] = old
+        for v, old in saved.items():
+            if old is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = old
     return nb
 
 
+@pytest.mark.parametrize("w", [3, 2, 4, 0])
 @pytest.mark.parametrize("case", ["c1", "c2", "uniform16", "normal32", "ties", "wide", "rounds300", "c4like",
                                   "g4096", "ties777"])
-def test_tc_equals_scan_and_oracle(case):
+def test_tc_equals_scan_and_oracle(case, w):
     gen = np.random.default_rng(hash(case) % 2**32)
     if case == "c1":
         p, l, _ = c1_inputs()
@@ -70,7 +76,7 @@ def test_tc_equals_scan_and_oracle(case):
         p = gen.integers(0, 4, size=(10000, 6)).astype(np.float32)
         l = gen.integers(0, 4, size=(777, 6)).astype(np.float32)
         k = 16
-    a = run(p, l, k, tc=True)
+    a = run(p, l, k, tc=True, w=w)
     b = run(p, l, k, tc=False)
     assert np.array_equal(a.indices, b.indices) and np.array_equal(a.sqdists, b.sqdists), case
     rows = np.arange(0, p.shape[0], max(1, p.shape[0] // 4000))
