@@ -138,21 +138,20 @@ __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, fl
 // Landmark centroid c (f64 mean, rounded to f32; dims >= d are 0): the
 // tensor-core screens work on x - c and l - c, whose norms (and so the error
 // bounds) are several times smaller than those of x and l.
-__global__ void center_kernel(const float* __restrict__ hi, int g, int d, int d16, float* __restrict__ cen) {
+__global__ void center_kernel(const float* __restrict__ hi, int g, int d, int dpad, float* __restrict__ cen) {
+    // one block per 32 dims: 8 row phases x 32 dims, f64 partial sums
     __shared__ double part[8][32];
-    const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;  // 256 threads: 8 row phases x 32 dims
-    for (int c0 = 0; c0 < d16; c0 += 32) {
-        double s = 0.0;
-        if (c0 + c < d)
-            for (int j = r0; j < g; j += 8) s += (double)hi[(int64_t)j * d + c0 + c];
-        part[r0][c] = s;
-        __syncthreads();
-        if (r0 == 0 && c0 + c < d16) {
-            double t = 0.0;
-            for (int q = 0; q < 8; ++q) t += part[q][c];
-            cen[c0 + c] = c0 + c < d ? (float)(t / g) : 0.0f;
-        }
-        __syncthreads();
+    const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+    const int c0 = blockIdx.x * 32;
+    double s = 0.0;
+    if (c0 + c < d)
+        for (int j = r0; j < g; j += 8) s += (double)hi[(int64_t)j * d + c0 + c];
+    part[r0][c] = s;
+    __syncthreads();
+    if (r0 == 0 && c0 + c < dpad) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += part[q][c];
+        cen[c0 + c] = c0 + c < d ? (float)(t / g) : 0.0f;
     }
 }
 
@@ -633,6 +632,11 @@ int grid_for(int64_t work, int threads) {
 struct ModelLayout {
     size_t lt, tri, bhi, blo, ln, lstats, lrow, total;
     int d16, gpad, ls;
+    // tensor-core GEMM screen for d > 32 (esom_tc3.cuh): per-model operands + per-chunk scratch
+    bool t3;
+    int dk, gp3;
+    int64_t t3chunk;
+    size_t cen3, b3hi, b3lo, ln3, ls3, a3hi, a3lo, xn3, cand3, cnt3, bmu3, perm3, hist3;
 };
 
 size_t a256(size_t b) { return (b + 255) / 256 * 256; }
@@ -661,6 +665,27 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
         m.ls = (((m.d16 + 3) / 4) | 1) * 4;
         o += a256((size_t)m.gpad * m.ls * 4);
     }
+    m.t3 = d > 32 && k <= 32 && g <= 65535;
+    if (m.t3) {
+        m.dk = (d + 31) / 32 * 32;
+        m.gp3 = (g + 255) / 256 * 256;
+        int64_t ch = (int64_t)(((size_t)512 << 20) / ((size_t)m.dk * 4 + 160));
+        ch = ch >= (1 << 18) ? (1 << 18) : (ch < 4096 ? 4096 : ch / 256 * 256);
+        m.t3chunk = ch;
+        m.cen3 = o;  o += a256((size_t)m.dk * 4);
+        m.b3hi = o;  o += a256((size_t)m.gp3 * m.dk * 2);
+        m.b3lo = o;  o += a256((size_t)m.gp3 * m.dk * 2);
+        m.ln3 = o;   o += a256((size_t)m.gp3 * 4);
+        m.ls3 = o;   o += 256;
+        m.a3hi = o;  o += a256((size_t)ch * m.dk * 2);
+        m.a3lo = o;  o += a256((size_t)ch * m.dk * 2);
+        m.xn3 = o;   o += a256((size_t)ch * 4);
+        m.cand3 = o; o += a256((size_t)ch * 64 * 2);
+        m.cnt3 = o;  o += a256((size_t)ch * 4);
+        m.bmu3 = o;  o += a256((size_t)ch * 4);
+        m.perm3 = o; o += a256((size_t)ch * 4);
+        m.hist3 = o; o += a256((size_t)m.gp3 * 4);
+    }
     m.total = o + 256;
     return m;
 }
@@ -679,7 +704,7 @@ bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1
 int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cudaStream_t st) {
     cudaMemsetAsync(ws + m.lstats, 0, 8, st);
     float* cen = reinterpret_cast<float*>(ws + m.lstats + 128);
-    center_kernel<<<1, 256, 0, st>>>(hi, g, d, m.d16, cen);
+    center_kernel<<<(m.d16 + 31) / 32, 256, 0, st>>>(hi, g, d, m.d16, cen);
     tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
         hi, g, d, m.d16, m.gpad, cen, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
         reinterpret_cast<float*>(ws + m.ln), reinterpret_cast<float*>(ws + m.lstats));
@@ -782,12 +807,93 @@ int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const ch
     return set_err(ESOM_ERR_UNSUPPORTED, "no tensor-core kernel for k%s", "");
 }
 
+// per-model operands of the d > 32 GEMM screen: centroid, B = -2 (l - c) split tiles, norms
+int prepare_tc3(const float* hi, int g, int d, const ModelLayout& m, char* ws, int32_t* flag, cudaStream_t st) {
+    if (!m.t3) return ESOM_OK;
+    cudaMemsetAsync(ws + m.ls3, 0, 8, st);
+    float* cen = reinterpret_cast<float*>(ws + m.cen3);
+    center_kernel<<<(m.dk + 31) / 32, 256, 0, st>>>(hi, g, d, m.dk, cen);
+    if (int e = cuda_check("center_kernel")) return e;
+    return t3_split(hi, g, m.gp3, d, m.dk, cen, -2.0f, 256, reinterpret_cast<uint16_t*>(ws + m.b3hi),
+                    reinterpret_cast<uint16_t*>(ws + m.b3lo), reinterpret_cast<float*>(ws + m.ln3), 1,
+                    reinterpret_cast<float*>(ws + m.ls3), flag, st);
+}
+
+bool t3_enabled() {  // ESOM_TC3=0 forces the CUDA-core scan for d > 32
+    const char* e = getenv("ESOM_TC3");
+    return tc_enabled() && (e ? atoi(e) != 0 : true);
+}
+
+// d > 32: split points -> tcgen05 GEMM screen -> approximate-BMU sort -> warp-exact re-evaluation,
+// in chunks of m.t3chunk points (the chunk scratch lives in the model workspace)
+int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_t st) {
+    char* ws = const_cast<char*>(wsc);
+    for (int64_t s = 0; s < a.n; s += m.t3chunk) {
+        const int64_t cn = a.n - s < m.t3chunk ? a.n - s : m.t3chunk;
+        const int64_t cpad = (cn + 255) / 256 * 256;
+        const float* X = a.X + s * a.d;
+        if (int e = t3_split(X, cn, cpad, a.d, m.dk, reinterpret_cast<const float*>(ws + m.cen3), 1.0f, 128,
+                             reinterpret_cast<uint16_t*>(ws + m.a3hi), reinterpret_cast<uint16_t*>(ws + m.a3lo),
+                             reinterpret_cast<float*>(ws + m.xn3), 0, nullptr, a.flag, st))
+            return e;
+        Tc3Args t{};
+        t.Ahi = reinterpret_cast<const uint16_t*>(ws + m.a3hi);
+        t.Alo = reinterpret_cast<const uint16_t*>(ws + m.a3lo);
+        t.xnorm = reinterpret_cast<const float*>(ws + m.xn3);
+        t.n = cn;
+        t.d = a.d;
+        t.dk = m.dk;
+        t.gpad = m.gp3;
+        t.k = a.k;
+        t.Bhi = reinterpret_cast<const uint16_t*>(ws + m.b3hi);
+        t.Blo = reinterpret_cast<const uint16_t*>(ws + m.b3lo);
+        t.ln = reinterpret_cast<const float*>(ws + m.ln3);
+        t.lstats = reinterpret_cast<const float*>(ws + m.ls3);
+        t.cand = reinterpret_cast<uint16_t*>(ws + m.cand3);
+        t.ccount = reinterpret_cast<int32_t*>(ws + m.cnt3);
+        t.bmu_approx = reinterpret_cast<int32_t*>(ws + m.bmu3);
+        t.stats = tc_stats_ptr();
+        const int kp = kp_for(a.k);
+        int e = kp == 4 ? launch_gemm_t<4>(t, st) : kp == 8 ? launch_gemm_t<8>(t, st)
+              : kp == 16 ? launch_gemm_t<16>(t, st) : launch_gemm_t<32>(t, st);
+        if (e) return e;
+        // visit points grouped by approximate nearest landmark: a CTA's candidate rows repeat (L1 hits)
+        int32_t* cntb = reinterpret_cast<int32_t*>(ws + m.hist3);
+        int32_t* perm = reinterpret_cast<int32_t*>(ws + m.perm3);
+        cudaMemsetAsync(cntb, 0, (size_t)a.g * 4, st);
+        bmu_hist_kernel<<<num_sms() * 2, 512, (size_t)a.g * 4, st>>>(t.bmu_approx, cn, 1, a.g, cntb);
+        bmu_scan_kernel<<<1, 1024, 0, st>>>(cntb, a.g);
+        bmu_scatter_kernel<<<grid_for(cn, 256), 256, 0, st>>>(t.bmu_approx, cn, 1, cntb, perm);
+        if (int e2 = cuda_check("t3 bmu sort")) return e2;
+        T3ExactArgs x{};
+        x.X = X;
+        x.n = cn;
+        x.d = a.d;
+        x.dpad = (a.d + 3) / 4 * 4;
+        x.g = a.g;
+        x.k = a.k;
+        x.L = a.L;
+        x.cand = t.cand;
+        x.ccount = t.ccount;
+        x.perm = perm;
+        x.out_idx = a.out_idx ? a.out_idx + s * a.k : nullptr;
+        x.out_sqd = a.out_sqd ? a.out_sqd + s * a.k : nullptr;
+        x.bmu = a.bmu ? a.bmu + s : nullptr;
+        x.qe_sum = a.qe_sum;
+        x.accS = a.accS;
+        x.accC = a.accC;
+        if (int e3 = launch_exact_warp_t<32>(x, st)) return e3;
+    }
+    return ESOM_OK;
+}
+
 // k-NN over a prepared model workspace: tensor-core screen when eligible, else the CUDA-core scan
 int run_knn(const Plan& p, const ModelLayout& m, ScanArgs a, const char* ws, cudaStream_t st) {
     if (tc_eligible(a.n, a.d, a.g, a.k)) {
         const int e = dispatch_tc(p, m, a, ws, st);
         if (e != ESOM_ERR_UNSUPPORTED) return e;
     }
+    if (m.t3 && t3_enabled() && a.n >= 256 && a.d <= 1536) return run_t3(m, a, ws, st);
     return dispatch_scan(p, a, st);
 }
 
@@ -870,6 +976,8 @@ int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, in
     if (int e = cuda_check("pack_landmarks")) return e;
     if (tc_eligible(n, d, g, k))
         if (int e = prepare_tc(L, g, d, m, ws, stream)) return e;
+    if (m.t3 && t3_enabled())
+        if (int e = prepare_tc3(L, g, d, m, ws, nonfinite_flag, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, L, g, k, Lt, nonfinite_flag);
     a.out_idx = idx;
     a.out_sqd = sqd;
@@ -908,6 +1016,8 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     if (int e = cuda_check("pair_table")) return e;
     if (tc_eligible(1 << 20, d, g, k))
         if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
+    if (m.t3 && t3_enabled())
+        if (int e = prepare_tc3(hi, g, d, m, ws, nonfinite_flag, stream)) return e;
     return ESOM_OK;
 }
 
@@ -1012,6 +1122,8 @@ int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, i
     if (int e = cuda_check("pack_landmarks")) return e;
     if (tc_eligible(n, d, g, 1))
         if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
+    if (m.t3 && t3_enabled())
+        if (int e = prepare_tc3(hi, g, d, m, ws, nonfinite_flag, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, hi, g, 1, Lt, nonfinite_flag);
     a.bmu = bmu;
     a.accS = acc_S;

@@ -84,6 +84,47 @@ struct Tc2Args {
     int32_t* stats;          // [0] += logged candidates, [1] += slow-path points (diagnostic, nullable)
 };
 
+// tensor-core GEMM screen for d > 32 (esom_tc3.cuh)
+struct Tc3Args {
+    const uint16_t* Ahi;     // points x - c, split bf16, [128-row tile][32-wide K chunk] canonical
+    const uint16_t* Alo;
+    const float* xnorm;      // n: |x - c| (rounded up)
+    int64_t n;
+    int d, dk, gpad, k;      // dk = d padded to 32, gpad = g padded to 256
+    const uint16_t* Bhi;     // -2 (l - c) split bf16, [256-row round][K chunk] canonical
+    const uint16_t* Blo;
+    const float* ln;         // gpad: |l - c|^2 (+inf padding)
+    const float* lstats;     // [0] max|l - c|, [1] max|l - c|^2
+    uint16_t* cand;          // n x 64 candidate landmark indices (index order)
+    int32_t* ccount;         // n: candidates, -1 = reference scan needed
+    int32_t* bmu_approx;     // n: landmark of the smallest screened distance
+    int32_t* stats;          // [0] += candidates, [1] += overflowed points (nullable)
+};
+
+struct T3ExactArgs {
+    const float* X;          // n x d points
+    int64_t n;
+    int d, dpad, g, k;       // dpad: d rounded up to 4 (smem row of one warp)
+    const float* L;          // g x d landmarks (row-major)
+    const uint16_t* cand;
+    const int32_t* ccount;
+    const int32_t* perm;     // visiting order (approximate-BMU sorted; nullable)
+    int32_t* out_idx;        // n x k (nullable: statistics only)
+    float* out_sqd;
+    int32_t* bmu;
+    double* qe_sum;
+    double* accS;
+    double* accC;
+};
+
+template <int KP>
+int launch_gemm_t(Tc3Args a, cudaStream_t st);        // esom_tc3.cuh, instantiated in inst/tc3.cu
+template <int KP>
+int launch_exact_warp_t(T3ExactArgs a, cudaStream_t st);
+// operand split of esom_tc3.cuh (rows x - c or -2 (l - c), canonical bf16 tiles, norms)
+int t3_split(const float* X, int64_t n, int64_t npad, int d, int dk, const float* cen, float scale, int rows_blk,
+             uint16_t* Hi, uint16_t* Lo, float* nrm, int nrm_sq, float* lstats, int32_t* flag, cudaStream_t st);
+
 template <int KP>
 int launch_tc_t(TcArgs a, cudaStream_t st);  // esom_tc.cuh, instantiated in inst/tc.cu
 

@@ -1,0 +1,757 @@
+// esom_tc3.cuh -- tensor-core GEMM screen for high-dimensional EXACT k-NN
+// (d > 32, e.g. C5: 2^20 x 512, 4096 landmarks, k = 32; tensor
+// bound).  Same exactness contract as esom_tc.cuh / esom_tc2.cuh: the tensor
+// cores only prune, the output equals knn_base (ref: knn.py:65-92) bit for bit.
+//
+// Pipeline (three kernels per <= kT3Chunk points, all on the caller's stream):
+//  1. t3_split_points: x' = x - c (c = landmark centroid) as split bf16
+//     (hi, lo) in canonical K-major tiles [128-point tile][32-wide K chunk],
+//     |x'| per point.  Landmarks were split the same way per model (B = -2 l',
+//     tiles [256-landmark round][K chunk]).
+//  2. knn_gemm_kernel: a persistent, warp-specialised tcgen05 GEMM.  A CTA owns
+//     256 points (two M = 128 tiles sharing every B chunk); one producer warp
+//     streams A/B chunks with 1-D TMA bulk copies through a 2-stage smem ring,
+//     one MMA warp issues 3 x kind::f16 MMAs per 16-wide K step per tile
+//     (x_hi l_hi + x_hi l_lo + x_lo l_hi) into TMEM (2 x 256 columns), and
+//     8 epilogue warps (thread = point = TMEM lane) read the accumulators:
+//       pass 1 (all landmark rounds): minima of 64 landmark groups j = q mod 64
+//         -> tau = k-th smallest group minimum >= k-th smallest D~;
+//       pass 2 (GEMM recomputed): log every landmark with D~_j <= tau + 2E
+//         (E: per-point error bound, t3_eps), refine to the k-th smallest
+//         logged D~ and write the candidate list (u16, <= kT3CMax per point)
+//         plus the approximate nearest landmark (for a locality sort).
+//  3. knn_exact_warp_kernel: one warp per point in approximate-BMU order (so a
+//     CTA's points share candidate rows in L1); lane e re-evaluates candidate
+//     e with the reference's sequential f32 sum (ref: knn.py:56-62), then the
+//     warp ranks (distance, index) across lanes and writes the k-NN row.
+// A point whose log overflows or whose candidate list exceeds kT3CMax is
+// flagged and re-done by the reference insertion scan (knn_point_slow).
+#pragma once
+#include "esom_tc2.cuh"
+
+namespace esom {
+
+constexpr int kT3Kc = 32;            // K elements per pipeline stage
+constexpr int kT3Rows = 256;         // landmarks per round (MMA N)
+constexpr int kT3Stages = 2;
+constexpr int kT3Epi = 256;          // epilogue threads: two 128-point tiles
+constexpr int kT3Threads = kT3Epi + 64;
+constexpr int kT3CMax = 64;          // candidates handed to the exact kernel per point
+constexpr int kT3LogCap = 64;        // per-thread candidate log in smem
+constexpr int kT3Groups = 64;        // landmark groups of the pass-1 bound
+constexpr uint32_t kT3AChunk = 128u * kT3Kc * 2u;   // one A tile chunk (hi or lo), bytes
+constexpr uint32_t kT3BChunk = 256u * kT3Kc * 2u;   // one B round chunk (hi or lo), bytes
+constexpr uint32_t kT3Stage = 4u * kT3AChunk + 2u * kT3BChunk;
+
+// Rigorous-by-model bound E on |D~_j - (d_ref_j - |x'|^2)|:
+//  split residual 8 2^-18 S; tensor-core accumulation budgeted at 4 2^-23 (N + 2S)
+//  per MMA instruction (3 dk/16 of them); |l'|^2 rounding and the epilogue add
+//  2^-23 (N + |D|); the reference's own sequential rounding (d + 3) 2^-24 d_true
+//  with d_true <= |x'|^2 + tau + 4 + E0; all x2.
+__device__ __forceinline__ float t3_eps(float xnorm, float lmax, float lnmax, int d, int dk, float tau) {
+    const float S = xnorm * lmax;
+    const float nm = 3.0f * (float)(dk >> 4);
+    const float e0 = 8.0f * 3.8147e-6f * S + 4.0f * nm * 1.1921e-7f * (lnmax + 2.0f * S) +
+                     1.1921e-7f * (2.0f * lnmax + xnorm * xnorm + fabsf(tau));
+    const float dtrue = fmaxf(xnorm * xnorm + tau, 0.0f) + 4.0f * e0 + 1.0f;
+    return 2.0f * (e0 + (d + 3.0f) * 5.9605e-8f * dtrue);
+}
+
+template <int KP>
+struct T3Compacted {
+    int m;
+    float tcut;
+};
+
+// log full: tighten the cut to the k-th smallest logged D~ (+2E) and keep the
+// survivors in index order (rare; out of line)
+template <int KP>
+__device__ __noinline__ T3Compacted<KP> t3_compact(float* logv, unsigned short* logj, int cnt, int k, float E2,
+                                                   float tcut) {
+    float vd[KP];
+    vlist_init<KP>(vd, k);
+    for (int e = 0; e < cnt; ++e) vlist_insert<KP>(vd, logv[e * kT3Epi]);
+    const float tau = vd[KP - 1];
+    const float nt = tau + E2 + 9.6e-7f * fabsf(tau);
+    T3Compacted<KP> r;
+    r.tcut = nt < tcut ? nt : tcut;
+    int m = 0;
+    for (int e = 0; e < cnt; ++e) {
+        const float v = logv[e * kT3Epi];
+        if (v <= r.tcut) {
+            logv[m * kT3Epi] = v;
+            logj[m * kT3Epi] = logj[e * kT3Epi];
+            ++m;
+        }
+    }
+    r.m = m;
+    return r;
+}
+
+// k-th smallest of the 64 group minima (vlist for k < KP; two sorted halves for k == 32)
+template <int KP>
+__device__ __forceinline__ float kth_of_64(const float (&gm)[kT3Groups], int k) {
+    float vd[KP];
+    vlist_init<KP>(vd, k);
+#pragma unroll
+    for (int q = 0; q < kT3Groups; ++q) vlist_insert<KP>(vd, gm[q]);
+    return vd[KP - 1];
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kT3Stages], empty[kT3Stages], tmem_full, tmem_empty;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int nkc = a.dk / kT3Kc;                 // K chunks
+    const int R = a.gpad / kT3Rows;               // landmark rounds
+    const int64_t nsup = (a.n + 255) / 256;       // 256-point super tiles
+    unsigned char* stage = smem_raw;
+    float* logv = reinterpret_cast<float*>(smem_raw + kT3Stages * kT3Stage);
+    unsigned short* logj = reinterpret_cast<unsigned short*>(logv + kT3LogCap * kT3Epi);
+
+    if (tid == 0) {
+        for (int s = 0; s < kT3Stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&tmem_full, 1);
+        mbar_init(&tmem_empty, kT3Epi);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == kT3Epi / 32) {
+        // ---------------- producer: TMA bulk copies of A / B chunks ----------------
+        if ((tid & 31) == 0) {
+            uint32_t q = 0;
+            for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int r = 0; r < R; ++r)
+                        for (int kc = 0; kc < nkc; ++kc, ++q) {
+                            const int s = (int)(q % kT3Stages);
+                            mbar_wait(&empty[s], ((q / kT3Stages) & 1u) ^ 1u);
+                            unsigned char* sb = stage + (size_t)s * kT3Stage;
+                            mbar_expect_tx(&full[s], kT3Stage);
+                            for (int t = 0; t < 2; ++t) {
+                                const size_t ao = ((size_t)(2 * st + t) * nkc + kc) * (kT3AChunk / 2);
+                                tma_bulk_g2s(sb + (2 * t) * kT3AChunk, a.Ahi + ao, kT3AChunk, &full[s]);
+                                tma_bulk_g2s(sb + (2 * t + 1) * kT3AChunk, a.Alo + ao, kT3AChunk, &full[s]);
+                            }
+                            const size_t bo = ((size_t)r * nkc + kc) * (kT3BChunk / 2);
+                            tma_bulk_g2s(sb + 4 * kT3AChunk, a.Bhi + bo, kT3BChunk, &full[s]);
+                            tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BChunk, a.Blo + bo, kT3BChunk, &full[s]);
+                        }
+        }
+    } else if (warp == kT3Epi / 32 + 1) {
+        // ---------------- MMA issuer ----------------
+        if ((tid & 31) == 0) {
+            uint32_t q = 0, rr = 0;
+            const uint32_t idesc = umma_idesc_bf16(128, kT3Rows);
+            const uint32_t sboA = (kT3Kc / 8) * 128, sboB = (kT3Kc / 8) * 128, lbo = 128;
+            for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int r = 0; r < R; ++r, ++rr) {
+                        mbar_wait(&tmem_empty, (rr & 1u) ^ 1u);  // epilogue has read the previous round
+                        tc_fence_after();
+                        for (int kc = 0; kc < nkc; ++kc, ++q) {
+                            const int s = (int)(q % kT3Stages);
+                            mbar_wait(&full[s], (q / kT3Stages) & 1u);
+                            tc_fence_after();
+                            const uint32_t sb = smem_u32(stage + (size_t)s * kT3Stage);
+                            const uint32_t bh = sb + 4 * kT3AChunk, bl = bh + kT3BChunk;
+                            for (int ks = 0; ks < kT3Kc / 16; ++ks) {
+                                const uint32_t ko = (uint32_t)ks * 256u;
+                                for (int t = 0; t < 2; ++t) {
+                                    const uint32_t ah = sb + (2 * t) * kT3AChunk, al = ah + kT3AChunk;
+                                    const uint32_t dcol = tmem + (uint32_t)(kT3Rows * t);
+                                    const uint32_t acc0 = (kc | ks) ? 1u : 0u;
+                                    umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
+                                              acc0);
+                                    umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bl + ko, lbo, sboB), idesc, 1);
+                                    umma_bf16(dcol, umma_desc(al + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc, 1);
+                                }
+                            }
+                            umma_commit(&empty[s]);  // stage reusable once these MMAs retire
+                        }
+                        umma_commit(&tmem_full);
+                    }
+        }
+    } else {
+        // ---------------- epilogue: thread = point = TMEM lane ----------------
+        const int t = tid >> 7;              // tile within the super tile
+        const int lane_row = tid & 127;
+        const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+        const uint32_t tcol = tmem + lane_off + (uint32_t)(kT3Rows * t);
+        const float lmax = __ldg(a.lstats), lnmax = __ldg(a.lstats + 1);
+        float* lv = logv + tid;
+        unsigned short* lj = logj + tid;
+        const int k = a.k;
+        uint32_t rr = 0;
+        int stat_local = 0, ovf_local = 0;
+        for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x) {
+            const int64_t i = st * 256 + t * 128 + lane_row;
+            const bool valid = i < a.n;
+            const float xnorm = valid ? __ldg(a.xnorm + i) : 0.0f;
+            float gm[kT3Groups];
+#pragma unroll
+            for (int q = 0; q < kT3Groups; ++q) gm[q] = kInf;
+            // ---- pass 1: group minima over all rounds ----
+            for (int r = 0; r < R; ++r, ++rr) {
+                mbar_wait(&tmem_full, rr & 1u);
+                tc_fence_after();
+                const float* lnr = a.ln + (size_t)r * kT3Rows;
+#pragma unroll 1
+                for (int c0 = 0; c0 < kT3Rows; c0 += 64) {
+                    uint32_t v0[32], v1[32];
+                    tmem_ld32_async(tcol + (uint32_t)c0, v0);
+                    tmem_ld32_async(tcol + (uint32_t)(c0 + 32), v1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {  // column c0 + q -> group q, c0 + 32 + q -> group 32 + q
+                        gm[q] = fminf(gm[q], __uint_as_float(v0[q]) + __ldg(lnr + c0 + q));
+                        gm[32 + q] = fminf(gm[32 + q], __uint_as_float(v1[q]) + __ldg(lnr + c0 + 32 + q));
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&tmem_empty);
+            }
+            const float tau = kth_of_64<KP>(gm, k);
+            const float E2 = 2.0f * t3_eps(xnorm, lmax, lnmax, a.d, a.dk, tau);
+            float tcut = tau + E2 + 9.6e-7f * fabsf(tau);
+            // ---- pass 2: log candidates (index order) ----
+            int cnt = 0;
+            bool ovf = false;
+            for (int r = 0; r < R; ++r, ++rr) {
+                mbar_wait(&tmem_full, rr & 1u);
+                tc_fence_after();
+                const float* lnr = a.ln + (size_t)r * kT3Rows;
+#pragma unroll 1
+                for (int c0 = 0; c0 < kT3Rows; c0 += 32) {
+                    uint32_t v0[32];
+                    tmem_ld32_async(tcol + (uint32_t)c0, v0);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float v = __uint_as_float(v0[q]) + __ldg(lnr + c0 + q);
+                        if (v <= tcut) {
+                            if (cnt == kT3LogCap) {
+                                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, E2, tcut);
+                                cnt = cr.m;
+                                tcut = cr.tcut;
+                                ovf |= cnt == kT3LogCap;
+                            }
+                            if (cnt < kT3LogCap && v <= tcut) {
+                                lv[cnt * kT3Epi] = v;
+                                lj[cnt * kT3Epi] = (unsigned short)(r * kT3Rows + c0 + q);
+                                ++cnt;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&tmem_empty);
+            }
+            if (!valid) continue;
+            // ---- refine and hand the candidates to the exact kernel ----
+            if (!ovf && cnt > k) {
+                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, E2, tcut);
+                cnt = cr.m;
+            }
+            int best = 0;
+            float bv = kInf;
+            unsigned short* outc = a.cand + (size_t)i * kT3CMax;
+            const bool fits = !ovf && cnt <= kT3CMax;
+            for (int e = 0; e < cnt; ++e) {
+                const float v = lv[e * kT3Epi];
+                const unsigned short j = lj[e * kT3Epi];
+                if (v < bv) {
+                    bv = v;
+                    best = j;
+                }
+                if (fits) outc[e] = j;
+            }
+            a.ccount[i] = fits ? cnt : -1;  // -1: exact kernel runs the reference scan for this point
+            a.bmu_approx[i] = best;
+            stat_local += cnt;
+            ovf_local += fits ? 0 : 1;
+        }
+        if (a.stats) {
+            if (stat_local) atomicAdd(a.stats, stat_local);
+            if (ovf_local) atomicAdd(a.stats + 1, ovf_local);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+template <int KP>
+int launch_gemm_t(Tc3Args a, cudaStream_t st) {
+    const size_t smem = (size_t)kT3Stages * kT3Stage + (size_t)kT3LogCap * kT3Epi * 6 + 128;
+    if (smem > (size_t)esom_host::max_smem_optin())
+        return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "gemm screen: shared memory%s", "");
+    auto kern = knn_gemm_kernel<KP>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t nsup = (a.n + 255) / 256;
+    int64_t grid = esom_host::num_sms();
+    if (grid > nsup) grid = nsup;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, kT3Threads, smem, st>>>(a);
+    return esom_host::cuda_check("knn_gemm_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Operand preparation: one warp per row; lane l handles the 8-wide K groups
+// l, l + 32, ... (coalesced 32-byte reads).  Canonical no-swizzle K-major
+// layout per (row block, 32-wide K chunk): [8-row group][8-elem K group][8 rows][8 elems].
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ size_t t3_canon(int64_t row, int c, int rows_blk, int nkc) {
+    const int64_t blk = row / rows_blk;
+    const int r = (int)(row % rows_blk), kc = c / kT3Kc, cc = c % kT3Kc;
+    return ((size_t)blk * nkc + kc) * ((size_t)rows_blk * kT3Kc) +
+           (size_t)(((r >> 3) * (kT3Kc / 8) + (cc >> 3)) * 64 + (r & 7) * 8);
+}
+
+// scale = 1 for points (x - c), -2 for landmarks (B = -2 (l - c)); nrm: |v'| (points) or |l'|^2 (landmarks)
+__global__ void t3_split_kernel(const float* __restrict__ X, int64_t n, int64_t npad, int d, int dk,
+                                const float* __restrict__ cen, float scale, int rows_blk, uint16_t* __restrict__ Hi,
+                                uint16_t* __restrict__ Lo, float* __restrict__ nrm, int nrm_sq, float* __restrict__ lstats,
+                                int32_t* flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wpb = blockDim.x >> 5;
+    const int nkc = dk / kT3Kc;
+    bool bad = false;
+    for (int64_t row = blockIdx.x * wpb + (threadIdx.x >> 5); row < npad; row += (int64_t)gridDim.x * wpb) {
+        const bool valid = row < n;
+        double s = 0.0;
+        for (int c0 = lane * 8; c0 < dk; c0 += 256) {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int c = c0 + q;
+                float x = 0.0f;
+                if (valid && c < d) {
+                    x = X[row * d + c];
+                    bad |= !finite_f(x);
+                    x = x - cen[c];
+                }
+                s += (double)x * (double)x;
+                v[q] = scale * x;
+            }
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+                const uint16_t h0 = bf16_bits(v[q]), h1 = bf16_bits(v[q + 1]);
+                const uint16_t l0 = bf16_bits(v[q] - bf16_val(h0)), l1 = bf16_bits(v[q + 1] - bf16_val(h1));
+                hw[q >> 1] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+                lw[q >> 1] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+            }
+            const size_t o = t3_canon(row, c0, rows_blk, nkc);
+            *reinterpret_cast<uint4*>(Hi + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(Lo + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0 && nrm) {
+            if (nrm_sq) {  // landmark norms |l'|^2 (+inf on padding rows) and the bound's maxima
+                nrm[row] = valid ? (float)s : __int_as_float(0x7f800000);
+                if (valid && lstats) {
+                    atomicMax(reinterpret_cast<int*>(lstats), __float_as_int((float)(sqrt(s) * (1.0 + 1e-6))));
+                    atomicMax(reinterpret_cast<int*>(lstats + 1), __float_as_int((float)(s * (1.0 + 1e-6))));
+                }
+            } else if (valid) {
+                nrm[row] = (float)(sqrt(s) * (1.0 + 1e-6));  // |x'| rounded up
+            }
+        }
+    }
+    if (flag) flag_nonfinite(flag, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Exact re-evaluation: one warp per point (approximate-BMU order), lane e owns
+// candidates e and e + 32; (distance, index) ranks by warp shuffles.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool t3_less(float va, int ja, float vb, int jb) { return va < vb || (va == vb && ja < jb); }
+
+constexpr int kT3ExactWarps = 32;  // one 1024-thread CTA per SM: its warps walk consecutive (BMU-sorted)
+                                   // points, so their candidate rows are shared in L1
+
+template <int KP>
+__global__ void __launch_bounds__(kT3ExactWarps * 32) knn_exact_warp_kernel(T3ExactArgs a) {
+    extern __shared__ __align__(16) float xs_all[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    float* xs = xs_all + (size_t)wib * a.dpad;
+    const int d = a.d, k = a.k;
+    const f2 nz = f2_pack(-0.0f, -0.0f);
+    double qe_local = 0.0;
+    const bool vec = (d & 7) == 0;
+    // contiguous range of the visiting order per CTA
+    const int64_t per = (a.n + gridDim.x - 1) / gridDim.x;
+    const int64_t p0 = (int64_t)blockIdx.x * per, p1 = p0 + per < a.n ? p0 + per : a.n;
+    for (int64_t pos = p0 + wib; pos < p1; pos += kT3ExactWarps) {
+        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
+        const float* xr = a.X + i * d;
+        const int cnt = __ldg(a.ccount + i);
+        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+        int b0 = 0;
+        float d0 = 0.0f;
+        if (cnt < k || cnt > kT3CMax) {
+            if (lane == 0) {
+                const SlowNearest sn = knn_point_slow(xr, d, a.L, a.g, k, oi, od);
+                b0 = sn.b0;
+                d0 = sn.d0;
+            }
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            d0 = __shfl_sync(0xffffffffu, d0, 0);
+        } else {
+            for (int c = lane * 4; c < d; c += 128) {
+                if ((d & 3) == 0) {
+                    *reinterpret_cast<float4*>(xs + c) = __ldg(reinterpret_cast<const float4*>(xr + c));
+                } else {
+                    for (int q = 0; q < 4 && c + q < d; ++q) xs[c + q] = __ldg(xr + c + q);
+                }
+            }
+            __syncwarp();
+            const unsigned short* cr = a.cand + (size_t)i * kT3CMax;
+            const bool h0 = lane < cnt, h1 = lane + 32 < cnt;
+            const int j0 = h0 ? (int)cr[lane] : 0, j1 = h1 ? (int)cr[lane + 32] : 0;
+            float s0 = 0.0f, s1 = 0.0f;
+            const float* l0 = a.L + (size_t)j0 * d;
+            const float* l1 = a.L + (size_t)j1 * d;
+            if (vec) {
+                // 8 dims (one full 32-byte sector of the candidate row) per step
+                auto acc8 = [&](float s, const float* lr, int c, const float4& xa, const float4& xb) {
+                    const float4 la = __ldg(reinterpret_cast<const float4*>(lr + c));
+                    const float4 lb = __ldg(reinterpret_cast<const float4*>(lr + c + 4));
+                    float q0, q1, q2, q3, q4, q5, q6, q7;
+                    f2_unpack(f2_sq(f2_sub(f2_pack(xa.x, xa.y), f2_pack(la.x, la.y)), nz), q0, q1);
+                    f2_unpack(f2_sq(f2_sub(f2_pack(xa.z, xa.w), f2_pack(la.z, la.w)), nz), q2, q3);
+                    f2_unpack(f2_sq(f2_sub(f2_pack(xb.x, xb.y), f2_pack(lb.x, lb.y)), nz), q4, q5);
+                    f2_unpack(f2_sq(f2_sub(f2_pack(xb.z, xb.w), f2_pack(lb.z, lb.w)), nz), q6, q7);
+                    s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, q0), q1), q2), q3);
+                    return __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, q4), q5), q6), q7);
+                };
+                for (int c = 0; c < d; c += 8) {
+                    const float4 xa = *reinterpret_cast<const float4*>(xs + c);
+                    const float4 xb = *reinterpret_cast<const float4*>(xs + c + 4);
+                    s0 = acc8(s0, l0, c, xa, xb);
+                    if (h1) s1 = acc8(s1, l1, c, xa, xb);
+                }
+            } else {
+                for (int c = 0; c < d; ++c) {
+                    const float t0 = __fsub_rn(xs[c], __ldg(l0 + c));
+                    s0 = __fadd_rn(s0, __fmul_rn(t0, t0));
+                    if (h1) {
+                        const float t1 = __fsub_rn(xs[c], __ldg(l1 + c));
+                        s1 = __fadd_rn(s1, __fmul_rn(t1, t1));
+                    }
+                }
+            }
+            const float v0 = h0 ? s0 : kInf, v1 = h1 ? s1 : kInf;
+            const int k0 = h0 ? j0 : 0x7fffffff, k1 = h1 ? j1 : 0x7fffffff;
+            int r0 = 0, r1 = 0;
+            const int nsrc = cnt < 32 ? cnt : 32;
+            for (int sl = 0; sl < nsrc; ++sl) {
+                const float wv0 = __shfl_sync(0xffffffffu, v0, sl), wv1 = __shfl_sync(0xffffffffu, v1, sl);
+                const int wj0 = __shfl_sync(0xffffffffu, k0, sl), wj1 = __shfl_sync(0xffffffffu, k1, sl);
+                r0 += (t3_less(wv0, wj0, v0, k0) ? 1 : 0) + (t3_less(wv1, wj1, v0, k0) ? 1 : 0);
+                r1 += (t3_less(wv0, wj0, v1, k1) ? 1 : 0) + (t3_less(wv1, wj1, v1, k1) ? 1 : 0);
+            }
+            if (h0 && r0 < k && oi) {
+                oi[r0] = j0;
+                od[r0] = v0;
+            }
+            if (h1 && r1 < k && oi) {
+                oi[r1] = j1;
+                od[r1] = v1;
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, h0 && r0 == 0), m1 = __ballot_sync(0xffffffffu, h1 && r1 == 0);
+            const int src = m0 ? __ffs(m0) - 1 : __ffs(m1) - 1;
+            const float sv = m0 ? v0 : v1;
+            const int sj = m0 ? j0 : j1;
+            d0 = __shfl_sync(0xffffffffu, sv, src);
+            b0 = __shfl_sync(0xffffffffu, sj, src);
+        }
+        if (lane == 0) {
+            if (a.bmu) a.bmu[i] = b0;
+            if (a.qe_sum) qe_local += (double)d0;
+            if (a.accC) atomicAdd(a.accC + b0, 1.0);
+        }
+        if (a.accS)
+            for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(xr + c));
+        __syncwarp();
+    }
+    if (a.qe_sum && lane == 0 && qe_local != 0.0) atomicAdd(a.qe_sum, qe_local);
+}
+
+// ---------------------------------------------------------------------------
+// Grouped exact re-evaluation (d % 8 == 0): a warp takes 8 consecutive points
+// of the approximate-BMU order, forms the union U of their candidate lists
+// (<= kT3UMax landmarks; points of one Voronoi cell share most candidates) and
+// lane e evaluates landmark U_e against all 8 points (each candidate row is
+// read once per group, 8 sequential f32 chains per landmark).  U contains
+// every point's true top k, so the top k of U by (distance, index) is exact.
+// ---------------------------------------------------------------------------
+constexpr int kT3GP = 8;       // points per warp group
+constexpr int kT3UMax = 96;    // union capacity (three landmark slots per lane)
+constexpr int kT3GWarps = 6;   // warps per CTA (two CTAs per SM at d = 512)
+
+__device__ __forceinline__ float acc8f(float s, const float4& la, const float4& lb, const float4& xa, const float4& xb,
+                                       f2 nz) {
+    float q0, q1, q2, q3, q4, q5, q6, q7;
+    f2_unpack(f2_sq(f2_sub(f2_pack(xa.x, xa.y), f2_pack(la.x, la.y)), nz), q0, q1);
+    f2_unpack(f2_sq(f2_sub(f2_pack(xa.z, xa.w), f2_pack(la.z, la.w)), nz), q2, q3);
+    f2_unpack(f2_sq(f2_sub(f2_pack(xb.x, xb.y), f2_pack(lb.x, lb.y)), nz), q4, q5);
+    f2_unpack(f2_sq(f2_sub(f2_pack(xb.z, xb.w), f2_pack(lb.z, lb.w)), nz), q6, q7);
+    s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, q0), q1), q2), q3);
+    return __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, q4), q5), q6), q7);
+}
+
+__host__ __device__ constexpr int t3_group_stride(int dpad, int g) {  // floats per warp, 16-B aligned
+    return (kT3GP * dpad + (g + 31) / 32 + kT3UMax + 3) / 4 * 4;
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kT3GWarps * 32) knn_exact_group_kernel(T3ExactArgs a) {
+    extern __shared__ __align__(16) float sm_all[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int d = a.d, k = a.k, dpad = a.dpad;
+    const int gw = (a.g + 31) >> 5;  // bitmap words
+    float* xs = sm_all + (size_t)wib * t3_group_stride(dpad, a.g);
+    uint32_t* bm = reinterpret_cast<uint32_t*>(xs + kT3GP * dpad);
+    int* ul = reinterpret_cast<int*>(bm + gw);
+    const f2 nz = f2_pack(-0.0f, -0.0f);
+    double qe_local = 0.0;
+    const int64_t per = ((a.n + gridDim.x - 1) / gridDim.x + kT3GP - 1) / kT3GP * kT3GP;
+    const int64_t p0 = (int64_t)blockIdx.x * per, p1 = p0 + per < a.n ? p0 + per : a.n;
+    for (int64_t gpos = p0 + (int64_t)wib * kT3GP; gpos < p1; gpos += (int64_t)kT3GWarps * kT3GP) {
+        // ---- the group's points ----
+        int64_t ip = 0;
+        int cp = -1;
+        if (lane < kT3GP && gpos + lane < p1) {
+            ip = a.perm ? (int64_t)__ldg(a.perm + gpos + lane) : gpos + lane;
+            cp = __ldg(a.ccount + ip);
+        }
+        const bool normal_l = lane < kT3GP && cp >= k && cp <= kT3CMax;
+        const unsigned nmask = __ballot_sync(0xffffffffu, normal_l);
+        // stage the normal points' rows once
+        for (int p = 0; p < kT3GP; ++p) {
+            if (!((nmask >> p) & 1u)) continue;
+            const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+            const float* xr = a.X + i * d;
+            for (int c = lane * 4; c < d; c += 128)
+                *reinterpret_cast<float4*>(xs + p * dpad + c) = __ldg(reinterpret_cast<const float4*>(xr + c));
+        }
+        // subsets of the group: all 8, else halves, else single points (a single point's list
+        // has <= kT3CMax <= kT3UMax landmarks, so the split always terminates)
+        unsigned todo[8];
+        int ntodo = 0;
+        if (nmask) todo[ntodo++] = nmask;
+        while (ntodo > 0) {
+            const unsigned sm = todo[--ntodo];
+            // ---- union of the subset's candidates ----
+            __syncwarp();
+            for (int w = lane; w < gw; w += 32) bm[w] = 0u;
+            __syncwarp();
+            for (int p = 0; p < kT3GP; ++p) {
+                if (!((sm >> p) & 1u)) continue;
+                const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+                const int c = __shfl_sync(0xffffffffu, cp, p);
+                const unsigned short* cr = a.cand + (size_t)i * kT3CMax;
+                for (int e = lane; e < c; e += 32) {
+                    const int j = cr[e];
+                    atomicOr(bm + (j >> 5), 1u << (j & 31));
+                }
+            }
+            __syncwarp();
+            int U = 0;
+            for (int w0 = 0; w0 < gw; w0 += 32) {
+                const uint32_t m = w0 + lane < gw ? bm[w0 + lane] : 0u;
+                const int c = __popc(m);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                int pos = U + incl - c;
+                uint32_t mm = m;
+                while (mm) {
+                    const int b = __ffs(mm) - 1;
+                    mm &= mm - 1u;
+                    if (pos < kT3UMax) ul[pos] = ((w0 + lane) << 5) + b;
+                    ++pos;
+                }
+                U += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (U > kT3UMax) {  // split the subset in two halves
+                unsigned lo = 0u, rest = sm;
+                const int half = __popc(sm) / 2;
+                for (int q = 0; q < half; ++q) {
+                    const unsigned bit = rest & (0u - rest);
+                    lo |= bit;
+                    rest ^= bit;
+                }
+                todo[ntodo++] = rest;
+                todo[ntodo++] = lo;
+                continue;
+            }
+            __syncwarp();
+            int jj[3];
+            bool hv[3];
+            const float* lr[3];
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl) {
+                hv[sl] = 32 * sl + lane < U;
+                jj[sl] = hv[sl] ? ul[32 * sl + lane] : 0;
+                lr[sl] = a.L + (size_t)jj[sl] * d;
+            }
+            float acc[3][kT3GP];
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+                for (int p = 0; p < kT3GP; ++p) acc[sl][p] = 0.0f;
+            const bool two = U > 32, three = U > 64;  // warp-uniform slot counts
+            for (int c = 0; c < d; c += 8) {
+                float4 la[3], lb[3];
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl) {
+                    if (sl == 0 || (sl == 1 && two) || (sl == 2 && three)) {
+                        la[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c));
+                        lb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 4));
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < kT3GP; ++p) {
+                    if (!((sm >> p) & 1u)) continue;
+                    const float4 xa = *reinterpret_cast<const float4*>(xs + p * dpad + c);
+                    const float4 xb = *reinterpret_cast<const float4*>(xs + p * dpad + c + 4);
+                    acc[0][p] = acc8f(acc[0][p], la[0], lb[0], xa, xb, nz);
+                    if (two) acc[1][p] = acc8f(acc[1][p], la[1], lb[1], xa, xb, nz);
+                    if (three) acc[2][p] = acc8f(acc[2][p], la[2], lb[2], xa, xb, nz);
+                }
+            }
+            // ---- per point: rank (distance, index) over U, write the k-NN row ----
+#pragma unroll
+            for (int p = 0; p < kT3GP; ++p) {
+                if (!((sm >> p) & 1u)) continue;
+                const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+                float v[3];
+                int key[3], rk[3] = {0, 0, 0};
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl) {
+                    v[sl] = hv[sl] ? acc[sl][p] : kInf;
+                    key[sl] = hv[sl] ? jj[sl] : 0x7fffffff;
+                }
+#pragma unroll
+                for (int ss = 0; ss < 3; ++ss) {
+                    if (32 * ss >= U) break;
+                    const int nsrc = U - 32 * ss < 32 ? U - 32 * ss : 32;
+                    for (int src = 0; src < nsrc; ++src) {
+                        const float wv = __shfl_sync(0xffffffffu, v[ss], src);
+                        const int wj = __shfl_sync(0xffffffffu, key[ss], src);
+#pragma unroll
+                        for (int sl = 0; sl < 3; ++sl) rk[sl] += t3_less(wv, wj, v[sl], key[sl]) ? 1 : 0;
+                    }
+                }
+                int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+                float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+                int src0 = 0, sl0 = 0;
+                bool found = false;
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl) {
+                    if (hv[sl] && rk[sl] < k && oi) {
+                        oi[rk[sl]] = key[sl];
+                        od[rk[sl]] = v[sl];
+                    }
+                    const unsigned m0 = __ballot_sync(0xffffffffu, hv[sl] && rk[sl] == 0);
+                    if (m0 && !found) {
+                        found = true;
+                        src0 = __ffs(m0) - 1;
+                        sl0 = sl;
+                    }
+                }
+                const float dv = sl0 == 0 ? v[0] : (sl0 == 1 ? v[1] : v[2]);
+                const int dj = sl0 == 0 ? key[0] : (sl0 == 1 ? key[1] : key[2]);
+                const float d0 = __shfl_sync(0xffffffffu, dv, src0);
+                const int b0 = __shfl_sync(0xffffffffu, dj, src0);
+                if (lane == 0) {
+                    if (a.bmu) a.bmu[i] = b0;
+                    if (a.qe_sum) qe_local += (double)d0;
+                    if (a.accC) atomicAdd(a.accC + b0, 1.0);
+                }
+                if (a.accS)
+                    for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)xs[p * dpad + c]);
+            }
+        }
+        // ---- points the screen could not bound (log overflow / too few candidates): reference scan ----
+        for (int p = 0; p < kT3GP; ++p) {
+            if (gpos + p >= p1) break;
+            if ((nmask >> p) & 1u) continue;
+            const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+            int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+            float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+            const float* xr = a.X + i * d;
+            int b0 = 0;
+            if (lane == 0) {
+                const SlowNearest sn = knn_point_slow(xr, d, a.L, a.g, k, oi, od);
+                b0 = sn.b0;
+                if (a.bmu) a.bmu[i] = b0;
+                if (a.qe_sum) qe_local += (double)sn.d0;
+                if (a.accC) atomicAdd(a.accC + b0, 1.0);
+            }
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (a.accS)
+                for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(xr + c));
+        }
+        __syncwarp();
+    }
+    if (a.qe_sum && lane == 0 && qe_local != 0.0) atomicAdd(a.qe_sum, qe_local);
+}
+
+template <int KP>
+int launch_exact_warp_t(T3ExactArgs a, cudaStream_t st) {
+    if ((a.d & 7) == 0 && !getenv("ESOM_T3_PERPOINT")) {
+        const size_t per_warp = (size_t)t3_group_stride(a.dpad, a.g) * 4;
+        const size_t smem = (size_t)kT3GWarps * per_warp;
+        if (smem <= (size_t)esom_host::max_smem_optin()) {
+            auto kern = knn_exact_group_kernel<KP>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT3GWarps * 32, smem);
+            if (per_sm < 1) per_sm = 1;
+            int64_t grid = (a.n + kT3GWarps * kT3GP - 1) / (kT3GWarps * kT3GP);
+            const int64_t cap = (int64_t)esom_host::num_sms() * per_sm;
+            if (grid > cap) grid = cap;
+            if (grid < 1) grid = 1;
+            kern<<<(unsigned)grid, kT3GWarps * 32, smem, st>>>(a);
+            return esom_host::cuda_check("knn_exact_group_kernel");
+        }
+    }
+    const size_t smem = (size_t)kT3ExactWarps * a.dpad * 4;
+    auto kern = knn_exact_warp_kernel<KP>;
+    if (smem > (size_t)esom_host::max_smem_optin())
+        return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact re-evaluation: d too large%s", "");
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t grid = (a.n + kT3ExactWarps - 1) / kT3ExactWarps;
+    const int64_t cap = (int64_t)esom_host::num_sms();
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, kT3ExactWarps * 32, smem, st>>>(a);
+    return esom_host::cuda_check("knn_exact_warp_kernel");
+}
+
+}  // namespace esom

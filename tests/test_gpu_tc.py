@@ -97,3 +97,48 @@ def test_tc_embed_and_stats_match_scan():
     del os.environ["ESOM_TC"]
     assert torch.equal(xa, xb)
     assert qa == pytest.approx(qb, rel=1e-12)
+
+
+def run3(p, l, k, tc3):
+    saved = os.environ.get("ESOM_TC3")
+    os.environ["ESOM_TC3"] = "1" if tc3 else "0"
+    try:
+        return esom.knn_base(p, l, k)
+    finally:
+        if saved is None:
+            os.environ.pop("ESOM_TC3", None)
+        else:
+            os.environ["ESOM_TC3"] = saved
+
+
+@pytest.mark.parametrize("case", ["c5like", "d64_g257", "d100_ties", "d48_k5", "d512_uniform"])
+def test_gemm_screen_equals_scan_and_oracle(case):
+    """d > 32: tcgen05 GEMM screen (esom_tc3.cuh) + warp-exact re-evaluation."""
+    gen = np.random.default_rng(abs(hash(case)) % 2**32)
+    if case == "c5like":
+        from paper_2201_00701_b200 import datagen
+        p = datagen.gaussians(32, 1 << 15, 512, seed=5)[0]
+        l = p[gen.choice(p.shape[0], 4096, replace=False)]
+        k = 32
+    elif case == "d64_g257":
+        p = gen.random((20000, 64)).astype(np.float32)
+        l = gen.random((257, 64)).astype(np.float32)
+        k = 16
+    elif case == "d100_ties":
+        p = gen.integers(0, 3, size=(8000, 100)).astype(np.float32)
+        l = gen.integers(0, 3, size=(300, 100)).astype(np.float32)
+        k = 8
+    elif case == "d48_k5":
+        p = (gen.normal(size=(9000, 48)) * 20 + 50).astype(np.float32)
+        l = (gen.normal(size=(700, 48)) * 20 + 50).astype(np.float32)
+        k = 5
+    else:
+        p = gen.random((6000, 512)).astype(np.float32)
+        l = gen.random((1000, 512)).astype(np.float32)
+        k = 32
+    a = run3(p, l, k, tc3=True)
+    b = run3(p, l, k, tc3=False)
+    assert np.array_equal(a.indices, b.indices) and np.array_equal(a.sqdists, b.sqdists), case
+    rows = np.arange(0, p.shape[0], max(1, p.shape[0] // 500))
+    wi, wd = oracle.knn(p[rows], l, k)
+    assert np.array_equal(a.indices[rows], wi) and np.array_equal(a.sqdists[rows], wd), case

@@ -1,0 +1,6 @@
+set -x
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_tc.py -x -q -k gemm > gpurun_out/s19_pytest.log 2>&1; echo pytest=$?
+tail -30 gpurun_out/s19_pytest.log
+PROBE_VARIANTS=scan,w4 timeout 300 python tools/tc_probe.py c5 > gpurun_out/s19_probe.log 2>&1
+cat gpurun_out/s19_probe.log
