@@ -19,6 +19,7 @@ bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -45,7 +46,7 @@ WORKLOADS = {
     "c4": (16, 1_250_000, 32, 32, 32, 16, True,
            "C4 shard: 1.25M x32 per GPU (10M over 8), 1024 landmarks, k=16, batch-SOM step + re-projection"),
     "c5": (32, 1 << 20, 512, 64, 64, 32, False,
-           "C5: 2^20x512, 4096 landmarks, k=32, projection only (CUDA-core exact path)"),
+           "C5: 2^20x512, 4096 landmarks, k=32, projection only (tcgen05 split-bf16 GEMM screen + exact re-evaluation)"),
 }
 
 
@@ -254,47 +255,64 @@ def run_ours(args):
     total_points = n * world
     value = total_points / (ms_max * 1e-3)
 
-    # ---- dominant kernel: the exact k-NN (tensor-core screened where eligible),
-    # timed alone over the whole shard with CUDA events on the launching stream.
-    # Algorithmic bytes of the k-NN API per point: 4d (X) + 8k (idx + sqd),
-    # SURVEY.md §8d.  The embed-level figure (4d + 8 per point) is reported too.
+    # ---- dominant kernel of the frame, timed live with CUDA events on the
+    # launching stream (libesom's esom_timing_* hooks around each launch),
+    # one extra L2-flushed frame after the timed region.  Algorithmic work per
+    # point: k-NN kernels 4d (X) + 8k (idx + sqd) bytes, the
+    # d > 32 GEMM screen 2 g d flops (one x.L^T), the projection 8k + 8 bytes.
     from paper_2201_00701_b200 import _dev as _d, _lib as _l
 
-    idx = torch.empty((n, k), dtype=torch.int32, device=dev)
-    sqd = torch.empty((n, k), dtype=torch.float32, device=dev)
-    wsk = torch.empty(_l.load().esom_workspace_bytes(g, d, k, 0), dtype=torch.uint8, device=dev)
-    kflag = _d.new_flag(dev)
-    sh = _d.stream_handle(dev)
-
-    def knn_call():
-        _l.call("esom_knn", _d.ptr(X), n, d, _d.ptr(loop.model.hi), g, k, _d.ptr(idx), _d.ptr(sqd), _d.ptr(kflag),
-                _d.ptr(wsk), wsk.numel(), sh)
-
-    def ev_time(fn, reps=5):
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            b.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
-
-    knn_call()
-    kern = ev_time(knn_call)
-    emb = ev_time(lambda: loop.model.embed_into(X, loop.xy, flag=loop.flag))
-    del idx, sqd, wsk
+    L = _l.load()
+    flush.zero_()
+    torch.cuda.synchronize(dev)
+    L.esom_timing_begin(1)
+    loop.frame()
+    torch.cuda.synchronize(dev)
+    ktimes = {}
+    for name in ("knn_tc2_kernel", "knn_gemm_kernel", "knn_exact_group_kernel", "project_kernel"):
+        cnt = ctypes.c_int32(0)
+        ms_k = L.esom_timing_query(name.encode(), ctypes.byref(cnt))
+        if cnt.value:
+            ktimes[name] = {"ms": ms_k, "launches": cnt.value, "share_of_frame": ms_k / ms}
+    L.esom_timing_begin(0)
+    dom = max(ktimes, key=lambda kk: ktimes[kk]["ms"]) if ktimes else None
     hbm_peak, bf16_peak, peak_kind = measured_peaks()
-    alg_bytes = n * (4 * d + 8 * k)
-    achieved = alg_bytes / (kern * 1e-3) / 1e9
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or 1965.0
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # lane-ops/s (T), at the sampled clock
-    exact_ops = n * 3.0 * g * d / (emb * 1e-3) / 1e12  # exact-path equivalent sub/mul/add per element
-    gemm_tflops = n * 2.0 * g * 16 * ((d + 15) // 16) * 3 / (kern * 1e-3) / 1e12  # split-bf16 screen
-    tc_used = d <= 32 and g <= 4096 and k <= 16 and os.environ.get("ESOM_TC", "1") != "0"
+    dk = (d + 31) // 32 * 32
+    if dom == "knn_gemm_kernel":
+        kms = ktimes[dom]["ms"]
+        alg_flops = 2.0 * n * g * d
+        mma_flops = 2.0 * n * g * dk * 3 * 2  # split-bf16 (3 products) x two passes, as executed
+        roofline = {"bound": "tensor", "achieved": alg_flops / (kms * 1e-3) / 1e12, "peak": bf16_peak,
+                    "unit": "TFLOP/s", "frac": alg_flops / (kms * 1e-3) / 1e12 / bf16_peak,
+                    "traffic": ncu_traffic(workload), "peak_kind": peak_kind, "kernel": dom,
+                    "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
+                    "alg_flops_per_point": 2 * g * d,
+                    "executed_mma_TFLOPs": mma_flops / (kms * 1e-3) / 1e12,
+                    "executed_mma_frac_of_bf16_peak": mma_flops / (kms * 1e-3) / 1e12 / bf16_peak,
+                    "note": "achieved = algorithmic 2gd flops/point (one x.L^T); the kernel issues 6x that in "
+                            "bf16 MMAs (x_hi l_hi + x_hi l_lo + x_lo l_hi, group-min pass + candidate pass)"}
+    elif dom is not None:
+        kms = ktimes[dom]["ms"]
+        per_pt = (4 * d + 8 * k) if dom.startswith("knn") else (8 * k + 8)
+        achieved = n * per_pt / (kms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": ncu_traffic(workload), "peak_kind": peak_kind,
+                    "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
+                    "alg_bytes_per_point": per_pt,
+                    "note": "issue-bound exact selection (SURVEY §8d: distance intensity >> HBM ridge); "
+                            "compute_roofline gives the pipe view"}
+    else:
+        roofline = None
+    embed_frac = n * (4 * d + 8) / (ms * 1e-3) / 1e9 / hbm_peak
+    exact_ops = n * 3.0 * g * d / (ms * 1e-3) / 1e12  # exact-path equivalent sub/mul/add per element
+    compute_roofline = {"exact_equiv_Tops": exact_ops, "fp32_peak_Tops_at_sampled_clock": fp32_peak,
+                        "exact_equiv_frac": exact_ops / fp32_peak, "embed_hbm_frac": embed_frac,
+                        "kernels": ktimes,
+                        "note": "exact_equiv = 3*g*d f32 ops per point / frame time (what an exact CUDA-core scan "
+                                "must issue); kernels: per-kernel device ms inside one frame"}
     # ---- end to end through the public API: pinned host points in, host xy out ----
     e2e = None
     if True:  # every rank measures; the slowest rank defines the job's e2e time
@@ -330,23 +348,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max, "fps": 1e3 / ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (exact k-NN), f64 accum",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": ("f32 exact k-NN (bf16x3 tcgen05 screen), f32/f64 projection" if d > 32 else "f32 exact k-NN (bf16x3 tcgen05 screen), f32/f64 projection"),
             "data": "synthetic Gaussian mixture (reference datagen.gaussians restated), SOM-initialised landmarks",
             "config": {"workload": desc, "n_per_rank": n, "d": d, "g": g, "k": k, "train": train,
                        "parallelism": f"points sharded x{world}, landmarks replicated",
                        "l2": "flushed between timed steps (256 MiB write outside the events); X = 128 MiB/rank"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": ncu_traffic(workload), "peak_kind": peak_kind,
-                         "kernel": ("knn_tc_kernel (tcgen05 split-bf16 screen + exact f32 recheck)" if tc_used
-                                    else "knn_scan_kernel (exact f32, CUDA cores)"),
-                         "kernel_ms": kern, "alg_bytes_per_point": 4 * d + 8 * k,
-                         "embed_ms": emb, "embed_hbm_frac": n * (4 * d + 8) / (emb * 1e-3) / 1e9 / hbm_peak},
-            "compute_roofline": {"exact_equiv_Tops": exact_ops, "fp32_peak_Tops_at_sampled_clock": fp32_peak,
-                                 "exact_equiv_frac": exact_ops / fp32_peak,
-                                 "tensor_TFLOPs": gemm_tflops if tc_used else 0.0,
-                                 "tensor_frac_of_bf16_peak": (gemm_tflops / bf16_peak) if tc_used else 0.0,
-                                 "note": "exact_equiv = 3*g*d f32 ops per point / embed time (what the exact "
-                                         "CUDA-core path must issue); tensor = split-bf16 x.L^T MMA flops / k-NN time"},
+            "roofline": roofline,
+            "compute_roofline": compute_roofline,
             "clocks": clocks,
             "gpu_launches": args.steps * loop.launches_per_frame,
             "e2e": e2e,

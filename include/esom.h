@@ -48,6 +48,14 @@ const char *esom_last_error(void);
  * number of candidates they re-evaluate exactly to *counter (device int32). */
 void esom_set_tc_stats(int32_t *counter);
 
+/* Diagnostic kernel timing: esom_timing_begin(1) clears and starts recording
+ * CUDA events on the launching stream around the hot kernels (knn_tc2_kernel,
+ * knn_gemm_kernel, knn_exact_group_kernel, project_kernel);
+ * esom_timing_query(name, &launches) synchronizes and returns their summed
+ * milliseconds.  esom_timing_begin(0) stops recording. */
+void esom_timing_begin(int32_t on);
+double esom_timing_query(const char *name, int32_t *launches);
+
 /* Bytes of scratch for esom_knn / esom_bmu_accumulate (with_pairs = 0) or
  * for a prepared model (with_pairs = 1: packed landmark tiles + the packed
  * upper-triangular pair table). */
@@ -78,7 +86,7 @@ int esom_prepare_model(const float *hi, int32_t g, int32_t d, int32_t k, void *w
 
 /* Per-call scratch of esom_embed_prepared for n points: the neighbour rows
  * of one L2-resident chunk of points (scan -> projection). */
-size_t esom_point_workspace_bytes(int64_t n, int32_t k);
+size_t esom_point_workspace_bytes(int64_t n, int32_t d, int32_t k);
 
 /* Embed on a prepared model: exact k-NN scan + scores + projection -> xy
  * (n×2 f32), two kernels per chunk.  Replaces embed (ref:

@@ -42,10 +42,12 @@ HELPERS = {
     "esom_last_error": ([], C.c_char_p),
     "esom_workspace_bytes": ([_i32, _i32, _i32, _i32], C.c_size_t),
     "esom_tick_workspace_bytes": ([_i32, _i32], C.c_size_t),
-    "esom_point_workspace_bytes": ([_i64, _i32], C.c_size_t),
+    "esom_point_workspace_bytes": ([_i64, _i32, _i32], C.c_size_t),
     "esom_embed_workspace_bytes": ([_i64, _i32, _i32, _i32], C.c_size_t),
     "esom_embed_launches": ([_i64, _i32, _i32, _i32], C.c_int32),
     "esom_set_tc_stats": ([_vp], None),
+    "esom_timing_begin": ([_i32], None),
+    "esom_timing_query": ([C.c_char_p, _vp], C.c_double),
 }
 
 

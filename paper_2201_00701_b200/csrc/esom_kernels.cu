@@ -20,6 +20,10 @@
 #include <string.h>
 #include <stdlib.h>
 
+#include <mutex>
+#include <string>
+#include <vector>
+
 #include "esom_common.cuh"
 #include "esom_host.h"
 #include "esom_scan_args.h"
@@ -75,6 +79,39 @@ size_t resident_limit() {
 }  // namespace esom_host
 
 using namespace esom_host;
+
+// ---------------------------------------------------------------------------
+// Kernel timing (diagnostic, off by default): CUDA events recorded on the
+// launching stream around the hot kernels, summed per kernel name on query.
+// bench.py uses it to time the dominant kernel live (esom_timing_*).
+// ---------------------------------------------------------------------------
+namespace {
+struct TimedLaunch {
+    std::string name;
+    cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+std::vector<TimedLaunch> g_tl;
+bool g_timing = false;
+
+struct KTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t st;
+    const char* name;
+    KTimer(const char* n, cudaStream_t s) : st(s), name(n) {
+        if (!g_timing) return;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+    }
+    ~KTimer() {
+        if (!a) return;
+        cudaEventRecord(b, st);
+        std::lock_guard<std::mutex> lk(g_tmu);
+        g_tl.push_back({name, a, b});
+    }
+};
+}  // namespace
 
 namespace {
 
@@ -727,6 +764,7 @@ int tc2_warpgroups() {  // ESOM_TC2_W selects 2..4 warpgroups per CTA (default 4
 template <int KP>
 int launch_tc2_w(Tc2Args a, int W, cudaStream_t st) {
     int e = ESOM_ERR_UNSUPPORTED;
+    KTimer tm("knn_tc2_kernel", st);
     if (W >= 4) e = launch_tc2_t<KP, 4>(a, st);
     if (e == ESOM_ERR_UNSUPPORTED && W >= 3) e = launch_tc2_t<KP, 3>(a, st);
     if (e == ESOM_ERR_UNSUPPORTED) e = launch_tc2_t<KP, 2>(a, st);
@@ -854,8 +892,12 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         t.bmu_approx = reinterpret_cast<int32_t*>(ws + m.bmu3);
         t.stats = tc_stats_ptr();
         const int kp = kp_for(a.k);
-        int e = kp == 4 ? launch_gemm_t<4>(t, st) : kp == 8 ? launch_gemm_t<8>(t, st)
+        int e;
+        {
+            KTimer tm("knn_gemm_kernel", st);
+            e = kp == 4 ? launch_gemm_t<4>(t, st) : kp == 8 ? launch_gemm_t<8>(t, st)
               : kp == 16 ? launch_gemm_t<16>(t, st) : launch_gemm_t<32>(t, st);
+        }
         if (e) return e;
         // visit points grouped by approximate nearest landmark: a CTA's candidate rows repeat (L1 hits)
         int32_t* cntb = reinterpret_cast<int32_t*>(ws + m.hist3);
@@ -882,7 +924,10 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         x.qe_sum = a.qe_sum;
         x.accS = a.accS;
         x.accC = a.accC;
-        if (int e3 = launch_exact_warp_t<32>(x, st)) return e3;
+        {
+            KTimer tm("knn_exact_group_kernel", st);
+            if (int e3 = launch_exact_warp_t<32>(x, st)) return e3;
+        }
     }
     return ESOM_OK;
 }
@@ -909,6 +954,32 @@ int esom_version(void) { return ESOM_ABI_VERSION; }
 
 void esom_set_tc_stats(int32_t* counter) { g_tc_stats = counter; }
 
+void esom_timing_begin(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    for (auto& t : g_tl) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    g_tl.clear();
+    g_timing = on != 0;
+}
+
+double esom_timing_query(const char* name, int32_t* launches) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    double ms = 0.0;
+    int n = 0;
+    for (auto& t : g_tl) {
+        if (t.name != name) continue;
+        cudaEventSynchronize(t.b);
+        float v = 0.0f;
+        cudaEventElapsedTime(&v, t.a, t.b);
+        ms += v;
+        ++n;
+    }
+    if (launches) *launches = n;
+    return ms;
+}
+
 const char* esom_last_error(void) { return g_err; }
 
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
@@ -918,15 +989,23 @@ size_t esom_workspace_bytes(int32_t g, int32_t d, int32_t k, int32_t with_pairs)
 }
 
 // points per embed chunk: the chunk's neighbour rows stay L2-resident between
-// the k-NN scan and the projection kernel
-static int64_t embed_chunk(int32_t k) {
+// the k-NN scan and the projection kernel.  For the d > 32 GEMM screen the
+// k-NN dominates by far, so the chunk is the screen's own (larger) chunk.
+static bool t3_shape(int32_t d, int32_t k) { return d > 32 && d <= 1536 && k <= 32; }
+
+static int64_t embed_chunk(int32_t d, int32_t k) {
     const char* e = getenv("ESOM_EMBED_CHUNK");
-    const int64_t c = e ? atoll(e) : (int64_t)(48u << 20) / (8 * (int64_t)k);
+    if (e) {
+        const int64_t c = atoll(e);
+        return c < 1024 ? 1024 : c;
+    }
+    if (t3_shape(d, k)) return model_layout(1, d, k, false).t3chunk;
+    const int64_t c = (int64_t)(48u << 20) / (8 * (int64_t)k);
     return c < 1024 ? 1024 : c;
 }
 
-size_t esom_point_workspace_bytes(int64_t n, int32_t k) {
-    const int64_t c = n < embed_chunk(k) ? n : embed_chunk(k);
+size_t esom_point_workspace_bytes(int64_t n, int32_t d, int32_t k) {
+    const int64_t c = n < embed_chunk(d, k) ? n : embed_chunk(d, k);
     const size_t rows = align256((size_t)(c > 0 ? c : 1) * k * 4) * 2;
     return rows + align256((size_t)(c > 0 ? c : 1) * 4) + align256(65536 * 4) + 256;  // + perm + bucket counts
 }
@@ -1027,14 +1106,14 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
     if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64%s", "");
     if (n == 0) return ESOM_OK;
-    if (point_ws_bytes < esom_point_workspace_bytes(n, k))
+    if (point_ws_bytes < esom_point_workspace_bytes(n, d, k))
         return set_err(ESOM_ERR_PARAM, "point workspace too small%s", "");
     const Plan p = make_plan(d, g, k);
     const ModelLayout ml = model_layout(g, d, k, true);
     const char* mws = reinterpret_cast<const char*>(model_ws);
     const float* Lt = reinterpret_cast<const float*>(mws + ml.lt);
     const float* T = reinterpret_cast<const float*>(mws + ml.tri);
-    const int64_t chunk = n < embed_chunk(k) ? n : embed_chunk(k);
+    const int64_t chunk = n < embed_chunk(d, k) ? n : embed_chunk(d, k);
     int32_t* idx = reinterpret_cast<int32_t*>(point_ws);
     float* sqd = reinterpret_cast<float*>(reinterpret_cast<char*>(point_ws) + align256((size_t)chunk * k * 4));
     for (int64_t s = 0; s < n; s += chunk) {
@@ -1072,28 +1151,36 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         q.X = X + s * d;
         q.hi = hi;
         q.d = d;
-        if (int e = dispatch_project(p.kp, q, stream)) return e;
+        {
+            KTimer tm("project_kernel", stream);
+            if (int e = dispatch_project(p.kp, q, stream)) return e;
+        }
     }
     return ESOM_OK;
 }
 
 int32_t esom_embed_launches(int64_t n, int32_t g, int32_t d, int32_t k) {
-    // kernels launched by one esom_embed_prepared call: per chunk the k-NN scan
-    // (or tensor-core screen) + the projection (+ 3 BMU-sort kernels when the
-    // pair table lives in L2)
+    // kernels launched by one esom_embed_prepared call, per embed chunk: the
+    // k-NN (tensor-core screen, CUDA-core scan, or for d > 32 per screen chunk
+    // split + GEMM + 3 BMU-sort + exact) and the projection (+ 3 BMU-sort
+    // kernels when the pair table lives in L2)
     if (n <= 0) return 0;
-    const int64_t chunk = n < embed_chunk(k) ? n : embed_chunk(k);
-    const int64_t chunks = (n + chunk - 1) / chunk;
+    const int64_t chunk = n < embed_chunk(d, k) ? n : embed_chunk(d, k);
     const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
     const bool sorted = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && g <= 8192;
-    (void)d;
-    int64_t per = 2 + (sorted ? 3 : 0);
-    if (sorted && chunk < 4096) per = 2;
-    return (int32_t)(chunks * per);
+    const ModelLayout m = model_layout(g, d, k, true);
+    int64_t total = 0;
+    for (int64_t s = 0; s < n; s += chunk) {
+        const int64_t cm = n - s < chunk ? n - s : chunk;
+        int64_t knn = 1;
+        if (m.t3 && t3_enabled() && cm >= 256 && d <= 1536) knn = 6 * ((cm + m.t3chunk - 1) / m.t3chunk);
+        total += knn + 1 + ((sorted && cm >= 4096) ? 3 : 0);
+    }
+    return (int32_t)total;
 }
 
 size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k) {
-    return esom_workspace_bytes(g, d, k, 1) + esom_point_workspace_bytes(n, k);
+    return esom_workspace_bytes(g, d, k, 1) + esom_point_workspace_bytes(n, d, k);
 }
 
 int esom_embed(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,

@@ -169,7 +169,7 @@ class PreparedModel:
         return self
 
     def point_workspace(self, n: int) -> torch.Tensor:
-        nbytes = _lib.load().esom_point_workspace_bytes(n, self.k)
+        nbytes = _lib.load().esom_point_workspace_bytes(n, self.d, self.k)
         pws = getattr(self, "pws", None)
         if pws is None or pws.numel() < nbytes:
             self.pws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
