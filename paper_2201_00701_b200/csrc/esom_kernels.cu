@@ -292,6 +292,112 @@ __global__ void bmu_scatter_kernel(const int32_t* __restrict__ idx, int64_t n, i
         perm[atomicAdd(cursor + __ldg(idx + i * k), 1)] = (int32_t)i;
 }
 
+// Scatter with CTA-local ranks: each CTA ranks its slice of points per bucket
+// in shared memory, reserves one range per (CTA, bucket) with a single global
+// atomic, then writes perm -- instead of one contended global atomic per point.
+constexpr int kScatItems = 8;
+
+__global__ void bmu_scatter2_kernel(const int32_t* __restrict__ idx, int64_t n, int k, int g,
+                                    int32_t* __restrict__ cursor, int32_t* __restrict__ perm) {
+    extern __shared__ int32_t sh[];
+    int32_t* hist = sh;       // g
+    int32_t* base = sh + g;   // g
+    const int64_t slice = (int64_t)blockDim.x * kScatItems;
+    for (int64_t s0 = blockIdx.x * slice; s0 < n; s0 += (int64_t)gridDim.x * slice) {
+        for (int b = threadIdx.x; b < g; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        int bk[kScatItems], rk[kScatItems];
+#pragma unroll
+        for (int q = 0; q < kScatItems; ++q) {
+            const int64_t i = s0 + (int64_t)q * blockDim.x + threadIdx.x;
+            bk[q] = i < n ? __ldg(idx + i * k) : -1;
+            rk[q] = bk[q] >= 0 ? atomicAdd(hist + bk[q], 1) : 0;
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < g; b += blockDim.x)
+            if (hist[b]) base[b] = atomicAdd(cursor + b, hist[b]);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kScatItems; ++q) {
+            const int64_t i = s0 + (int64_t)q * blockDim.x + threadIdx.x;
+            if (bk[q] >= 0) perm[base[bk[q]] + rk[q]] = (int32_t)i;
+        }
+        __syncthreads();
+    }
+}
+
+int grid_for(int64_t work, int threads);
+
+// BMU counting sort of n neighbour rows (bucket = idx[i * k]): counts, exclusive
+// scan, scatter.  Afterwards cntb[b] is the end of bucket b in perm.
+int bmu_sort(const int32_t* idx, int64_t n, int k, int g, int32_t* cntb, int32_t* perm, cudaStream_t st) {
+    cudaMemsetAsync(cntb, 0, (size_t)g * 4, st);
+    bmu_hist_kernel<<<num_sms() * 2, 512, (size_t)g * 4, st>>>(idx, n, k, g, cntb);
+    bmu_scan_kernel<<<1, 1024, 0, st>>>(cntb, g);
+    if (g <= 8192) {
+        const size_t smem = (size_t)g * 8;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(bmu_scatter2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t slices = (n + 256 * kScatItems - 1) / (256 * kScatItems);
+        const int64_t cap = (int64_t)num_sms() * 4;
+        bmu_scatter2_kernel<<<(unsigned)(slices < cap ? (slices < 1 ? 1 : slices) : cap), 256, smem, st>>>(idx, n, k, g,
+                                                                                                         cntb, perm);
+    } else {
+        bmu_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx, n, k, cntb, perm);
+    }
+    return cuda_check("bmu_sort");
+}
+
+// Batch-SOM statistics from a BMU-sorted order (after bmu_scatter, ends[b] is
+// the end of landmark b's segment of perm): one warp per (landmark, 32-dim
+// slice, part of <= kSegPart points) sums its points' coordinates in f64 and
+// adds the partial to S / C (a handful of f64 atomics per address instead of
+// one per point and dimension).
+constexpr int kSegPart = 256;
+
+__global__ void bmu_segsum_kernel(const float* __restrict__ X, int d, const int32_t* __restrict__ perm,
+                                  const int32_t* __restrict__ ends, int g, int parts, double* __restrict__ S,
+                                  double* __restrict__ C) {
+    const int lane = threadIdx.x & 31;
+    const int nsl = (d + 31) / 32;
+    const int64_t nw = (int64_t)g * nsl * parts;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int part = (int)(w % parts);
+        const int sl = (int)((w / parts) % nsl);
+        const int b = (int)(w / ((int64_t)parts * nsl));
+        const int c = sl * 32 + lane;
+        const int e1s = ends[b], e0s = b ? ends[b - 1] : 0;
+        double acc = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        int cntp = 0;
+        for (int e0 = e0s + part * kSegPart; e0 < e1s; e0 += parts * kSegPart) {  // parts stride the segment
+            const int e1 = e0 + kSegPart < e1s ? e0 + kSegPart : e1s;
+            if (S)
+                for (int base = e0; base < e1; base += 32) {  // 32 perm entries per coalesced load
+                    const int pe = base + lane < e1 ? __ldg(perm + base + lane) : 0;
+                    const int nb = e1 - base < 32 ? e1 - base : 32;
+                    float v[32];  // 32 row loads in flight per lane
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const int r = __shfl_sync(0xffffffffu, pe, q);
+                        v[q] = (q < nb && c < d) ? __ldg(X + (int64_t)r * d + c) : 0.0f;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 32; q += 4) {
+                        acc += (double)v[q];
+                        acc1 += (double)v[q + 1];
+                        acc2 += (double)v[q + 2];
+                        acc3 += (double)v[q + 3];
+                    }
+                }
+            cntp += e1 - e0;
+        }
+        acc += (acc1 + acc2) + acc3;
+        if (!cntp) continue;
+        if (S && c < d) atomicAdd(S + (int64_t)b * d + c, acc);
+        if (C && lane == 0 && sl == 0) atomicAdd(C + b, (double)cntp);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Scores (ref: projection.py:38-59).  numba's float(f32) stays f32, so the
 // root is sqrtf, widened; the rest is f64.  `exp` is CUDA's (<= 1 ulp from
@@ -558,6 +664,7 @@ __global__ void batch_update_kernel(const double* __restrict__ S, const double* 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* h = reinterpret_cast<double*>(smem_raw);  // g
     __shared__ double red[32];
+    __shared__ double red2[16][32];
     const double denom = 2.0 * sigma * sigma;
     for (int j = blockIdx.x; j < g; j += gridDim.x) {
         const double ljx = lo[2 * j], ljy = lo[2 * j + 1];
@@ -586,18 +693,28 @@ __global__ void batch_update_kernel(const double* __restrict__ S, const double* 
             den += red[q];
             Btot += red[16 + q];
         }
-        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        // num_j = H_j. S in 32-dim slices: lane = dimension, warps split b (coalesced S rows)
+        const int lane = threadIdx.x & 31;
+        for (int c0 = 0; c0 < d; c0 += 32) {
+            const int c = c0 + lane;
             double num = 0.0;
-            for (int b = 0; b < g; ++b) num = fma(h[b], S[(int64_t)b * d + c], num);
-            float* hj = hi + (int64_t)j * d + c;
-            if (mode == 1) {
-                if (den > 0.0) *hj = (float)(num / den);
-            } else if (Btot > 0.0) {
-                const double h0 = (double)*hj;
-                *hj = (float)(h0 + (alpha / Btot) * (num - den * h0));
+            if (c < d)
+                for (int b = w; b < g; b += nw) num = fma(h[b], S[(int64_t)b * d + c], num);
+            red2[w][lane] = num;
+            __syncthreads();
+            if (w == 0 && c < d) {
+                double tot = 0.0;
+                for (int q = 0; q < nw; ++q) tot += red2[q][lane];
+                float* hj = hi + (int64_t)j * d + c;
+                if (mode == 1) {
+                    if (den > 0.0) *hj = (float)(tot / den);
+                } else if (Btot > 0.0) {
+                    const double h0 = (double)*hj;
+                    *hj = (float)(h0 + (alpha / Btot) * (tot - den * h0));
+                }
             }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -902,11 +1019,7 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         // visit points grouped by approximate nearest landmark: a CTA's candidate rows repeat (L1 hits)
         int32_t* cntb = reinterpret_cast<int32_t*>(ws + m.hist3);
         int32_t* perm = reinterpret_cast<int32_t*>(ws + m.perm3);
-        cudaMemsetAsync(cntb, 0, (size_t)a.g * 4, st);
-        bmu_hist_kernel<<<num_sms() * 2, 512, (size_t)a.g * 4, st>>>(t.bmu_approx, cn, 1, a.g, cntb);
-        bmu_scan_kernel<<<1, 1024, 0, st>>>(cntb, a.g);
-        bmu_scatter_kernel<<<grid_for(cn, 256), 256, 0, st>>>(t.bmu_approx, cn, 1, cntb, perm);
-        if (int e2 = cuda_check("t3 bmu sort")) return e2;
+        if (int e2 = bmu_sort(t.bmu_approx, cn, 1, a.g, cntb, perm, st)) return e2;
         T3ExactArgs x{};
         x.X = X;
         x.n = cn;
@@ -1122,23 +1235,29 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         a.out_idx = idx;
         a.out_sqd = sqd;
         a.bmu = bmu ? bmu + s : nullptr;
-        a.accS = acc_S;
-        a.accC = acc_C;
-        a.qe_sum = qe_sum;
+        a.qe_sum = qe_sum;  // batch-SOM sums come from the BMU-sorted order below (no atomics)
         if (int e = run_knn(p, ml, a, mws, stream)) return e;
         ProjArgs q{};
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
-        if (tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192) {
-            // pair table stays in L2: visit points grouped by BMU
+        const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
+        if (l2_table || acc_S || acc_C) {
+            // BMU counting sort of the chunk (BMU = idx[:, 0]): the projection visits
+            // points grouped by BMU (pair-table reads coalesce when the table is in
+            // L2) and the batch-SOM sums are segment sums over the same order
             char* base = reinterpret_cast<char*>(point_ws) + 2 * align256((size_t)chunk * k * 4);
             int32_t* perm = reinterpret_cast<int32_t*>(base);
             int32_t* cntb = reinterpret_cast<int32_t*>(base + align256((size_t)chunk * 4));
-            cudaMemsetAsync(cntb, 0, (size_t)g * 4, stream);
-            bmu_hist_kernel<<<num_sms() * 2, 512, (size_t)g * 4, stream>>>(idx, m, k, g, cntb);
-            bmu_scan_kernel<<<1, 1024, 0, stream>>>(cntb, g);
-            bmu_scatter_kernel<<<grid_for(m, 256), 256, 0, stream>>>(idx, m, k, cntb, perm);
-            if (int e = cuda_check("bmu_sort")) return e;
-            q.perm = perm;
+            if (int e = bmu_sort(idx, m, k, g, cntb, perm, stream)) return e;
+            if (acc_S || acc_C) {
+                // parts per landmark sized for the mean segment; long segments loop over parts
+                const int64_t mean = (m + g - 1) / g;
+                const int parts = (int)((4 * mean + kSegPart - 1) / kSegPart) + 1;
+                const int64_t warps = (int64_t)g * ((d + 31) / 32) * parts;
+                bmu_segsum_kernel<<<grid_for(warps * 32, 256), 256, 0, stream>>>(X + s * d, d, perm, cntb, g, parts,
+                                                                                  acc_S, acc_C);
+                if (int e = cuda_check("bmu_segsum_kernel")) return e;
+            }
+            if (l2_table) q.perm = perm;
         }
         q.idx = idx;
         q.sqd = sqd;
@@ -1251,7 +1370,7 @@ int esom_batch_som_update(const double* acc_S, const double* acc_C, const float*
     const size_t smem = (size_t)g * 8;
     if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g too large%s", "");
     cudaFuncSetAttribute(batch_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int threads = d >= 256 ? 256 : 128;
+    const int threads = 256;
     batch_update_kernel<<<g < num_sms() * 4 ? g : num_sms() * 4, threads, smem, stream>>>(acc_S, acc_C, lo, g, d, sigma,
                                                                                           alpha, mode, hi_inout);
     return cuda_check("batch_update_kernel");
