@@ -1008,6 +1008,10 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         t.ccount = reinterpret_cast<int32_t*>(ws + m.cnt3);
         t.bmu_approx = reinterpret_cast<int32_t*>(ws + m.bmu3);
         t.stats = tc_stats_ptr();
+        {
+            const char* ev = getenv("ESOM_T3_PASSES");  // 1: experimental one-pass (log compaction) mode
+            t.passes = ev && atoi(ev) == 1 ? 1 : 2;
+        }
         const int kp = kp_for(a.k);
         int e;
         {

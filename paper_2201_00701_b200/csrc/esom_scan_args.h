@@ -91,6 +91,7 @@ struct Tc3Args {
     const float* xnorm;      // n: |x - c| (rounded up)
     int64_t n;
     int d, dk, gpad, k;      // dk = d padded to 32, gpad = g padded to 256
+    int passes;              // 2: group-min bound pass + candidate pass; 1: candidate pass with log compaction
     const uint16_t* Bhi;     // -2 (l - c) split bf16, [256-row round][K chunk] canonical
     const uint16_t* Blo;
     const float* ln;         // gpad: |l - c|^2 (+inf padding)

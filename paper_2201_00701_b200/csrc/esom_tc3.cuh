@@ -66,12 +66,13 @@ struct T3Compacted {
 // log full: tighten the cut to the k-th smallest logged D~ (+2E) and keep the
 // survivors in index order (rare; out of line)
 template <int KP>
-__device__ __noinline__ T3Compacted<KP> t3_compact(float* logv, unsigned short* logj, int cnt, int k, float E2,
-                                                   float tcut) {
+__device__ __noinline__ T3Compacted<KP> t3_compact(float* logv, unsigned short* logj, int cnt, int k, float xnorm,
+                                                   float lmax, float lnmax, int d, int dk, float tcut) {
     float vd[KP];
     vlist_init<KP>(vd, k);
     for (int e = 0; e < cnt; ++e) vlist_insert<KP>(vd, logv[e * kT3Epi]);
     const float tau = vd[KP - 1];
+    const float E2 = 2.0f * t3_eps(xnorm, lmax, lnmax, d, dk, tau);
     const float nt = tau + E2 + 9.6e-7f * fabsf(tau);
     T3Compacted<KP> r;
     r.tcut = nt < tcut ? nt : tcut;
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
         if ((tid & 31) == 0) {
             uint32_t q = 0;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = 2 - a.passes; pass < 2; ++pass)
                     for (int r = 0; r < R; ++r)
                         for (int kc = 0; kc < nkc; ++kc, ++q) {
                             const int s = (int)(q % kT3Stages);
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             const uint32_t idesc = umma_idesc_bf16(128, kT3Rows);
             const uint32_t sboA = (kT3Kc / 8) * 128, sboB = (kT3Kc / 8) * 128, lbo = 128;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = 2 - a.passes; pass < 2; ++pass)
                     for (int r = 0; r < R; ++r, ++rr) {
                         mbar_wait(&tmem_empty, (rr & 1u) ^ 1u);  // epilogue has read the previous round
                         tc_fence_after();
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             float gm[kT3Groups];
 #pragma unroll
             for (int q = 0; q < kT3Groups; ++q) gm[q] = kInf;
-            // ---- pass 1: group minima over all rounds ----
-            for (int r = 0; r < R; ++r, ++rr) {
+            // ---- pass 1 (two-pass mode): group minima over all rounds ----
+            for (int r = 0; r < (a.passes == 2 ? R : 0); ++r, ++rr) {
                 mbar_wait(&tmem_full, rr & 1u);
                 tc_fence_after();
                 const float* lnr = a.ln + (size_t)r * kT3Rows;
@@ -227,9 +228,13 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                 tc_fence_before();
                 mbar_arrive(&tmem_empty);
             }
-            const float tau = kth_of_64<KP>(gm, k);
-            const float E2 = 2.0f * t3_eps(xnorm, lmax, lnmax, a.d, a.dk, tau);
-            float tcut = tau + E2 + 9.6e-7f * fabsf(tau);
+            // one-pass mode: no bound yet (every landmark is logged until the first
+            // compaction sets the cut to the k-th smallest logged D~ + 2E)
+            float tcut = kInf;
+            if (a.passes == 2) {
+                const float tau = kth_of_64<KP>(gm, k);
+                tcut = tau + 2.0f * t3_eps(xnorm, lmax, lnmax, a.d, a.dk, tau) + 9.6e-7f * fabsf(tau);
+            }
             // ---- pass 2: log candidates (index order) ----
             int cnt = 0;
             bool ovf = false;
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                         const float v = __uint_as_float(v0[q]) + __ldg(lnr + c0 + q);
                         if (v <= tcut) {
                             if (cnt == kT3LogCap) {
-                                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, E2, tcut);
+                                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
                                 cnt = cr.m;
                                 tcut = cr.tcut;
                                 ovf |= cnt == kT3LogCap;
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             if (!valid) continue;
             // ---- refine and hand the candidates to the exact kernel ----
             if (!ovf && cnt > k) {
-                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, E2, tcut);
+                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
                 cnt = cr.m;
             }
             int best = 0;
