@@ -137,14 +137,15 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic(workload: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(workload: str, points_per_launch: float):
+    """DRAM bytes per launch of the dominant kernel: the committed ncu capture's
+    bytes/point (profiles/traffic.json) x the points one launch processes here."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         j = json.loads(p.read_text())
         v = j.get(workload)
-        if isinstance(v, dict):
-            return v.get("dram_bytes_per_launch")
+        if isinstance(v, dict) and v.get("points"):
+            return v["dram_bytes"] / v["points"] * points_per_launch
     return None
 
 
@@ -287,8 +288,8 @@ def run_ours(args):
         mma_flops = 2.0 * n * g * dk * 3 * 2  # split-bf16 (3 products) x two passes, as executed
         roofline = {"bound": "tensor", "achieved": alg_flops / (kms * 1e-3) / 1e12, "peak": bf16_peak,
                     "unit": "TFLOP/s", "frac": alg_flops / (kms * 1e-3) / 1e12 / bf16_peak,
-                    "traffic": ncu_traffic(workload), "peak_kind": peak_kind, "kernel": dom,
-                    "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
+                    "traffic": ncu_traffic(workload, n / ktimes[dom]["launches"]), "peak_kind": peak_kind,
+                    "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
                     "alg_flops_per_point": 2 * g * d,
                     "executed_mma_TFLOPs": mma_flops / (kms * 1e-3) / 1e12,
                     "executed_mma_frac_of_bf16_peak": mma_flops / (kms * 1e-3) / 1e12 / bf16_peak,
@@ -299,7 +300,8 @@ def run_ours(args):
         per_pt = (4 * d + 8 * k) if dom.startswith("knn") else (8 * k + 8)
         achieved = n * per_pt / (kms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": achieved / hbm_peak, "traffic": ncu_traffic(workload), "peak_kind": peak_kind,
+                    "frac": achieved / hbm_peak, "traffic": ncu_traffic(workload, n / ktimes[dom]["launches"]),
+                    "peak_kind": peak_kind,
                     "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
                     "alg_bytes_per_point": per_pt,
                     "note": "issue-bound exact selection (SURVEY §8d: distance intensity >> HBM ridge); "

@@ -236,7 +236,10 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
     unsigned char* Ahi = p + (size_t)w * 2 * a_bytes;
     unsigned char* Alo = Ahi + a_bytes;
     p += (size_t)W * 2 * a_bytes;
-    uint32_t* bmap = reinterpret_cast<uint32_t*>(p) + (size_t)w * nwords * 128 + wt;  // [word][128]
+    uint32_t* bmap0 = reinterpret_cast<uint32_t*>(p) + (size_t)w * nwords * 128;  // [word][128]
+    uint32_t* bmap = bmap0 + wt;
+    p += (size_t)W * nwords * 128 * 4;
+    uint32_t* pkey = reinterpret_cast<uint32_t*>(p) + (size_t)w * 4 * 128;  // per WG: key | cnt | nzw | bad
 
     if (tid == 0) {
         mbar_init(&bar_load, 1);
@@ -279,8 +282,8 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
     for (int64_t t = w;; t += W) {
         const int64_t tile = blockIdx.x + t * (int64_t)gridDim.x;
         if (tile >= ntiles) break;
-        const int64_t i = tile * 128 + wt;
-        const bool valid = i < a.n;
+        int64_t i = tile * 128 + wt;
+        bool valid = i < a.n;
         // ---- stage the centred point as the split-bf16 A operand ----
         float xn = 0.0f;
         bool xbad = false;
@@ -417,9 +420,46 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         tc_fence_before();
         mbar_arrive(&bar_slot[slot][use % M]);
 
+        const uint32_t* bx;  // bitmap column of the point this thread re-evaluates
+        // ---- locality: the WG's threads take the tile's points in order of their
+        // lowest candidate (points of one cluster share candidate rows, so a warp's
+        // row loads hit the same smem banks / L1 lines); bitonic sort of 128 keys
+        {
+            const int w0 = __ffs(nzw) - 1;
+            const uint32_t m0 = w0 >= 0 ? bmap[(size_t)w0 * 128] : 0u;
+            const uint32_t j0 = (valid && m0) ? (uint32_t)(32 * w0 + __ffs(m0) - 1) : 0xFFFFFFu;
+            pkey[wt] = (j0 << 7) | (uint32_t)wt;
+            pkey[128 + wt] = (uint32_t)cnt;
+            pkey[256 + wt] = nzw;
+            pkey[384 + wt] = (valid ? 1u : 0u) | (xbad ? 2u : 0u);
+            named_bar(1 + w, 128);
+            for (int size = 2; size <= 128; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    const int pt = wt ^ stride;
+                    if (pt > wt) {
+                        const uint32_t ka = pkey[wt], kb = pkey[pt];
+                        if ((ka > kb) == ((wt & size) == 0)) {
+                            pkey[wt] = kb;
+                            pkey[pt] = ka;
+                        }
+                    }
+                    named_bar(1 + w, 128);
+                }
+            }
+            const int pp = (int)(pkey[wt] & 127u);
+            stat_local += cnt;
+            cnt = (int)pkey[128 + pp];
+            nzw = pkey[256 + pp];
+            const uint32_t fl = pkey[384 + pp];
+            named_bar(1 + w, 128);  // pkey is rewritten by this WG's next tile
+            i = tile * 128 + pp;
+            valid = (fl & 1u) != 0;
+            xbad = (fl & 2u) != 0;
+            bx = bmap0 + pp;
+        }
+
         // ---- exact phase: reference f32 distances of the candidates, index order ----
         if (!valid) continue;
-        stat_local += cnt;
         int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
         float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
         int b0 = 0;
@@ -456,7 +496,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
                     if (m == 0u) {
                         wi = __ffs(nzw) - 1;  // nzw == 0 only past the last candidate (jq unused)
                         nzw &= nzw - 1u;
-                        m = bmap[(size_t)(wi < 0 ? 0 : wi) * 128];
+                        m = bx[(size_t)(wi < 0 ? 0 : wi) * 128];
                     }
                     jq[u] = 32 * wi + (__ffs(m) - 1);
                     m &= m - 1u;
@@ -535,6 +575,7 @@ size_t tc2_smem_bytes(const Tc2Args& a, bool rows_smem) {
     if (rows_smem) b += ((size_t)a.gpad * a.ls * 4 + 127) / 128 * 128;     // f32 rows
     b += (size_t)W * 2 * 128 * a.d16 * 2;                                  // A hi/lo per WG
     b += (size_t)W * (a.gpad / 32) * 128 * 4;                              // candidate bitmaps
+    b += (size_t)W * 4 * 128 * 4;                                          // locality sort keys
     return b + 256;
 }
 
