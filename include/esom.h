@@ -54,6 +54,8 @@ void esom_set_tc_stats(int32_t *counter);
  * esom_timing_query(name, &launches) synchronizes and returns their summed
  * milliseconds.  esom_timing_begin(0) stops recording. */
 void esom_timing_begin(int32_t on);
+/* Number of kernels libesom has launched so far (process-wide counter). */
+int64_t esom_launch_count(void);
 double esom_timing_query(const char *name, int32_t *launches);
 
 /* Bytes of scratch for esom_knn / esom_bmu_accumulate (with_pairs = 0) or

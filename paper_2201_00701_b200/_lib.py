@@ -47,6 +47,7 @@ HELPERS = {
     "esom_embed_launches": ([_i64, _i32, _i32, _i32], C.c_int32),
     "esom_set_tc_stats": ([_vp], None),
     "esom_timing_begin": ([_i32], None),
+    "esom_launch_count": ([], C.c_int64),
     "esom_timing_query": ([C.c_char_p, _vp], C.c_double),
 }
 

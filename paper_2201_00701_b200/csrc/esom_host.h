@@ -6,7 +6,7 @@
 
 namespace esom_host {
 int set_err(int code, const char* fmt, const char* a = "", long long b = 0, long long c = 0);
-int cuda_check(const char* where);
+int cuda_check(const char* where, int launches = 1);  // also counts our kernel launches
 int num_sms();
 int max_smem_optin();
 size_t resident_limit();

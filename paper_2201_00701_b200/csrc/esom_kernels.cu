@@ -20,6 +20,7 @@
 #include <string.h>
 #include <stdlib.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -40,7 +41,10 @@ int set_err(int code, const char* fmt, const char* a, long long b, long long c) 
     return code;
 }
 
-int cuda_check(const char* where) {
+std::atomic<long long> g_launches{0};
+
+int cuda_check(const char* where, int launches) {
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         snprintf(g_err, sizeof(g_err), "CUDA error in %s: %s", where, cudaGetErrorString(e));
@@ -344,7 +348,7 @@ int bmu_sort(const int32_t* idx, int64_t n, int k, int g, int32_t* cntb, int32_t
     } else {
         bmu_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx, n, k, cntb, perm);
     }
-    return cuda_check("bmu_sort");
+    return cuda_check("bmu_sort", 3);
 }
 
 // Batch-SOM statistics from a BMU-sorted order (after bmu_scatter, ends[b] is
@@ -784,7 +788,8 @@ int grid_for(int64_t work, int threads) {
 }
 
 struct ModelLayout {
-    size_t lt, tri, bhi, blo, ln, lstats, lrow, total;
+    size_t lt, tri, bhi, blo, ln, lstats, lrow, rec, total;
+    bool has_rec;  // g x g pair records for project_reg3_kernel (k <= 16, g <= 1024)
     int d16, gpad, ls;
     // tensor-core GEMM screen for d > 32 (esom_tc3.cuh): per-model operands + per-chunk scratch
     bool t3;
@@ -805,6 +810,9 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
     o += a256((size_t)p.ntiles * p.tile_bytes);
     m.tri = o;
     if (with_pairs) o += a256((size_t)g * (g > 1 ? g - 1 : 1) / 2 * 4);
+    m.has_rec = with_pairs && g <= 1024 && k <= 16;
+    m.rec = o;
+    if (m.has_rec) o += a256((size_t)g * g * 16);
     m.bhi = o;
     o += a256((size_t)m.gpad * m.d16 * 2);
     m.blo = o;
@@ -862,7 +870,7 @@ int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cu
     tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
         hi, g, d, m.d16, m.gpad, cen, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
         reinterpret_cast<float*>(ws + m.ln), reinterpret_cast<float*>(ws + m.lstats));
-    if (int e = cuda_check("tc_prepare_kernel")) return e;
+    if (int e = cuda_check("tc_prepare_kernel", 2)) return e;  // center + operands
     if (m.ls) {
         lrow_kernel<<<grid_for((int64_t)m.gpad * m.ls, 256), 256, 0, st>>>(hi, g, d, m.gpad, m.ls,
                                                                           reinterpret_cast<float*>(ws + m.lrow));
@@ -1071,6 +1079,8 @@ int esom_version(void) { return ESOM_ABI_VERSION; }
 
 void esom_set_tc_stats(int32_t* counter) { g_tc_stats = counter; }
 
+int64_t esom_launch_count(void) { return (int64_t)g_launches.load(std::memory_order_relaxed); }
+
 void esom_timing_begin(int32_t on) {
     std::lock_guard<std::mutex> lk(g_tmu);
     for (auto& t : g_tl) {
@@ -1231,6 +1241,12 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
     const float* Lt = reinterpret_cast<const float*>(mws + ml.lt);
     const float* T = reinterpret_cast<const float*>(mws + ml.tri);
     const int64_t chunk = n < embed_chunk(d, k) ? n : embed_chunk(d, k);
+    // pair records {T, g, g.lo_u} for this call's layout (project_reg3_kernel)
+    // (g <= 256: the triangle table sits in shared memory and v2 is as fast without the record build)
+    const bool use_rec = ml.has_rec && g > 256 && !getenv("ESOM_PROJ_V2") && !getenv("ESOM_PROJ_V1");
+    float4* rec = reinterpret_cast<float4*>(const_cast<char*>(mws) + ml.rec);
+    if (use_rec)
+        if (int e = launch_pair_records(T, lo, g, rec, stream)) return e;
     int32_t* idx = reinterpret_cast<int32_t*>(point_ws);
     float* sqd = reinterpret_cast<float*>(reinterpret_cast<char*>(point_ws) + align256((size_t)chunk * k * 4));
     for (int64_t s = 0; s < n; s += chunk) {
@@ -1244,7 +1260,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         ProjArgs q{};
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
         const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
-        if (l2_table || acc_S || acc_C) {
+        if (l2_table || acc_S || acc_C || (use_rec && m >= 4096)) {
             // BMU counting sort of the chunk (BMU = idx[:, 0]): the projection visits
             // points grouped by BMU (pair-table reads coalesce when the table is in
             // L2) and the batch-SOM sums are segment sums over the same order
@@ -1261,7 +1277,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
                                                                                   acc_S, acc_C);
                 if (int e = cuda_check("bmu_segsum_kernel")) return e;
             }
-            if (l2_table) q.perm = perm;
+            if (l2_table || use_rec) q.perm = perm;
         }
         q.idx = idx;
         q.sqd = sqd;
@@ -1274,6 +1290,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         q.X = X + s * d;
         q.hi = hi;
         q.d = d;
+        q.rec = use_rec ? rec : nullptr;
         {
             KTimer tm("project_kernel", stream);
             if (int e = dispatch_project(p.kp, q, stream)) return e;

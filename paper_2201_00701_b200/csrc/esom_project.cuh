@@ -626,6 +626,194 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// v3 (default for k <= 16, g <= 1024): everything a pair needs that depends
+// only on the landmark pair is precomputed per (hi, lo) into a g x g record
+// table {T = 0.5/hd2 (or -1 = skip), g = (lo_v - lo_u)/|lo_v - lo_u|^2,
+// g . lo_u} (16 MB at g = 1024, L2-resident; points are visited in BMU order
+// so a warp's lanes share records).  Per pair: one 16-byte load, the weight,
+// h = 1/2 + g.lo_u + (sqd_u - sqd_v) T, five FMAs.  Same fallbacks as v2.
+// ---------------------------------------------------------------------------
+__global__ void pair_record_kernel(const float* __restrict__ T, const float* __restrict__ lo, int g,
+                                   float4* __restrict__ rec) {
+    const int64_t total = (int64_t)g * g;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int u = (int)(e / g), v = (int)(e % g);
+        float4 r = make_float4(-1.0f, 0.0f, 0.0f, 0.0f);
+        if (u != v) {
+            const int a = min(u, v), b = max(u, v);
+            const float t = __ldg(T + ((int64_t)a * (2 * g - 1 - a) >> 1) + b - a - 1);
+            const float lux = lo[2 * u], luy = lo[2 * u + 1];
+            const float ex = __fsub_rn(lo[2 * v], lux), ey = __fsub_rn(lo[2 * v + 1], luy);
+            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));  // as the reference forms it
+            if (t >= 0.0f && ld2 >= kLd2Min) {
+                const double g1 = (double)ex / (double)ld2, g2 = (double)ey / (double)ld2;
+                r = make_float4(t, (float)g1, (float)g2, (float)(g1 * (double)lux + g2 * (double)luy));
+            }
+        }
+        rec[e] = r;
+    }
+}
+
+// f64 pair accumulation from the records (ill-conditioned f32 systems)
+static __device__ __noinline__ void pairs_rec_f64(int k, const int* J, const float* SQ, const float* SC,
+                                                  const float4* __restrict__ rec, const float* __restrict__ lo, int g,
+                                                  double* out5) {
+    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int u = 0; u < k; ++u) {
+        if (!(SC[u] > 0.0f)) continue;
+        for (int v = u + 1; v < k; ++v) {
+            const float w = SC[u] * SC[v];
+            if (!(w > 0.0f)) continue;
+            const float4 r = __ldg(rec + (int64_t)J[u] * g + J[v]);
+            if (!(r.x >= 0.0f)) continue;
+            const float ex = __fsub_rn(lo[2 * J[v]], lo[2 * J[u]]), ey = __fsub_rn(lo[2 * J[v] + 1], lo[2 * J[u] + 1]);
+            const double ld2 = (double)__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            const double G1 = (double)ex / ld2, G2 = (double)ey / ld2;
+            const double h = 0.5 + (double)(SQ[u] - SQ[v]) * (double)r.x + G1 * (double)lo[2 * J[u]] +
+                             G2 * (double)lo[2 * J[u] + 1];
+            const double W = w;
+            a11 = fma(W * G1, G1, a11);
+            a12 = fma(W * G1, G2, a12);
+            a22 = fma(W * G2, G2, a22);
+            c1 = fma(W * h, G1, c1);
+            c2 = fma(W * h, G2, c2);
+        }
+    }
+    out5[0] = a11;
+    out5[1] = a12;
+    out5[2] = a22;
+    out5[3] = c1;
+    out5[4] = c2;
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
+    constexpr int PT = kRegThreads;
+    const int tid = threadIdx.x;
+    const int g = a.g, k = a.k;
+    const bool vec = (k == KP) && ((KP & 3) == 0);
+    const float4* __restrict__ rec = a.rec;
+
+    for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
+        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
+        int jj[KP], rowb[KP];
+        float sq[KP], sc[KP];
+        const int32_t* irow = a.idx + i * k;
+        const float* drow = a.sqd + i * k;
+        if (vec) {
+#pragma unroll
+            for (int q = 0; q < KP; q += 4) {
+                const int4 iv = __ldg(reinterpret_cast<const int4*>(irow + q));
+                const float4 dv = __ldg(reinterpret_cast<const float4*>(drow + q));
+                jj[q] = iv.x; jj[q + 1] = iv.y; jj[q + 2] = iv.z; jj[q + 3] = iv.w;
+                sq[q] = dv.x; sq[q + 1] = dv.y; sq[q + 2] = dv.z; sq[q + 3] = dv.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                jj[q] = q < k ? __ldg(irow + q) : 0;  // padding slots: zero weight (diagonal record)
+                sq[q] = q < k ? __ldg(drow + q) : 0.0f;
+            }
+        }
+        float sig = 0.0f, sqk = 0.0f, sqmax = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            rowb[q] = jj[q] * g;
+            sig += q < k ? sqrt_approx(sq[q]) : 0.0f;
+            if (q == k - 1) sqk = sq[q];
+            sqmax = fmaxf(sqmax, sq[q]);
+        }
+        // scores as in v2 (scale-free f32 expm1 form)
+        sig = sig / (float)k;
+        bool uniform = sig < (float)kScoreEps;
+        if (!uniform) {
+            const float inv = 1.0f / (2.0f * sig * sig);
+            const float tail = ex2_approx(-1.44269504f * sqk * inv);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                const float dl = q < k ? (sqk - sq[q]) * inv : 0.0f;
+                const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
+                                                                       1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+                sc[q] = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
+                if (q == 0) uniform = ex2_approx(-1.44269504f * sq[0] * inv) - tail < (float)kScoreEps;
+            }
+        }
+        if (uniform) {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
+        }
+
+        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
+        int pj[KP];
+        float psq[KP], psc[KP];
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            pj[q] = jj[q];
+            psq[q] = sq[q];
+            psc[q] = sc[q];
+        }
+        for (int r = 1; r <= KP / 2; ++r) {  // ring schedule: round r pairs slot u with u + r mod KP
+            {
+                const int j0 = pj[0];
+                const float s0 = psq[0], c0 = psc[0];
+#pragma unroll
+                for (int q = 0; q < KP - 1; ++q) {
+                    pj[q] = pj[q + 1];
+                    psq[q] = psq[q + 1];
+                    psc[q] = psc[q + 1];
+                }
+                pj[KP - 1] = j0;
+                psq[KP - 1] = s0;
+                psc[KP - 1] = c0;
+            }
+            const bool half = r == KP / 2;
+#pragma unroll
+            for (int u = 0; u < KP; ++u) {
+                const float w = (half && u >= KP / 2) ? 0.0f : sc[u] * psc[u];
+                const float4 rc = __ldg(rec + rowb[u] + pj[u]);
+                const bool keep = (w > 0.0f) & (rc.x >= 0.0f);
+                tmax = keep ? fmaxf(tmax, rc.x) : tmax;
+                const float wk = keep ? w : 0.0f;
+                const float h = fmaf(sq[u] - psq[u], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
+                const float wg1 = wk * rc.y, wg2 = wk * rc.z;
+                a11 = fmaf(wg1, rc.y, a11);
+                a12 = fmaf(wg1, rc.z, a12);
+                a22 = fmaf(wg2, rc.z, a22);
+                c1 = fmaf(wg1, h, c1);
+                c2 = fmaf(wg2, h, c2);
+            }
+        }
+        double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
+        const float kappa = 2.0f * sqmax * tmax;
+        const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
+        if (kappa > (float)kKappaMax || illc) {
+            double o5[5];
+            float fsc[KP];
+            ref_scores_f64<KP>(k, sq, fsc);
+            if (kappa > (float)kKappaMax)
+                pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, fsc, 1, o5);
+            else
+                pairs_rec_f64(k, jj, sq, fsc, rec, a.lo, g, o5);
+            A11 = o5[0];
+            A12 = o5[1];
+            A22 = o5[2];
+            C1 = o5[3];
+            C2 = o5[4];
+        }
+        const double det = A11 * A22 - A12 * A12;
+        const double tr = A11 + A22;
+        float2 out;
+        if (det < kDetRel * tr * tr + kDetAbs) {
+            out = make_float2(__ldg(a.lo + 2 * jj[0]), __ldg(a.lo + 2 * jj[0] + 1));
+        } else {
+            out.x = (float)((C1 * A22 - C2 * A12) / det);
+            out.y = (float)((A11 * C2 - A12 * C1) / det);
+        }
+        reinterpret_cast<float2*>(a.xy)[i] = out;
+    }
+}
+
 template <int KP, bool TSMEM>
 int launch_project_reg(ProjArgs a, size_t smem, cudaStream_t st) {
     static const bool v1 = getenv("ESOM_PROJ_V1") != nullptr;  // A/B switch (measurement only)
@@ -645,6 +833,18 @@ int launch_project_reg(ProjArgs a, size_t smem, cudaStream_t st) {
 template <int KP>
 int launch_project_t(ProjArgs a, cudaStream_t st) {
     if constexpr (KP <= 16) {
+        if (a.rec) {
+            auto kern = project_reg3_kernel<KP>;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRegThreads, 0);
+            if (per_sm < 1) per_sm = 1;
+            const int64_t nblk = (a.n + kRegThreads - 1) / kRegThreads;
+            int64_t grid = (int64_t)esom_host::num_sms() * per_sm;
+            if (grid > nblk) grid = nblk;
+            if (grid < 1) grid = 1;
+            kern<<<(unsigned)grid, kRegThreads, 0, st>>>(a);
+            return esom_host::cuda_check("project_reg3_kernel");
+        }
         const size_t base = (size_t)a.g * 12 + 256;
         const size_t tbytes = (size_t)a.g * (a.g - 1) / 2 * 4;
         const size_t cap = (size_t)esom_host::max_smem_optin() - 1024;

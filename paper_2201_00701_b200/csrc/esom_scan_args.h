@@ -36,6 +36,7 @@ struct ProjArgs {
     const float* hi;
     int d;
     const int32_t* perm;     // optional visiting order (nullable)
+    const float4* rec;       // g x g pair records {T, g1, g2, g.lo_u} (project_reg3_kernel; nullable)
 };
 
 // tensor-core screened k-NN (esom_tc.cuh)
@@ -136,6 +137,8 @@ template <int DC, int KP>
 int launch_scan_t(ScanArgs a, cudaStream_t st);   // esom_scan.cuh, instantiated in inst/*.cu
 
 template <int KP>
-int launch_project_t(ProjArgs a, cudaStream_t st);  // esom_project.cuh, instantiated in inst/*.cu
+int launch_project_t(ProjArgs a, cudaStream_t st);
+// g x g pair records of project_reg3_kernel from the pair triangle T and the layout lo
+int launch_pair_records(const float* T, const float* lo, int g, float4* rec, cudaStream_t st);  // esom_project.cuh, instantiated in inst/*.cu
 
 }  // namespace esom

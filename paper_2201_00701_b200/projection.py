@@ -14,6 +14,7 @@
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -237,8 +238,8 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
         return _dev.out_like(xy, want_numpy)
 
 
-PIPE_CHUNK = 1 << 17  # points per H2D/compute/D2H stage of the host pipeline
-PIPE_DEPTH = 3        # rotating device buffers
+PIPE_CHUNK = int(os.environ.get("ESOM_PIPE_CHUNK", 1 << 16))  # points per H2D/compute/D2H stage
+PIPE_DEPTH = int(os.environ.get("ESOM_PIPE_DEPTH", 4))        # rotating device buffers
 
 
 def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:

@@ -17,7 +17,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def declared_symbols():
     text = (ROOT / "include" / "esom.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int32_t|int|size_t|void|double|const char \*)\s*\*?\s*(esom_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int32_t|int|size_t|void|double|const char \*)\s*\*?\s*(esom_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
