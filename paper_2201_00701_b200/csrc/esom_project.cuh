@@ -79,6 +79,115 @@ static __device__ __noinline__ void pairs_exact_f64(const float* __restrict__ x,
 // computes it) is skipped iff ld2 < kLd2Min  (ref: projection.py:346)
 constexpr float kLd2Min = 1.000000104e-12f;  // 0x2b8cbccd
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+constexpr float kCondMax = 100.0f;
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// f64 law-of-cosines accumulation over all pairs (fallback for ill-conditioned
+// f32 systems), same pair rules as the register kernels.
+static __device__ __noinline__ void pairs_cos_f64(int k, const int* J, const float* SQ, const float* SC, int st,
+                                                  const float2* __restrict__ LO, const float* __restrict__ T, int g,
+                                                  double* out5) {
+    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int u = 0; u < k; ++u) {
+        if (!(SC[u * st] > 0.0f)) continue;
+        for (int v = u + 1; v < k; ++v) {
+            const float w = SC[u * st] * SC[v * st];
+            if (!(w > 0.0f)) continue;
+            const int lo_j = min(J[u * st], J[v * st]), hi_j = max(J[u * st], J[v * st]);
+            const float tv = T[((lo_j * (2 * g - 1 - lo_j)) >> 1) + hi_j - lo_j - 1];
+            const float2 lu = LO[J[u * st]], lv = LO[J[v * st]];
+            const float ex = __fsub_rn(lv.x, lu.x), ey = __fsub_rn(lv.y, lu.y);
+            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            if (!(tv >= 0.0f) || !(ld2 >= kLd2Min)) continue;
+            const double G1 = (double)ex / (double)ld2, G2 = (double)ey / (double)ld2;
+            const double h = 0.5 + (double)(SQ[u * st] - SQ[v * st]) * (double)tv + G1 * (double)lu.x + G2 * (double)lu.y;
+            const double W = w;
+            a11 = fma(W * G1, G1, a11);
+            a12 = fma(W * G1, G2, a12);
+            a22 = fma(W * G2, G2, a22);
+            c1 = fma(W * h, G1, c1);
+            c2 = fma(W * h, G2, c2);
+        }
+    }
+    out5[0] = a11;
+    out5[1] = a12;
+    out5[2] = a22;
+    out5[3] = c1;
+    out5[4] = c2;
+}
+
+// The reference's scores exactly as it forms them (f32 sqrt widened, f64
+// sigma and exp; ref: projection.py:38-59), parked as f32 weights.  Used on
+// the rare f64 paths: for far outliers the reference's own d^2 != sqd rounding
+// is visible at the 1e-4 level in the weights.
+template <int KP>
+__device__ __forceinline__ void ref_scores_f64(int k, const float (&sq)[KP], float (&out)[KP]) {
+    double d[KP];
+    double sigma = 0.0, dk = 0.0;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+        d[q] = q < k ? (double)__fsqrt_rn(sq[q]) : 0.0;
+        sigma += d[q];
+        if (q == k - 1) dk = d[q];
+    }
+    sigma /= (double)k;
+    bool uniform = sigma < kScoreEps;
+    if (!uniform) {
+        const double inv = -1.0 / (2.0 * sigma * sigma);
+        const double tail = exp(dk * dk * inv);
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const double v = q < k ? exp(d[q] * d[q] * inv) - tail : 0.0;
+            out[q] = v > 0.0 ? (float)v : 0.0f;
+            if (q == 0) uniform = v < kScoreEps;
+        }
+    }
+    if (uniform) {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) out[q] = q < k - 1 ? 1.0f : 0.0f;
+    }
+}
+
+// strided form (rows in shared memory, one column per thread)
+static __device__ __noinline__ void ref_scores_f64_strided(int k, const float* sq, int st, float* out) {
+    double sigma = 0.0, dk = 0.0;
+    for (int q = 0; q < k; ++q) {
+        const double dq = (double)__fsqrt_rn(sq[q * st]);
+        sigma += dq;
+        dk = dq;
+    }
+    sigma /= (double)k;
+    bool uniform = sigma < kScoreEps;
+    if (!uniform) {
+        const double inv = -1.0 / (2.0 * sigma * sigma);
+        const double tail = exp(dk * dk * inv);
+        for (int q = 0; q < k; ++q) {
+            const double dq = (double)__fsqrt_rn(sq[q * st]);
+            const double v = exp(dq * dq * inv) - tail;
+            out[q * st] = v > 0.0 ? (float)v : 0.0f;
+            if (q == 0) uniform = v < kScoreEps;
+        }
+    }
+    if (uniform)
+        for (int q = 0; q < k; ++q) out[q * st] = q < k - 1 ? 1.0f : 0.0f;
+}
+
 template <int KP>
 __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjArgs a) {
     constexpr int PT = proj_threads<KP>();
@@ -110,32 +219,35 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
     for (int64_t i = blockIdx.x * (int64_t)PT + tid; i < a.n; i += (int64_t)gridDim.x * PT) {
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
-        // scores (f64 like the reference; ref: projection.py:38-59), parked as f32 weights
-        double sigma = 0.0, dk = 0.0;
+        // scores: the scale-free f32 form of project_reg2_kernel
+        float sig = 0.0f, sqk = 0.0f;
         for (int q = 0; q < k; ++q) {
             const float sq = __ldg(drow + q);
-            const double dq = (double)__fsqrt_rn(sq);
-            sigma += dq;
+            sig += sqrt_approx(sq);
             J[q * PT + tid] = __ldg(irow + q);
             Q[q * PT + tid] = sq;
-            dk = dq;
+            sqk = sq;
         }
-        sigma /= (double)k;
-        bool uniform = sigma < kScoreEps;
+        sig = sig / (float)k;
+        bool uniform = sig < (float)kScoreEps;
         if (!uniform) {
-            const double inv = -1.0 / (2.0 * sigma * sigma);
-            const double tail = exp(dk * dk * inv);
+            const float inv = 1.0f / (2.0f * sig * sig);
+            const float tail = ex2_approx(-1.44269504f * sqk * inv);
             for (int q = 0; q < k; ++q) {
-                const double dq = (double)__fsqrt_rn(Q[q * PT + tid]);
-                const double v = exp(dq * dq * inv) - tail;
-                S[q * PT + tid] = v > 0.0 ? (float)v : 0.0f;
-                if (q == 0) uniform = v < kScoreEps;
+                const float sq = Q[q * PT + tid];
+                const float dl = (sqk - sq) * inv;
+                const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
+                                                                       1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+                S[q * PT + tid] = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
+                if (q == 0) uniform = ex2_approx(-1.44269504f * sq * inv) - tail < (float)kScoreEps;
             }
         }
         if (uniform)
             for (int q = 0; q < k; ++q) S[q * PT + tid] = q == k - 1 ? 0.0f : 1.0f;
 
-        double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+        // pairs in f32 about o = lo[idx0] (see project_reg2_kernel), solved in f64
+        const float2 o = LO[J[tid]];
+        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f;
         float kappa = 0.0f;
         for (int u = 0; u + 1 < k; ++u) {
             const float su = S[u * PT + tid];
@@ -144,8 +256,8 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
             const float squ = Q[u * PT + tid];
             const float2 lu = LO[ju];
             const int rbu = RB[ju];
-            const double lux = lu.x, luy = lu.y;
-#pragma unroll 2
+            const float lux = lu.x - o.x, luy = lu.y - o.y;
+#pragma unroll 4
             for (int v = u + 1; v < k; ++v) {
                 const float sv = S[v * PT + tid];
                 const int jv = J[v * PT + tid];
@@ -156,38 +268,43 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
                 // layout terms in f32 exactly as the reference forms them (ref: projection.py:341-348)
                 const float ex = __fsub_rn(lv.x, lu.x), ey = __fsub_rn(lv.y, lu.y);
                 const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-                const bool keep = (su * sv > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
+                const float w = su * sv;
+                const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
                 kappa = keep ? fmaxf(kappa, (squ + sqv) * tv) : kappa;
-                const double w = keep ? (double)(su * sv) : 0.0;
-                const double r = keep ? 1.0 / (double)ld2 : 0.0;
-                const double g1 = (double)ex * r, g2 = (double)ey * r;
-                // dnum/hd2 by the law of cosines + g . lo_u  (f64 like the reference's h)
-                const double h = 0.5 + (double)((squ - sqv) * tv) + fma(g1, lux, g2 * luy);
-                const double wg1 = w * g1, wg2 = w * g2, wh = w * h;
-                a11 = fma(wg1, g1, a11);
-                a12 = fma(wg1, g2, a12);
-                a22 = fma(wg2, g2, a22);
-                c1 = fma(wh, g1, c1);
-                c2 = fma(wh, g2, c2);
+                const float rr = keep ? rcp_approx(ld2) : 0.0f;
+                const float g1 = ex * rr, g2 = ey * rr, wr = w * rr;
+                const float h = fmaf(squ - sqv, tv, 0.5f) + fmaf(g1, lux, g2 * luy);
+                const float wg1 = wr * ex, wg2 = wr * ey;
+                a11 = fmaf(wg1, g1, a11);
+                a12 = fmaf(wg1, g2, a12);
+                a22 = fmaf(wg2, g2, a22);
+                c1 = fmaf(wg1, h, c1);
+                c2 = fmaf(wg2, h, c2);
             }
         }
-        if (kappa > (float)kKappaMax) {
+        double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
+        const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
+        if (kappa > (float)kKappaMax || illc) {
             double o5[5];
-            pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, J + tid, S + tid, PT, o5);
-            a11 = o5[0];
-            a12 = o5[1];
-            a22 = o5[2];
-            c1 = o5[3];
-            c2 = o5[4];
+            ref_scores_f64_strided(k, Q + tid, PT, S + tid);  // the reference's f64 scores
+            if (kappa > (float)kKappaMax)
+                pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, J + tid, S + tid, PT, o5);
+            else
+                pairs_cos_f64(k, J + tid, Q + tid, S + tid, PT, LO, Ts, g, o5);
+            A11 = o5[0];
+            A12 = o5[1];
+            A22 = o5[2];
+            C1 = o5[3] - (o5[0] * (double)o.x + o5[1] * (double)o.y);
+            C2 = o5[4] - (o5[1] * (double)o.x + o5[2] * (double)o.y);
         }
-        const double det = a11 * a22 - a12 * a12;
-        const double tr = a11 + a22;
+        const double det = A11 * A22 - A12 * A12;
+        const double tr = A11 + A22;
         float2 out;
         if (det < kDetRel * tr * tr + kDetAbs) {
-            out = LO[J[tid]];
+            out = o;
         } else {
-            out.x = (float)((c1 * a22 - c2 * a12) / det);
-            out.y = (float)((a11 * c2 - a12 * c1) / det);
+            out.x = (float)((C1 * A22 - C2 * A12) / det + (double)o.x);
+            out.y = (float)((A11 * C2 - A12 * C1) / det + (double)o.y);
         }
         reinterpret_cast<float2*>(a.xy)[i] = out;
     }
@@ -199,12 +316,6 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
 // loads except the pair-table entry).  Same arithmetic as above.
 // ---------------------------------------------------------------------------
 constexpr int kRegThreads = 256;
-
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 
 template <int KP, bool TSMEM>
 __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
@@ -374,85 +485,6 @@ __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
 //  * pair-table index from per-slot row bases (no triangle arithmetic per pair),
 //    unconditional table reads, vector loads of the neighbour rows.
 // ---------------------------------------------------------------------------
-constexpr float kCondMax = 100.0f;
-
-__device__ __forceinline__ float sqrt_approx(float x) {
-    float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float ex2_approx(float x) {
-    float r;
-    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// f64 law-of-cosines accumulation over all pairs (fallback for ill-conditioned
-// f32 systems), same pair rules as the register kernels.
-static __device__ __noinline__ void pairs_cos_f64(int k, const int* J, const float* SQ, const float* SC,
-                                                  const float2* __restrict__ LO, const float* __restrict__ T, int g,
-                                                  double* out5) {
-    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-    for (int u = 0; u < k; ++u) {
-        if (!(SC[u] > 0.0f)) continue;
-        for (int v = u + 1; v < k; ++v) {
-            const float w = SC[u] * SC[v];
-            if (!(w > 0.0f)) continue;
-            const int lo_j = min(J[u], J[v]), hi_j = max(J[u], J[v]);
-            const float tv = T[((lo_j * (2 * g - 1 - lo_j)) >> 1) + hi_j - lo_j - 1];
-            const float2 lu = LO[J[u]], lv = LO[J[v]];
-            const float ex = __fsub_rn(lv.x, lu.x), ey = __fsub_rn(lv.y, lu.y);
-            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-            if (!(tv >= 0.0f) || !(ld2 >= kLd2Min)) continue;
-            const double G1 = (double)ex / (double)ld2, G2 = (double)ey / (double)ld2;
-            const double h = 0.5 + (double)(SQ[u] - SQ[v]) * (double)tv + G1 * (double)lu.x + G2 * (double)lu.y;
-            const double W = w;
-            a11 = fma(W * G1, G1, a11);
-            a12 = fma(W * G1, G2, a12);
-            a22 = fma(W * G2, G2, a22);
-            c1 = fma(W * h, G1, c1);
-            c2 = fma(W * h, G2, c2);
-        }
-    }
-    out5[0] = a11;
-    out5[1] = a12;
-    out5[2] = a22;
-    out5[3] = c1;
-    out5[4] = c2;
-}
-
-// The reference's scores exactly as it forms them (f32 sqrt widened, f64
-// sigma and exp; ref: projection.py:38-59), parked as f32 weights.  Used on
-// the rare f64 paths: for far outliers the reference's own d^2 != sqd rounding
-// is visible at the 1e-4 level in the weights.
-template <int KP>
-__device__ __forceinline__ void ref_scores_f64(int k, const float (&sq)[KP], float (&out)[KP]) {
-    double d[KP];
-    double sigma = 0.0, dk = 0.0;
-#pragma unroll
-    for (int q = 0; q < KP; ++q) {
-        d[q] = q < k ? (double)__fsqrt_rn(sq[q]) : 0.0;
-        sigma += d[q];
-        if (q == k - 1) dk = d[q];
-    }
-    sigma /= (double)k;
-    bool uniform = sigma < kScoreEps;
-    if (!uniform) {
-        const double inv = -1.0 / (2.0 * sigma * sigma);
-        const double tail = exp(dk * dk * inv);
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const double v = q < k ? exp(d[q] * d[q] * inv) - tail : 0.0;
-            out[q] = v > 0.0 ? (float)v : 0.0f;
-            if (q == 0) uniform = v < kScoreEps;
-        }
-    }
-    if (uniform) {
-#pragma unroll
-        for (int q = 0; q < KP; ++q) out[q] = q < k - 1 ? 1.0f : 0.0f;
-    }
-}
-
 template <int KP, bool TSMEM>
 __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
     constexpr int PT = kRegThreads;
@@ -603,7 +635,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
                 o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
                 o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
             } else {
-                pairs_cos_f64(k, jj, sq, fsc, LO, T, g, o5);
+                pairs_cos_f64(k, jj, sq, fsc, 1, LO, T, g, o5);
                 o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
                 o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
             }
