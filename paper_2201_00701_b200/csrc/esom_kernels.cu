@@ -1019,6 +1019,8 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         {
             const char* ev = getenv("ESOM_T3_PASSES");  // 1: experimental one-pass (log compaction) mode
             t.passes = ev && atoi(ev) == 1 ? 1 : 2;
+            const char* ec = getenv("ESOM_T3_COARSE");
+            t.coarse1 = ec ? atoi(ec) != 0 : 0;  // coarse bound pass: fewer MMAs but a looser cut (slower today)
         }
         const int kp = kp_for(a.k);
         int e;

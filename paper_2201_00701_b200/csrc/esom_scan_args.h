@@ -93,6 +93,7 @@ struct Tc3Args {
     int64_t n;
     int d, dk, gpad, k;      // dk = d padded to 32, gpad = g padded to 256
     int passes;              // 2: group-min bound pass + candidate pass; 1: candidate pass with log compaction
+    int coarse1;             // bound pass with x_hi . l_hi only (looser bound E1, a third of the MMAs)
     const uint16_t* Bhi;     // -2 (l - c) split bf16, [256-row round][K chunk] canonical
     const uint16_t* Blo;
     const float* ln;         // gpad: |l - c|^2 (+inf padding)
