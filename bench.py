@@ -274,7 +274,8 @@ def run_ours(args):
     loop.frame()
     torch.cuda.synchronize(dev)
     ktimes = {}
-    for name in ("knn_tc2_kernel", "knn_gemm_kernel", "knn_exact_group_kernel", "project_kernel"):
+    for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "knn_gemm_kernel", "knn_exact_group_kernel",
+                 "project_kernel"):
         cnt = ctypes.c_int32(0)
         ms_k = L.esom_timing_query(name.encode(), ctypes.byref(cnt))
         if cnt.value:

@@ -796,6 +796,9 @@ struct ModelLayout {
     int dk, gp3;
     int64_t t3chunk;
     size_t cen3, b3hi, b3lo, ln3, ls3, a3hi, a3lo, xn3, cand3, cnt3, bmu3, perm3, hist3;
+    // split tc2 screen (d <= 32, g > 256): per-chunk candidate bitmaps + info
+    int64_t t2chunk;
+    size_t t2bits, t2info;
 };
 
 size_t a256(size_t b) { return (b + 255) / 256 * 256; }
@@ -826,6 +829,12 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
     if (d <= 32) {  // padded f32 rows of the pipelined tensor-core screen (esom_tc2.cuh)
         m.ls = (((m.d16 + 3) / 4) | 1) * 4;
         o += a256((size_t)m.gpad * m.ls * 4);
+    }
+    m.t2chunk = 0;
+    if (d <= 32 && m.gpad > 256 && m.gpad <= 1024) {
+        m.t2chunk = 1 << 20;
+        m.t2bits = o;  o += a256((size_t)m.t2chunk * (m.gpad / 32) * 4);
+        m.t2info = o;  o += a256((size_t)m.t2chunk * 8);
     }
     m.t3 = d > 32 && k <= 32 && g <= 65535;
     if (m.t3) {
@@ -889,7 +898,6 @@ int tc2_warpgroups() {  // ESOM_TC2_W selects 2..4 warpgroups per CTA (default 4
 template <int KP>
 int launch_tc2_w(Tc2Args a, int W, cudaStream_t st) {
     int e = ESOM_ERR_UNSUPPORTED;
-    KTimer tm("knn_tc2_kernel", st);
     if (W >= 4) e = launch_tc2_t<KP, 4>(a, st);
     if (e == ESOM_ERR_UNSUPPORTED && W >= 3) e = launch_tc2_t<KP, 3>(a, st);
     if (e == ESOM_ERR_UNSUPPORTED) e = launch_tc2_t<KP, 2>(a, st);
@@ -924,6 +932,35 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
     a.qe_sum = s.qe_sum;
     a.flag = s.flag;
     a.stats = tc_stats_ptr();
+    if (m.t2chunk && !getenv("ESOM_TC2_FUSED")) {
+        const int Ws = getenv("ESOM_TC2_W") ? W : 3;  // measured best for the screen-only kernel (C4)
+        // g > 256: screen-only kernel (more warpgroups: no bitmaps / rows in its smem) writes
+        // candidate bitmaps; knn_exact_bits_kernel re-evaluates them with the rows in smem
+        char* w = const_cast<char*>(ws);
+        for (int64_t s0 = 0; s0 < s.n; s0 += m.t2chunk) {
+            Tc2Args c = a;
+            c.n = s.n - s0 < m.t2chunk ? s.n - s0 : m.t2chunk;
+            c.X = s.X + s0 * s.d;
+            c.out_idx = s.out_idx ? s.out_idx + s0 * s.k : nullptr;
+            c.out_sqd = s.out_sqd ? s.out_sqd + s0 * s.k : nullptr;
+            c.bmu = s.bmu ? s.bmu + s0 : nullptr;
+            c.cbits = reinterpret_cast<uint32_t*>(w + m.t2bits);
+            c.cinfo = reinterpret_cast<int2*>(w + m.t2info);
+            int e;
+            {
+                KTimer tm("knn_tc2_kernel", st);
+                e = p.kp == 4 ? launch_tc2_w<4>(c, Ws, st) : p.kp == 8 ? launch_tc2_w<8>(c, Ws, st)
+                                                                        : launch_tc2_w<16>(c, Ws, st);
+            }
+            if (e) return e;
+            KTimer tm2("knn_exact_bits_kernel", st);
+            e = p.kp == 4 ? launch_exact_bits_t<4>(c, st) : p.kp == 8 ? launch_exact_bits_t<8>(c, st)
+                                                                      : launch_exact_bits_t<16>(c, st);
+            if (e) return e;
+        }
+        return ESOM_OK;
+    }
+    KTimer tm("knn_tc2_kernel", st);
     switch (p.kp) {
         case 4: return launch_tc2_w<4>(a, W, st);
         case 8: return launch_tc2_w<8>(a, W, st);

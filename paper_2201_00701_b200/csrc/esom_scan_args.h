@@ -83,6 +83,8 @@ struct Tc2Args {
     double* qe_sum;
     int32_t* flag;
     int32_t* stats;          // [0] += logged candidates, [1] += slow-path points (diagnostic, nullable)
+    uint32_t* cbits;         // split mode (g > 256): n x gpad/32 candidate bitmaps (nullable = fused)
+    int2* cinfo;             // split mode: n x {candidates (-1: non-finite input), non-empty word mask}
 };
 
 // tensor-core GEMM screen for d > 32 (esom_tc3.cuh)
@@ -133,6 +135,8 @@ int launch_tc_t(TcArgs a, cudaStream_t st);  // esom_tc.cuh, instantiated in ins
 
 template <int KP, int W>
 int launch_tc2_t(Tc2Args a, cudaStream_t st);  // esom_tc2.cuh, instantiated in inst/tc2.cu
+template <int KP>
+int launch_exact_bits_t(Tc2Args a, cudaStream_t st);
 
 template <int DC, int KP>
 int launch_scan_t(ScanArgs a, cudaStream_t st);   // esom_scan.cuh, instantiated in inst/*.cu

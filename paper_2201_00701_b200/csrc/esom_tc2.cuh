@@ -209,7 +209,7 @@ __device__ __forceinline__ float kth_of_32(const float (&gm)[32], int k) {
 template <int KP, int W>
 __host__ __device__ constexpr int tc2_slot_bars() { return (W + kTc2Slots - 1) / kTc2Slots + 1; }
 
-template <int KP, int W, bool RS>
+template <int KP, int W, bool RS, bool SPLIT>
 __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
     constexpr int S = kTc2Slots;
     constexpr int M = tc2_slot_bars<KP, W>();  // release barriers per slot (no parity aliasing, see acquire)
@@ -236,9 +236,10 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
     unsigned char* Ahi = p + (size_t)w * 2 * a_bytes;
     unsigned char* Alo = Ahi + a_bytes;
     p += (size_t)W * 2 * a_bytes;
+    // fused mode: candidate bitmaps and locality-sort keys in smem; SPLIT mode: bitmaps to global
     uint32_t* bmap0 = reinterpret_cast<uint32_t*>(p) + (size_t)w * nwords * 128;  // [word][128]
     uint32_t* bmap = bmap0 + wt;
-    p += (size_t)W * nwords * 128 * 4;
+    if (!SPLIT) p += (size_t)W * nwords * 128 * 4;
     uint32_t* pkey = reinterpret_cast<uint32_t*>(p) + (size_t)w * 4 * 128;  // per WG: key | cnt | nzw | bad
 
     if (tid == 0) {
@@ -411,7 +412,11 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
                 tmem_wait_ld();
                 const uint32_t m = le_mask32(v0, tcut, std::make_integer_sequence<int, 32>{});
                 const int wd = wb + (c0 >> 5);
-                bmap[(size_t)wd * 128] = m;
+                if (SPLIT) {
+                    if (valid) a.cbits[(size_t)i * nwords + wd] = m;
+                } else {
+                    bmap[(size_t)wd * 128] = m;
+                }
                 nzw |= (m != 0u) ? (1u << wd) : 0u;
                 cnt += __popc(m);
             }
@@ -419,6 +424,11 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         // ---- release the slot: the next tile's MMA may overwrite it ----
         tc_fence_before();
         mbar_arrive(&bar_slot[slot][use % M]);
+        if (SPLIT) {  // the exact phase runs in knn_exact_bits_kernel
+            if (valid) a.cinfo[i] = make_int2(xbad ? -1 : cnt, (int)nzw);
+            stat_local += valid ? cnt : 0;
+            continue;
+        }
 
         const uint32_t* bx;  // bitmap column of the point this thread re-evaluates
         // ---- locality: the WG's threads take the tile's points in order of their
@@ -498,7 +508,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
                         nzw &= nzw - 1u;
                         m = bx[(size_t)(wi < 0 ? 0 : wi) * 128];
                     }
-                    jq[u] = 32 * wi + (__ffs(m) - 1);
+                    jq[u] = max(32 * wi + (__ffs(m) - 1), 0);  // past the last candidate: any valid row
                     m &= m - 1u;
                 }
                 const float4* lr[4];
@@ -569,23 +579,27 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
 }
 
 template <int W>
-size_t tc2_smem_bytes(const Tc2Args& a, bool rows_smem) {
+size_t tc2_smem_bytes(const Tc2Args& a, bool rows_smem, bool split = false) {
     size_t b = 2 * (size_t)a.gpad * a.d16 * 2;                             // B hi/lo
     b += ((size_t)a.gpad * 4 + 127) / 128 * 128;                           // |l|^2
-    if (rows_smem) b += ((size_t)a.gpad * a.ls * 4 + 127) / 128 * 128;     // f32 rows
+    if (rows_smem && !split) b += ((size_t)a.gpad * a.ls * 4 + 127) / 128 * 128;  // f32 rows
     b += (size_t)W * 2 * 128 * a.d16 * 2;                                  // A hi/lo per WG
-    b += (size_t)W * (a.gpad / 32) * 128 * 4;                              // candidate bitmaps
-    b += (size_t)W * 4 * 128 * 4;                                          // locality sort keys
+    if (!split) {
+        b += (size_t)W * (a.gpad / 32) * 128 * 4;                          // candidate bitmaps
+        b += (size_t)W * 4 * 128 * 4;                                      // locality sort keys
+    }
     return b + 256;
 }
 
 template <int KP, int W>
 int launch_tc2_t(Tc2Args a, cudaStream_t st) {
     const size_t cap = (size_t)esom_host::max_smem_optin();
-    const bool rs = tc2_smem_bytes<W>(a, true) <= cap && !getenv("ESOM_TC2_ROWS_L2");
-    const size_t smem = tc2_smem_bytes<W>(a, rs);
+    const bool split = a.cbits != nullptr;
+    const bool rs = !split && tc2_smem_bytes<W>(a, true) <= cap && !getenv("ESOM_TC2_ROWS_L2");
+    const size_t smem = tc2_smem_bytes<W>(a, rs, split);
     if (smem > cap) return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "tc2: shape exceeds shared memory%s", "");
-    auto kern = rs ? knn_tc2_kernel<KP, W, true> : knn_tc2_kernel<KP, W, false>;
+    auto kern = split ? knn_tc2_kernel<KP, W, false, true>
+                      : (rs ? knn_tc2_kernel<KP, W, true, false> : knn_tc2_kernel<KP, W, false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t ntiles = (a.n + 127) / 128;
     int64_t grid = esom_host::num_sms();
@@ -594,6 +608,160 @@ int launch_tc2_t(Tc2Args a, cudaStream_t st) {
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, 128 * W, smem, st>>>(a);
     return esom_host::cuda_check("knn_tc2_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Exact phase of the split screen (g > 256, esom_tc2.cuh SPLIT mode): thread =
+// point, landmark rows (gpad x ls f32, up to 147 KB at g = 1024) staged once per
+// CTA by TMA, candidate bitmaps from the screen; same arithmetic and ordered
+// insertion as the fused kernel.  Splitting frees the screen's shared memory
+// (B stays resident, more warpgroups) and gives the exact phase the rows.
+// ---------------------------------------------------------------------------
+constexpr int kExactBitsThreads = 512;
+
+template <int KP>
+__global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc2Args a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bar_load;
+    const int tid = threadIdx.x;
+    const int d = a.d, d16 = a.d16, k = a.k, ls = a.ls;
+    const int off = KP - k;
+    const int nwords = a.gpad >> 5;
+    float* Ls = reinterpret_cast<float*>(smem_raw);
+    const uint32_t r_bytes = (uint32_t)a.gpad * ls * 4u;
+    if (tid == 0) {
+        mbar_init(&bar_load, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&bar_load, r_bytes);
+        tma_bulk_g2s(Ls, a.Lrow, r_bytes, &bar_load);
+    }
+    mbar_wait(&bar_load, 0);
+    const f2 nz = f2_pack(-0.0f, -0.0f);
+    const int d4 = (d16 + 3) >> 2;
+    double qe_local = 0.0;
+    int slow_local = 0;
+    for (int64_t i = blockIdx.x * (int64_t)kExactBitsThreads + tid; i < a.n;
+         i += (int64_t)gridDim.x * kExactBitsThreads) {
+        const int2 info = a.cinfo[i];
+        const int cnt = info.x;
+        uint32_t nzw = (uint32_t)info.y;
+        const uint32_t* bx = a.cbits + (size_t)i * nwords;
+        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+        int b0 = 0;
+        float d0 = 0.0f;
+        int written = 0;
+        if (cnt >= 0) {
+            float x[32];
+            const float* xr = a.X + i * d;
+            if ((d & 3) == 0) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (c < d) u = __ldg(reinterpret_cast<const float4*>(xr + c));
+                    x[c] = u.x; x[c + 1] = u.y; x[c + 2] = u.z; x[c + 3] = u.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) x[c] = c < d ? __ldg(xr + c) : 0.0f;
+            }
+            float td[KP];
+            int ti[KP];
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                td[q] = q >= off ? kInf : -kInf;
+                ti[q] = a.g;
+            }
+            int wi = 0;
+            uint32_t m = 0;
+            for (int e = 0; e < cnt; e += 4) {
+                int jq[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (m == 0u) {
+                        wi = __ffs(nzw) - 1;
+                        nzw &= nzw - 1u;
+                        m = __ldg(bx + (wi < 0 ? 0 : wi));
+                    }
+                    jq[u] = max(32 * wi + (__ffs(m) - 1), 0);  // past the last candidate: any valid row
+                    m &= m - 1u;
+                }
+                const float4* lr[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) lr[u] = reinterpret_cast<const float4*>(Ls + (size_t)jq[u] * ls);
+                float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    if (c4 < d4) {
+                        const f2 x01 = f2_pack(x[4 * c4], x[4 * c4 + 1]);
+                        const f2 x23 = f2_pack(x[4 * c4 + 2], x[4 * c4 + 3]);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float4 l4 = lr[u][c4];
+                            const f2 q01 = f2_sq(f2_sub(x01, f2_pack(l4.x, l4.y)), nz);
+                            const f2 q23 = f2_sq(f2_sub(x23, f2_pack(l4.z, l4.w)), nz);
+                            float a0, a1, a2, a3;
+                            f2_unpack(q01, a0, a1);
+                            f2_unpack(q23, a2, a3);
+                            s4[u] = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s4[u], a0), a1), a2), a3);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (e + u < cnt && s4[u] < td[KP - 1]) topk_insert<KP>(td, ti, s4[u], jq[u]);
+            }
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                if (q >= off) {
+                    written += ti[q] < a.g ? 1 : 0;
+                    if (oi) {
+                        oi[q - off] = ti[q];
+                        od[q - off] = td[q];
+                    }
+                    if (q == off) {
+                        b0 = ti[q];
+                        d0 = td[q];
+                    }
+                }
+            }
+        }
+        if (written != k) {
+            const SlowNearest sn = knn_point_slow(a.X + i * d, d, a.L, a.g, k, oi, od);
+            b0 = sn.b0;
+            d0 = sn.d0;
+            ++slow_local;
+        }
+        if (a.bmu) a.bmu[i] = b0;
+        if (a.qe_sum) qe_local += (double)d0;
+        if (a.accS) {
+            atomicAdd(a.accC + b0, 1.0);
+            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(a.X + i * d + c));
+        }
+    }
+    if (a.stats && slow_local) atomicAdd(a.stats + 1, slow_local);
+    if (a.qe_sum) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) qe_local += __shfl_xor_sync(0xffffffffu, qe_local, o);
+        if ((tid & 31) == 0 && qe_local != 0.0) atomicAdd(a.qe_sum, qe_local);
+    }
+}
+
+template <int KP>
+int launch_exact_bits_t(Tc2Args a, cudaStream_t st) {
+    const size_t smem = (size_t)a.gpad * a.ls * 4 + 128;
+    if (smem > (size_t)esom_host::max_smem_optin())
+        return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact rows exceed shared memory%s", "");
+    auto kern = knn_exact_bits_kernel<KP>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t grid = (a.n + kExactBitsThreads - 1) / kExactBitsThreads;
+    if (grid > esom_host::num_sms()) grid = esom_host::num_sms();
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, kExactBitsThreads, smem, st>>>(a);
+    return esom_host::cuda_check("knn_exact_bits_kernel");
 }
 
 }  // namespace esom

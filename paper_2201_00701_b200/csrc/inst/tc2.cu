@@ -2,6 +2,7 @@
 #include "../esom_tc2.cuh"
 namespace esom {
 #define ESOM_TC2(KP) \
+    template int launch_exact_bits_t<KP>(Tc2Args, cudaStream_t); \
     template int launch_tc2_t<KP, 2>(Tc2Args, cudaStream_t); \
     template int launch_tc2_t<KP, 3>(Tc2Args, cudaStream_t); \
     template int launch_tc2_t<KP, 4>(Tc2Args, cudaStream_t);
