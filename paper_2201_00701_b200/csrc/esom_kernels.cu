@@ -798,7 +798,7 @@ struct ModelLayout {
     size_t cen3, b3hi, b3lo, ln3, ls3, a3hi, a3lo, xn3, cand3, cnt3, bmu3, perm3, hist3;
     // split tc2 screen (d <= 32, g > 256): per-chunk candidate bitmaps + info
     int64_t t2chunk;
-    size_t t2bits, t2info;
+    size_t t2bits, t2info, t2key, t2perm, t2hist;
 };
 
 size_t a256(size_t b) { return (b + 255) / 256 * 256; }
@@ -831,10 +831,13 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
         o += a256((size_t)m.gpad * m.ls * 4);
     }
     m.t2chunk = 0;
-    if (d <= 32 && m.gpad > 256 && m.gpad <= 1024) {
+    if (d <= 32 && m.gpad <= 1024) {
         m.t2chunk = 1 << 20;
         m.t2bits = o;  o += a256((size_t)m.t2chunk * (m.gpad / 32) * 4);
         m.t2info = o;  o += a256((size_t)m.t2chunk * 8);
+        m.t2key = o;   o += a256((size_t)m.t2chunk * 4);
+        m.t2perm = o;  o += a256((size_t)m.t2chunk * 4);
+        m.t2hist = o;  o += a256((size_t)m.gpad * 4);
     }
     m.t3 = d > 32 && k <= 32 && g <= 65535;
     if (m.t3) {
@@ -932,8 +935,10 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
     a.qe_sum = s.qe_sum;
     a.flag = s.flag;
     a.stats = tc_stats_ptr();
-    if (m.t2chunk && !getenv("ESOM_TC2_FUSED")) {
-        const int Ws = getenv("ESOM_TC2_W") ? W : 3;  // measured best for the screen-only kernel (C4)
+    // screen-only kernel + separate exact kernel (default; ESOM_TC2_FUSED=1 keeps the fused kernel)
+    const bool split = m.t2chunk && !getenv("ESOM_TC2_FUSED");
+    if (split) {
+        const int Ws = getenv("ESOM_TC2_W") ? W : (m.gpad > 256 ? 3 : 4);  // measured best (C4 / C2)
         // g > 256: screen-only kernel (more warpgroups: no bitmaps / rows in its smem) writes
         // candidate bitmaps; knn_exact_bits_kernel re-evaluates them with the rows in smem
         char* w = const_cast<char*>(ws);
@@ -946,6 +951,8 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
             c.bmu = s.bmu ? s.bmu + s0 : nullptr;
             c.cbits = reinterpret_cast<uint32_t*>(w + m.t2bits);
             c.cinfo = reinterpret_cast<int2*>(w + m.t2info);
+            const bool lsort = c.n >= 4096 && !getenv("ESOM_TC2_NOSORT");
+            c.ckey = lsort ? reinterpret_cast<int32_t*>(w + m.t2key) : nullptr;
             int e;
             {
                 KTimer tm("knn_tc2_kernel", st);
@@ -953,6 +960,12 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
                                                                         : launch_tc2_w<16>(c, Ws, st);
             }
             if (e) return e;
+            if (lsort) {
+                c.perm = reinterpret_cast<int32_t*>(w + m.t2perm);
+                if (int e2 = bmu_sort(c.ckey, c.n, 1, s.g, reinterpret_cast<int32_t*>(w + m.t2hist),
+                                      const_cast<int32_t*>(c.perm), st))
+                    return e2;
+            }
             KTimer tm2("knn_exact_bits_kernel", st);
             e = p.kp == 4 ? launch_exact_bits_t<4>(c, st) : p.kp == 8 ? launch_exact_bits_t<8>(c, st)
                                                                       : launch_exact_bits_t<16>(c, st);

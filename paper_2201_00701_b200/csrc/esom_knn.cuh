@@ -95,4 +95,61 @@ __device__ __forceinline__ int vlist_count_lt(const float (&vd)[KP], float v) {
     return c;
 }
 
+// ---- batched top-16 (exact phase): sort 8 new candidates, merge into the
+// sorted 16-list by a bitonic half-cleaner + bitonic merge.  Compares values
+// only; equal values are detected afterwards (adjacent equal list entries, or
+// a discarded value equal to the last kept one) and the caller falls back to
+// the index-ordered insertion, so the result is the (distance, index) order.
+__device__ __forceinline__ void ce_vj(float& va, int& ja, float& vb, int& jb) {
+    const bool sw = va > vb;
+    const float lo = fminf(va, vb), hi = fmaxf(va, vb);
+    const int jl = sw ? jb : ja, jh = sw ? ja : jb;
+    va = lo;
+    vb = hi;
+    ja = jl;
+    jb = jh;
+}
+
+// Batcher odd-even merge sort of 8 (19 comparators, generated)
+__device__ __forceinline__ void sort8_vj(float (&v)[8], int (&j)[8]) {
+    ce_vj(v[0], j[0], v[1], j[1]);
+    ce_vj(v[2], j[2], v[3], j[3]);
+    ce_vj(v[4], j[4], v[5], j[5]);
+    ce_vj(v[6], j[6], v[7], j[7]);
+    ce_vj(v[0], j[0], v[2], j[2]);
+    ce_vj(v[1], j[1], v[3], j[3]);
+    ce_vj(v[4], j[4], v[6], j[6]);
+    ce_vj(v[5], j[5], v[7], j[7]);
+    ce_vj(v[1], j[1], v[2], j[2]);
+    ce_vj(v[5], j[5], v[6], j[6]);
+    ce_vj(v[0], j[0], v[4], j[4]);
+    ce_vj(v[1], j[1], v[5], j[5]);
+    ce_vj(v[2], j[2], v[6], j[6]);
+    ce_vj(v[3], j[3], v[7], j[7]);
+    ce_vj(v[2], j[2], v[4], j[4]);
+    ce_vj(v[3], j[3], v[5], j[5]);
+    ce_vj(v[1], j[1], v[2], j[2]);
+    ce_vj(v[3], j[3], v[4], j[4]);
+    ce_vj(v[5], j[5], v[6], j[6]);
+}
+
+// L (ascending, 16) <- the 16 smallest of L and B (8, ascending); dmin tracks the
+// smallest discarded value
+__device__ __forceinline__ void merge16_8(float (&L)[16], int (&LJ)[16], const float (&B)[8], const int (&BJ)[8],
+                                          float& dmin) {
+#pragma unroll
+    for (int i = 8; i < 16; ++i) {  // half-cleaner against the reversed, +inf-padded B
+        const float y = B[15 - i];
+        const bool take = y < L[i];
+        dmin = fminf(dmin, fmaxf(L[i], y));
+        LJ[i] = take ? BJ[15 - i] : LJ[i];
+        L[i] = fminf(L[i], y);
+    }
+#pragma unroll
+    for (int st = 8; st > 0; st >>= 1)  // bitonic merge (ascending)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if ((i & st) == 0) ce_vj(L[i], LJ[i], L[i + st], LJ[i + st]);
+}
+
 }  // namespace esom

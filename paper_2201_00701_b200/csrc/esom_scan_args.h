@@ -85,6 +85,8 @@ struct Tc2Args {
     int32_t* stats;          // [0] += logged candidates, [1] += slow-path points (diagnostic, nullable)
     uint32_t* cbits;         // split mode (g > 256): n x gpad/32 candidate bitmaps (nullable = fused)
     int2* cinfo;             // split mode: n x {candidates (-1: non-finite input), non-empty word mask}
+    int32_t* ckey;           // split mode: n x lowest candidate (locality sort key)
+    const int32_t* perm;     // split mode, exact kernel: visiting order (nullable)
 };
 
 // tensor-core GEMM screen for d > 32 (esom_tc3.cuh)

@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         // the mask of non-empty words (gpad <= 1024: one 32-bit word) ----
         int cnt = 0;
         uint32_t nzw = 0;
+        int first = -1;  // lowest candidate (split mode: locality sort key)
         for (int r = 0; r < R; ++r) {
             const int nr = (R > 1) ? run_round(r) : min(kTc2SlotCols, gpad);
             const int wb = (kTc2SlotCols * r) >> 5;
@@ -414,6 +415,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
                 const int wd = wb + (c0 >> 5);
                 if (SPLIT) {
                     if (valid) a.cbits[(size_t)i * nwords + wd] = m;
+                    if (first < 0 && m) first = 32 * wd + __ffs(m) - 1;
                 } else {
                     bmap[(size_t)wd * 128] = m;
                 }
@@ -425,7 +427,10 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         tc_fence_before();
         mbar_arrive(&bar_slot[slot][use % M]);
         if (SPLIT) {  // the exact phase runs in knn_exact_bits_kernel
-            if (valid) a.cinfo[i] = make_int2(xbad ? -1 : cnt, (int)nzw);
+            if (valid) {
+                a.cinfo[i] = make_int2(xbad ? -1 : cnt, (int)nzw);
+                if (a.ckey) a.ckey[i] = first < 0 ? 0 : first;
+            }
             stat_local += valid ? cnt : 0;
             continue;
         }
@@ -629,6 +634,9 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
     const int nwords = a.gpad >> 5;
     float* Ls = reinterpret_cast<float*>(smem_raw);
     const uint32_t r_bytes = (uint32_t)a.gpad * ls * 4u;
+    // per-thread copy of the point's candidate bitmap ([word][thread]): the extraction
+    // then waits on shared, not global, memory
+    uint32_t* bsm = reinterpret_cast<uint32_t*>(smem_raw + ((r_bytes + 127) / 128) * 128) + tid;
     if (tid == 0) {
         mbar_init(&bar_load, 1);
         fence_mbar_init();
@@ -639,16 +647,31 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
         tma_bulk_g2s(Ls, a.Lrow, r_bytes, &bar_load);
     }
     mbar_wait(&bar_load, 0);
-    const f2 nz = f2_pack(-0.0f, -0.0f);
+    const f2 nz2 = f2_pack(-0.0f, -0.0f);
     const int d4 = (d16 + 3) >> 2;
     double qe_local = 0.0;
     int slow_local = 0;
-    for (int64_t i = blockIdx.x * (int64_t)kExactBitsThreads + tid; i < a.n;
-         i += (int64_t)gridDim.x * kExactBitsThreads) {
+    for (int64_t pos = blockIdx.x * (int64_t)kExactBitsThreads + tid; pos < a.n;
+         pos += (int64_t)gridDim.x * kExactBitsThreads) {
+        // points grouped by lowest candidate: a warp's lanes share landmark rows (smem broadcasts)
+        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
         const int2 info = a.cinfo[i];
         const int cnt = info.x;
         uint32_t nzw = (uint32_t)info.y;
-        const uint32_t* bx = a.cbits + (size_t)i * nwords;
+        {
+            const uint32_t* bg = a.cbits + (size_t)i * nwords;
+            if ((nwords & 3) == 0) {
+                for (int w4 = 0; w4 < nwords; w4 += 4) {
+                    const uint4 u = __ldg(reinterpret_cast<const uint4*>(bg + w4));
+                    bsm[(w4 + 0) * kExactBitsThreads] = u.x;
+                    bsm[(w4 + 1) * kExactBitsThreads] = u.y;
+                    bsm[(w4 + 2) * kExactBitsThreads] = u.z;
+                    bsm[(w4 + 3) * kExactBitsThreads] = u.w;
+                }
+            } else {
+                for (int w1 = 0; w1 < nwords; ++w1) bsm[w1 * kExactBitsThreads] = __ldg(bg + w1);
+            }
+        }
         int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
         float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
         int b0 = 0;
@@ -668,23 +691,15 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
 #pragma unroll
                 for (int c = 0; c < 32; ++c) x[c] = c < d ? __ldg(xr + c) : 0.0f;
             }
-            float td[KP];
-            int ti[KP];
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                td[q] = q >= off ? kInf : -kInf;
-                ti[q] = a.g;
-            }
-            int wi = 0;
-            uint32_t m = 0;
-            for (int e = 0; e < cnt; e += 4) {
-                int jq[4];
+            const uint32_t nzw0 = nzw;
+            // exact distances of the next 4 candidates of the bitmap (index order)
+            auto next4 = [&](int& wi, uint32_t& m, uint32_t& nz, int* jq, float* s4) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     if (m == 0u) {
-                        wi = __ffs(nzw) - 1;
-                        nzw &= nzw - 1u;
-                        m = __ldg(bx + (wi < 0 ? 0 : wi));
+                        wi = __ffs(nz) - 1;
+                        nz &= nz - 1u;
+                        m = bsm[(wi < 0 ? 0 : wi) * kExactBitsThreads];
                     }
                     jq[u] = max(32 * wi + (__ffs(m) - 1), 0);  // past the last candidate: any valid row
                     m &= m - 1u;
@@ -692,7 +707,8 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                 const float4* lr[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) lr[u] = reinterpret_cast<const float4*>(Ls + (size_t)jq[u] * ls);
-                float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) s4[u] = 0.0f;
 #pragma unroll
                 for (int c4 = 0; c4 < 8; ++c4) {
                     if (c4 < d4) {
@@ -701,8 +717,8 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const float4 l4 = lr[u][c4];
-                            const f2 q01 = f2_sq(f2_sub(x01, f2_pack(l4.x, l4.y)), nz);
-                            const f2 q23 = f2_sq(f2_sub(x23, f2_pack(l4.z, l4.w)), nz);
+                            const f2 q01 = f2_sq(f2_sub(x01, f2_pack(l4.x, l4.y)), nz2);
+                            const f2 q23 = f2_sq(f2_sub(x23, f2_pack(l4.z, l4.w)), nz2);
                             float a0, a1, a2, a3;
                             f2_unpack(q01, a0, a1);
                             f2_unpack(q23, a2, a3);
@@ -710,21 +726,81 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                         }
                     }
                 }
+            };
+            bool done = false;
+            if (KP == 16 && k == 16) {
+                // batches of 8: sort, half-clean + bitonic-merge into the sorted 16-list
+                float L[16], dmin = kInf;
+                int LJ[16];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (e + u < cnt && s4[u] < td[KP - 1]) topk_insert<KP>(td, ti, s4[u], jq[u]);
-            }
+                for (int q = 0; q < 16; ++q) {
+                    L[q] = kInf;
+                    LJ[q] = a.g;
+                }
+                int wi = 0;
+                uint32_t m = 0, nz = nzw0;
+                for (int e = 0; e < cnt; e += 8) {
+                    float bv[8];
+                    int bj[8];
+                    next4(wi, m, nz, bj, bv);
+                    if (e + 4 < cnt) {
+                        next4(wi, m, nz, bj + 4, bv + 4);
+                    } else {
 #pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                if (q >= off) {
-                    written += ti[q] < a.g ? 1 : 0;
-                    if (oi) {
-                        oi[q - off] = ti[q];
-                        od[q - off] = td[q];
+                        for (int u = 4; u < 8; ++u) bv[u] = kInf;
                     }
-                    if (q == off) {
-                        b0 = ti[q];
-                        d0 = td[q];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (e + u >= cnt) bv[u] = kInf;
+                    sort8_vj(bv, bj);
+                    merge16_8(L, LJ, bv, bj, dmin);
+                }
+                bool amb = !(L[15] < kInf) || dmin == L[15];
+#pragma unroll
+                for (int q = 0; q < 15; ++q) amb |= L[q] == L[q + 1];
+                if (!amb) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        if (oi) {
+                            oi[q] = LJ[q];
+                            od[q] = L[q];
+                        }
+                    b0 = LJ[0];
+                    d0 = L[0];
+                    written = k;
+                    done = true;
+                }
+            }
+            if (!done) {  // k < KP, or equal distances: index-ordered insertion
+                float td[KP];
+                int ti[KP];
+#pragma unroll
+                for (int q = 0; q < KP; ++q) {
+                    td[q] = q >= off ? kInf : -kInf;
+                    ti[q] = a.g;
+                }
+                int wi = 0;
+                uint32_t m = 0, nz = nzw0;
+                for (int e = 0; e < cnt; e += 4) {
+                    int jq[4];
+                    float s4[4];
+                    next4(wi, m, nz, jq, s4);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (e + u < cnt && s4[u] < td[KP - 1]) topk_insert<KP>(td, ti, s4[u], jq[u]);
+                }
+#pragma unroll
+                for (int q = 0; q < KP; ++q) {
+                    if (q >= off) {
+                        written += ti[q] < a.g ? 1 : 0;
+                        if (oi) {
+                            oi[q - off] = ti[q];
+                            od[q - off] = td[q];
+                        }
+                        if (q == off) {
+                            b0 = ti[q];
+                            d0 = td[q];
+                        }
                     }
                 }
             }
@@ -752,7 +828,7 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
 
 template <int KP>
 int launch_exact_bits_t(Tc2Args a, cudaStream_t st) {
-    const size_t smem = (size_t)a.gpad * a.ls * 4 + 128;
+    const size_t smem = ((size_t)a.gpad * a.ls * 4 + 127) / 128 * 128 + (size_t)(a.gpad / 32) * kExactBitsThreads * 4;
     if (smem > (size_t)esom_host::max_smem_optin())
         return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact rows exceed shared memory%s", "");
     auto kern = knn_exact_bits_kernel<KP>;

@@ -16,10 +16,15 @@ pytestmark = pytest.mark.gpu
 
 
 def run(p, l, k, tc, w=None):
-    saved = {v: os.environ.get(v) for v in ("ESOM_TC", "ESOM_TC2_W")}
+    """w: warpgroups of the split tc2 screen ("f<W>": the fused screen + exact kernel, 0: esom_tc.cuh)."""
+    saved = {v: os.environ.get(v) for v in ("ESOM_TC", "ESOM_TC2_W", "ESOM_TC2_FUSED")}
     os.environ["ESOM_TC"] = "1" if tc else "0"
     if w is not None:
-        os.environ["ESOM_TC2_W"] = str(w)
+        w = str(w)
+        if w.startswith("f"):
+            os.environ["ESOM_TC2_FUSED"] = "1"
+            w = w[1:]
+        os.environ["ESOM_TC2_W"] = w
     try:
         nb = esom.knn_base(p, l, k)
     finally:
@@ -31,7 +36,7 @@ def run(p, l, k, tc, w=None):
     return nb
 
 
-@pytest.mark.parametrize("w", [3, 2, 4, 0])
+@pytest.mark.parametrize("w", [3, 2, 4, "f4", "f3", 0])
 @pytest.mark.parametrize("case", ["c1", "c2", "uniform16", "normal32", "ties", "wide", "rounds300", "c4like",
                                   "g4096", "ties777"])
 def test_tc_equals_scan_and_oracle(case, w):
