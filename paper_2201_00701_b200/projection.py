@@ -209,7 +209,8 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
     want_numpy = not _dev.is_device_tensor(points)
     dev = _dev.cuda_device(points)
     if (isinstance(points, torch.Tensor) and not points.is_cuda and points.is_pinned() and mode == "fast"
-            and k <= 64 and points.dtype == torch.float32 and points.is_contiguous() and ps[0] >= 2 * PIPE_CHUNK
+            and k <= 64 and points.dtype == torch.float32 and points.is_contiguous()
+            and ps[0] >= 2 * _pipe_chunk(model.hi.shape[0])
             and not chunk_size):
         with torch.cuda.device(dev):
             return _embed_host_pipelined(points, model, k, dev)
@@ -238,8 +239,14 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
         return _dev.out_like(xy, want_numpy)
 
 
-PIPE_CHUNK = int(os.environ.get("ESOM_PIPE_CHUNK", 1 << 16))  # points per H2D/compute/D2H stage
-PIPE_DEPTH = int(os.environ.get("ESOM_PIPE_DEPTH", 4))        # rotating device buffers
+# points per H2D/compute/D2H stage (measured on B200, PCIe 54 GB/s each way: 2^17 best at
+# g <= 256, 2^18 above, where each stage carries more fixed kernel work) and rotating buffers
+PIPE_CHUNK = int(os.environ.get("ESOM_PIPE_CHUNK", 0)) or None
+PIPE_DEPTH = int(os.environ.get("ESOM_PIPE_DEPTH", 3))
+
+
+def _pipe_chunk(g: int) -> int:
+    return PIPE_CHUNK or (1 << 17 if g <= 256 else 1 << 18)
 
 
 def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
@@ -254,7 +261,7 @@ def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
     out = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
     comp = torch.cuda.current_stream(dev)
     h2d, d2h = _copy_streams(dev)
-    c = min(PIPE_CHUNK, n)
+    c = min(_pipe_chunk(model.hi.shape[0]), n)
     nb = PIPE_DEPTH
     Xd = [torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(nb)]
     Yd = [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(nb)]
