@@ -953,6 +953,7 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
             c.cinfo = reinterpret_cast<int2*>(w + m.t2info);
             const bool lsort = c.n >= 4096 && !getenv("ESOM_TC2_NOSORT");
             c.ckey = lsort ? reinterpret_cast<int32_t*>(w + m.t2key) : nullptr;
+            c.key_by_count = getenv("ESOM_TC2_KEYCNT") ? 1 : 0;
             int e;
             {
                 KTimer tm("knn_tc2_kernel", st);
@@ -1101,6 +1102,7 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         x.qe_sum = a.qe_sum;
         x.accS = a.accS;
         x.accC = a.accC;
+        x.stats = tc_stats_ptr();
         {
             KTimer tm("knn_exact_group_kernel", st);
             if (int e3 = launch_exact_warp_t<32>(x, st)) return e3;

@@ -87,6 +87,7 @@ struct Tc2Args {
     int2* cinfo;             // split mode: n x {candidates (-1: non-finite input), non-empty word mask}
     int32_t* ckey;           // split mode: n x lowest candidate (locality sort key)
     const int32_t* perm;     // split mode, exact kernel: visiting order (nullable)
+    int key_by_count;        // experiment: sort the exact phase by candidate count instead of locality
 };
 
 // tensor-core GEMM screen for d > 32 (esom_tc3.cuh)
@@ -122,6 +123,7 @@ struct T3ExactArgs {
     double* qe_sum;
     double* accS;
     double* accC;
+    int32_t* stats;          // diagnostic: [2] += union sizes, [3] += groups evaluated, [4] += splits
 };
 
 template <int KP>

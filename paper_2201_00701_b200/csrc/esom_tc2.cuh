@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         if (SPLIT) {  // the exact phase runs in knn_exact_bits_kernel
             if (valid) {
                 a.cinfo[i] = make_int2(xbad ? -1 : cnt, (int)nzw);
-                if (a.ckey) a.ckey[i] = first < 0 ? 0 : first;
+                if (a.ckey) a.ckey[i] = a.key_by_count ? min(cnt, a.g - 1) : (first < 0 ? 0 : first);
             }
             stat_local += valid ? cnt : 0;
             continue;

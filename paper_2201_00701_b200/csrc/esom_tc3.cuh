@@ -625,6 +625,10 @@ __global__ void __launch_bounds__(kT3GWarps * 32) knn_exact_group_kernel(T3Exact
                 }
                 U += __shfl_sync(0xffffffffu, incl, 31);
             }
+            if (a.stats && lane == 0) {
+                atomicAdd(a.stats + 2, U);
+                atomicAdd(a.stats + (U > kT3UMax ? 4 : 3), 1);
+            }
             if (U > kT3UMax) {  // split the subset in two halves
                 unsigned lo = 0u, rest = sm;
                 const int half = __popc(sm) / 2;

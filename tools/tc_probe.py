@@ -24,7 +24,7 @@ def main(names):
     dev = torch.device("cuda", 0)
     L = _lib.load()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(8, dtype=torch.int32, device=dev)
     for name in names:
         pts, hi, lo, k, _ = make_inputs(name, 0)
         n, d = pts.shape
@@ -63,7 +63,7 @@ def main(names):
             same = (torch.equal(idx, outs["scan"][0]) and torch.equal(sqd, outs["scan"][1])) if "scan" in outs else None
             print(json.dumps({"shape": name, "variant": var, "ms": statistics.median(ts[1:]),
                               "Mpts_per_s": n / statistics.median(ts[1:]) / 1e3,
-                              "cand_per_pt": int(cnt[0].item()) / n, "slow_pts": int(cnt[1].item()), "bit_equal_scan": same}), flush=True)
+                              "cand_per_pt": int(cnt[0].item()) / n, "slow_pts": int(cnt[1].item()), "union_mean": int(cnt[2].item()) / max(1, int(cnt[3].item()) + int(cnt[4].item())), "groups": int(cnt[3].item()), "splits": int(cnt[4].item()), "bit_equal_scan": same}), flush=True)
         os.environ.pop("ESOM_TC2_W", None)
         os.environ.pop("ESOM_TC", None)
         del X, outs
