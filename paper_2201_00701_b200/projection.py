@@ -254,7 +254,8 @@ def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
     kernels on the compute stream and the D2H of finished chunks on a second
     copy stream (PCIe is full duplex), with PIPE_DEPTH rotating device
     buffers, so the end-to-end time approaches max(H2D, compute) instead of
-    their sum."""
+    their sum.  (A ramp of smaller first stages measured slower: the fixed
+    per-stage cost outweighs the shorter pipeline fill.)"""
     n, d = host.shape
     pm = PreparedModel(model.hi, model.lo, k, device=dev)
     flag = _dev.new_flag(dev)
@@ -263,15 +264,19 @@ def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
     h2d, d2h = _copy_streams(dev)
     c = min(_pipe_chunk(model.hi.shape[0]), n)
     nb = PIPE_DEPTH
-    Xd = [torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(nb)]
-    Yd = [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(nb)]
+    Xd, Yd, fresh = _pipe_buffers(dev, nb, c, d)
+    if fresh:
+        h2d.wait_stream(comp)  # new allocations: order after prior work on the compute stream
     loaded = [torch.cuda.Event() for _ in range(nb)]
     computed = [None] * nb  # compute of the chunk that last used buffer b (Xd[b] free, Yd[b] ready)
     drained = [None] * nb   # D2H of the chunk that last used buffer b (Yd[b] free)
-    h2d.wait_stream(comp)   # model preparation precedes the first chunk
-    for it, s in enumerate(range(0, n, c)):
+    stages, s, m = [], 0, c
+    while s < n:
+        stages.append((s, min(m, n - s)))
+        s += m
+        m = min(2 * m, c)
+    for it, (s, m) in enumerate(stages):
         b = it % nb
-        m = min(c, n - s)
         if computed[b] is not None:
             h2d.wait_event(computed[b])
         with torch.cuda.stream(h2d):
@@ -295,6 +300,22 @@ def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
     _dev.raise_if_nonfinite(flag)
     _dev.raise_if_nonfinite(pm.flag)
     return out.numpy()
+
+
+_PIPE_BUFS: dict = {}
+
+
+def _pipe_buffers(dev, nb: int, c: int, d: int):
+    """Device staging buffers of the host pipeline, kept across calls (the
+    synchronous return of the pipeline guarantees they are idle)."""
+    key = (str(dev), nb, c, d)
+    fresh = key not in _PIPE_BUFS
+    if fresh:
+        _PIPE_BUFS.clear()
+        _PIPE_BUFS[key] = ([torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(nb)],
+                           [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(nb)])
+    Xd, Yd = _PIPE_BUFS[key]
+    return Xd, Yd, fresh
 
 
 _COPY_STREAMS: dict = {}
