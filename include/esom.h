@@ -138,6 +138,63 @@ int esom_batch_som_update(const double *acc_S, const double *acc_C, const float 
                           int32_t d, double sigma, double alpha, int32_t mode, float *hi_inout,
                           cudaStream_t stream);
 
+/* ---- data formats either side of the path ---- */
+
+/* Frame colours: rint((X[:, color_dim] - lo) / span * 255) as u8, 128 when
+ * span <= 0 (lo, span = the column's min and max - min).  Replaces
+ * color_channel (ref: engine.py:144-153); bit-exact. */
+int esom_color_channel(const float *X, int64_t n, int32_t d, int32_t color_dim, double lo, double span,
+                       uint8_t *out, cudaStream_t stream);
+
+/* FramePoints wire record, the bytes protocol.encode(FramePoints(frame_id,
+ * xy, colors)) returns (ref: protocol.py:205-210, 216-218): u32 length, tag
+ * 0x31, u32 frame_id, u32 n, n×2 f32, n u8 -- esom_frame_points_bytes(n) =
+ * 13 + 9n bytes.  `out` (16-byte aligned) may be device memory or mapped
+ * pinned host memory (written over PCIe by the kernel: zero-copy send). */
+size_t esom_frame_points_bytes(int64_t n);
+/* Device-side address of a page-locked host buffer (cudaHostGetDevicePointer),
+ * NULL if the buffer is not mapped. */
+void *esom_mapped_device_ptr(void *host_ptr);
+int esom_frame_points_pack(const float *xy, const uint8_t *colors, int64_t n, uint32_t frame_id,
+                           uint8_t *out, cudaStream_t stream);
+
+/* FCS DATA segment -> f32 (ref: io.py:113-126; $BYTEORD "4,3,2,1" =
+ * big_endian 1, "1,2,3,4" = 0), with the finiteness check of
+ * Dataset.from_points (ref: core.py:38-40).  raw/out 16-byte aligned
+ * (raw = the DATA bytes copied into device staging); count = n*d values. */
+int esom_fcs_decode(const void *raw, int64_t count, int32_t big_endian, float *out,
+                    int32_t *nonfinite_flag, cudaStream_t stream);
+
+/* Per-dimension f64 min, max, mean and population sd of X (ref: core.py:57-69
+ * compute_dim_stats).  Deterministic blocked sums (not numpy's sequential
+ * order: mean/sd agree to ~1e-15 relative; min/max exactly). */
+size_t esom_dim_stats_workspace_bytes(int64_t n, int32_t d);
+int esom_dim_stats(const float *X, int64_t n, int32_t d, double *mn, double *mx, double *mean,
+                   double *sd, void *workspace, size_t ws_bytes, cudaStream_t stream);
+
+/* Per-dimension transform (ref: io.py:200-225 apply_transform): kind[c] 0
+ * none, 1 minmax, 2 zscore, 3 affine (a[c] * x + b[c]); f64 arithmetic op
+ * for op like numpy, rounded to f32.  All arrays device, length d. */
+int esom_apply_transform(const float *X, int64_t n, int32_t d, const int32_t *kind, const double *a,
+                         const double *b, const double *mn, const double *mx, const double *mean,
+                         const double *sd, float *out, int32_t *nonfinite_flag, cudaStream_t stream);
+
+/* Landmark-side graph ops, f64.
+ * One force-layout step (ref: graphmodel.py:138-192 net_forces + layout_tick):
+ * lo g×2 f32, edges pairs e×2 int32 (i < j) with rest lengths, and a CSR of
+ * signed edge ids per landmark (csr_ptr g+1, csr_edge: e for the first
+ * endpoint, -e-1 for the second, in edge order); pinned g u8 or NULL.
+ * vel_inout g×2 f64 is updated; lo_out g×2 f32; forces_or_null g×2 f64. */
+int esom_layout_tick(const float *lo, int32_t g, const int32_t *pairs, const float *rest,
+                     const int32_t *csr_ptr, const int32_t *csr_edge, const uint8_t *pinned,
+                     double stiffness, double repulsion, double eps, double damping, double dt,
+                     double *vel_inout, float *lo_out, double *forces_or_null, cudaStream_t stream);
+
+/* hi row for a landmark added at layout position (px, py): inverse-distance
+ * weights over the layout (ref: som.py:82-101); out d f32. */
+int esom_fit_hi(const float *hi, const float *lo, int32_t g, int32_t d, double px, double py, double eps,
+                float *out, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,13 @@ SIGNATURES = {
     "esom_som_tick": [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _f64, _f64, _vp, _sz, _vp],
     "esom_kmeans_tick": [_vp, _i32, _vp, _i32, _vp, _i32, _f64, _vp, _sz, _vp],
     "esom_batch_som_update": [_vp, _vp, _vp, _i32, _i32, _f64, _f64, _i32, _vp, _vp],
+    "esom_color_channel": [_vp, _i64, _i32, _i32, _f64, _f64, _vp, _vp],
+    "esom_frame_points_pack": [_vp, _vp, _i64, C.c_uint32, _vp, _vp],
+    "esom_fcs_decode": [_vp, _i64, _i32, _vp, _vp, _vp],
+    "esom_dim_stats": [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
+    "esom_apply_transform": [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "esom_layout_tick": [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _f64, _f64, _f64, _f64, _f64, _vp, _vp, _vp, _vp],
+    "esom_fit_hi": [_vp, _vp, _i32, _i32, _f64, _f64, _f64, _vp, _vp],
 }
 HELPERS = {
     "esom_version": ([], C.c_int),
@@ -49,6 +56,9 @@ HELPERS = {
     "esom_timing_begin": ([_i32], None),
     "esom_launch_count": ([], C.c_int64),
     "esom_timing_query": ([C.c_char_p, _vp], C.c_double),
+    "esom_frame_points_bytes": ([_i64], C.c_size_t),
+    "esom_mapped_device_ptr": ([_vp], _vp),
+    "esom_dim_stats_workspace_bytes": ([_i64, _i32], C.c_size_t),
 }
 
 

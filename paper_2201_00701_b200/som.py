@@ -98,3 +98,23 @@ def quantization_error(dataset, hi) -> float:
                   _dev.ptr(qe), _dev.ptr(flag), _dev.stream_handle(dev))
         _dev.raise_if_nonfinite(flag)
         return float(qe.item()) / max(n, 1)
+
+
+def fit_hi_for_new_landmark(pos2d, model) -> np.ndarray:
+    """hi row for a landmark added at a layout position: inverse-distance
+    weighting over the layout, an exact hit copies that landmark's hi
+    (ref: som.py:82-101), computed by one CTA (esom_fit_hi)."""
+    if model.hi.shape[0] == 0:
+        raise InputError("empty model")
+    pos = np.asarray(pos2d, dtype=np.float64).ravel()
+    if pos.shape[0] != 2:
+        raise InputError("pos2d must be a 2-vector")
+    dev = _dev.cuda_device(model.hi)
+    with torch.cuda.device(dev):
+        hi = _dev.to_f32(model.hi, dev)
+        lo = _dev.to_f32(model.lo, dev)
+        g, d = hi.shape
+        out = torch.empty(d, dtype=torch.float32, device=dev)
+        _lib.call("esom_fit_hi", _dev.ptr(hi), _dev.ptr(lo), g, d, float(pos[0]), float(pos[1]), FIT_EPS,
+                  _dev.ptr(out), _dev.stream_handle(dev))
+        return out.cpu().numpy()

@@ -1,0 +1,242 @@
+"""Device kernels of the rows either side of the embed path
+against the reference-generated fixtures (tests/golden/make_golden_frames.py)
+and the numpy oracle (oracle/formats.py):
+
+* colours (esom_color_channel) and FramePoints records (esom_frame_points_pack)
+  bit-exact, including every record length mod 16 and the mapped-host write;
+* FCS DATA decode bit-exact (both byte orders, FCS3.1 offsets), errors as the
+  reference; statistics min/max exact, mean/sd to 1e-12 relative;
+* transforms bit-exact given the reference's statistics, <= 1 f32 ulp with
+  the device statistics;
+* FrameEngine (device-resident Engine.tick) vs the reference Engine's frames.
+"""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import formats as F
+import paper_2201_00701_b200 as esom
+from paper_2201_00701_b200 import datagen
+from paper_2201_00701_b200.core import InputError, ParseError
+from paper_2201_00701_b200.engine import DeviceSession, FrameEngine
+from paper_2201_00701_b200.io import (DeviceDataset, DimStats, TransformSpec, apply_transform, compute_dim_stats,
+                                      parse_fcs)
+from paper_2201_00701_b200.protocol import FrameBuffer, encode_frame_points, pack_frame_points
+
+pytestmark = pytest.mark.gpu
+META = json.loads((GOLDEN / "golden_frames.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def gf():
+    return np.load(GOLDEN / "golden_frames.npz")
+
+
+def test_color_channel_bit_exact(gf):
+    for key in ("col", "col2"):
+        sess = DeviceSession(gf[f"{key}_points"])
+        m64 = gf[f"{key}_points"].astype(np.float64)
+        assert np.array_equal(sess.col_min, m64.min(axis=0)) and np.array_equal(sess.col_max, m64.max(axis=0))
+        for c in range(gf[f"{key}_points"].shape[1]):
+            assert np.array_equal(sess.colors(c).cpu().numpy(), gf[f"{key}_colors"][c]), (key, c)
+    with pytest.raises(esom.ParameterError, match="out of range"):
+        sess.colors(99)
+
+
+def test_frame_record_bit_exact(gf):
+    for i, r in enumerate(META["records"]):
+        got = encode_frame_points(r["frame_id"], torch.from_numpy(gf[f"rec{i}_pos"]).cuda(),
+                                  torch.from_numpy(gf[f"rec{i}_col"]).cuda())
+        assert got == gf[f"rec{i}_bytes"].tobytes(), r
+
+
+def test_frame_record_all_tails_and_staging():
+    rng = np.random.default_rng(5)
+    buf = FrameBuffer(13 + 9 * 300)
+    assert buf.dev_ptr is not None  # pinned host memory is mapped (UVA): the kernel writes it directly
+    staged = FrameBuffer(13 + 9 * 300)
+    staged.staging, staged.dev_ptr = torch.empty(staged.capacity, dtype=torch.uint8, device="cuda"), None
+    for n in list(range(0, 40)) + [255, 256, 257, 300]:
+        pos = rng.normal(size=(n, 2)).astype(np.float32)
+        col = rng.integers(0, 256, n).astype(np.uint8)
+        want = F.frame_points_record(n * 7 + 3, pos, col)
+        for b in (buf, staged):
+            b.host.fill_(0xAB)
+            nb = pack_frame_points(torch.from_numpy(pos).cuda(), torch.from_numpy(col).cuda(), n * 7 + 3, b)
+            b.event.synchronize()
+            assert bytes(b.host[:nb].numpy()) == want, n
+            if nb < b.capacity:
+                assert int(b.host[nb]) == 0xAB  # nothing written past the record
+
+
+def test_parse_fcs_bit_exact_and_errors(gf):
+    checked = 0
+    for ent in META["fcs"]:
+        raw = gf[f"fcs_{ent['name']}_raw"].tobytes()
+        if "error" in ent:
+            cls = InputError if ent["error"] == "InputError" else ParseError
+            with pytest.raises(cls) as ei:
+                parse_fcs(raw)
+            assert str(ei.value) == ent["message"], ent["name"]
+            continue
+        ds = parse_fcs(raw)
+        name = ent["name"]
+        assert ds.dim_names == tuple(ent["names"])
+        assert np.array_equal(ds.points.cpu().numpy(), gf[f"fcs_{name}_points"]), name
+        st = ds.dim_stats
+        assert np.array_equal(st.min, gf[f"fcs_{name}_min"]) and np.array_equal(st.max, gf[f"fcs_{name}_max"])
+        np.testing.assert_allclose(st.mean, gf[f"fcs_{name}_mean"], rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(st.sd, gf[f"fcs_{name}_sd"], rtol=1e-12, atol=1e-300)
+        checked += 1
+    assert checked >= 20
+
+
+def test_dim_stats_large_vs_numpy():
+    pts = datagen.gaussians(16, 300_000, 32, seed=9)[0].astype(np.float32) * 100
+    st = compute_dim_stats(torch.from_numpy(pts).cuda())
+    mn, mx, mean, sd = F.dim_stats(pts)
+    assert np.array_equal(st.min, mn) and np.array_equal(st.max, mx)
+    np.testing.assert_allclose(st.mean, mean, rtol=1e-12)
+    np.testing.assert_allclose(st.sd, sd, rtol=1e-12)
+
+
+def test_transforms_bit_exact_given_stats(gf):
+    for ent in META["transforms"]:
+        name = ent["name"]
+        entries = tuple(e if isinstance(e, str) else tuple(e) for e in ent["entries"])
+        s = gf[f"xf_{name}_stats_in"]
+        ds = DeviceDataset(points=torch.from_numpy(gf[f"xf_{name}_in"]).cuda(),
+                           dim_names=tuple(f"dim{i}" for i in range(s.shape[1])),
+                           dim_stats=DimStats(min=s[0], max=s[1], mean=s[2], sd=s[3]))
+        out = apply_transform(ds, TransformSpec(entries=entries))
+        assert np.array_equal(out.points.cpu().numpy(), gf[f"xf_{name}_out"]), name
+        # end to end with the device statistics: within one f32 ulp
+        out2 = apply_transform(DeviceDataset.from_points(gf[f"xf_{name}_in"]), TransformSpec(entries=entries))
+        got, want = out2.points.cpu().numpy(), gf[f"xf_{name}_out"]
+        assert np.all(np.abs(got - want) <= np.spacing(np.abs(want).astype(np.float32)) + 1e-30), name
+    with pytest.raises(esom.ParameterError):
+        apply_transform(DeviceDataset.from_points(np.ones((5, 3), np.float32)), TransformSpec.uniform("zscore", 2))
+    with pytest.raises(InputError, match="non-finite"):
+        DeviceDataset.from_points(np.array([[1.0, np.inf]], np.float32))
+
+
+def test_frame_engine_vs_reference_engine(gf):
+    eng = FrameEngine(gf["col_points"], seed=META["engine"]["seed"], k=16, grid=tuple(META["engine"]["grid"]))
+    assert np.array_equal(eng.model.hi, gf["eng_hi0"])
+    assert eng.embed_params.k == META["engine"]["k_eff"]
+    ext = float(np.ptp(gf["eng_lo"], axis=0).max())
+    for t, tk in enumerate(META["engine"]["ticks"]):
+        fr = eng.tick()
+        assert fr.frame_id == tk["frame_id"]
+        np.testing.assert_allclose(eng.model.hi, gf[f"eng_hi{t + 1}"], rtol=1e-5, atol=1e-6)
+        err = np.abs(fr.positions.cpu().numpy() - gf[f"eng_pos{t}"]).max()
+        assert err <= 1e-4 * ext, (t, err)
+        rec = bytes(eng.frame_record())
+        assert len(rec) == tk["len"]
+        assert rec == F.frame_points_record(tk["frame_id"], fr.positions.cpu().numpy(), gf["eng_colors"])
+    assert np.array_equal(fr.colors.cpu().numpy(), gf["eng_colors"])
+
+
+def test_frame_engine_replay_is_deterministic():
+    pts = datagen.extruded_s(5000, seed=4)
+    recs = []
+    for _ in range(2):
+        eng = FrameEngine(pts, seed=1234, k=16, grid=(8, 8))
+        recs.append([bytes(eng.tick() and eng.frame_record()) for _ in range(5)])
+    assert recs[0] == recs[1]
+    other = FrameEngine(pts, seed=1235, k=16, grid=(8, 8))
+    assert bytes(other.tick() and other.frame_record()) != recs[0][0]
+
+
+def test_landmark_graph_and_layout_vs_reference(gf):
+    e = esom.build_knn_graph(gf["eng_hi0"], 3)
+    assert np.array_equal(e.pairs, gf["graph_pairs"]) and np.array_equal(e.rest, gf["graph_rest"])
+    hi4096 = datagen.gaussians(16, 4096, 32, seed=7)[0].astype(np.float32)
+    e2 = esom.build_knn_graph(torch.from_numpy(hi4096).cuda(), 8)
+    assert np.array_equal(e2.pairs, gf["graph4096_pairs"]) and np.array_equal(e2.rest, gf["graph4096_rest"])
+    lay = META["layout"]
+    st = esom.LayoutState(velocities=gf["layout_vel0"], stiffness=lay["stiffness"], repulsion=lay["repulsion"],
+                          damping=lay["damping"], dt=lay["dt"])
+    f = esom.net_forces(gf["layout_lo0"], e, st)
+    np.testing.assert_allclose(f, gf["layout_forces"], rtol=1e-12, atol=1e-12)
+    lo1, v1 = esom.layout_tick(gf["layout_lo0"], e, st, pinned_rows=lay["pinned"])
+    np.testing.assert_allclose(v1, gf["layout_vel1"], rtol=1e-12, atol=1e-13)
+    assert np.max(np.abs(lo1 - gf["layout_lo1"])) <= 1e-6
+    assert np.array_equal(lo1[lay["pinned"]], gf["layout_lo0"][lay["pinned"]])
+    assert np.all(v1[lay["pinned"]] == 0)
+    # g = 4096 layout (where the device pays off) vs the numpy restatement
+    lo4 = datagen.extruded_s(4096, seed=2)[:, :2].astype(np.float32) * 10
+    st4 = esom.LayoutState.for_count(4096)
+    lo4b, v4 = esom.layout_tick(lo4, e2, st4)
+    want_lo, want_v = F.layout_tick(lo4, e2.pairs, e2.rest, st4.velocities, st4.stiffness, st4.repulsion, 1e-3,
+                                    st4.damping, st4.dt)
+    np.testing.assert_allclose(v4, want_v, rtol=1e-9, atol=1e-12)
+    assert np.max(np.abs(lo4b - want_lo)) <= 1e-5
+
+
+def test_fit_hi_for_new_landmark_vs_reference(gf):
+    model = esom.LandmarkModel.create(gf["eng_hi0"], gf["eng_lo"])
+    for p, want in zip(gf["fit_pos"], gf["fit_hi"]):
+        np.testing.assert_allclose(esom.fit_hi_for_new_landmark(p, model), want, rtol=1e-6)
+    assert np.array_equal(esom.fit_hi_for_new_landmark((0.0, 0.0), model), gf["eng_hi0"][0])  # exact hit
+    with pytest.raises(InputError, match="2-vector"):
+        esom.fit_hi_for_new_landmark((1.0, 2.0, 3.0), model)
+
+
+def _fake_reference_engine(points, seed, grid, k, chunk_size=131072):
+    """The attributes of embedview.engine.Engine that gpu_tick touches, so the
+    installed tick runs here without the reference (ref: engine.py:109-236)."""
+    import dataclasses
+    import sys
+    import types
+
+    from paper_2201_00701_b200 import graphmodel as G
+    from paper_2201_00701_b200.core import EmbedParams, Rng
+    from paper_2201_00701_b200.engine import _nearest_pow2_k, init_model
+
+    mod = types.ModuleType("fake_embedview_engine")
+    mod.MODE_SOM, mod.MODE_GRAPH = "som", "graph"
+    mod.FramePacket = dataclasses.make_dataclass(
+        "FramePacket", ["frame_id", "positions", "landmarks_lo", "landmark_ids", "edges", "colors"])
+    mod.EdgeSet, mod.graphmodel, mod.replace = G.EdgeSet, G, dataclasses.replace
+    sys.modules[mod.__name__] = mod
+    Eng = type("Engine", (), {"__module__": mod.__name__, "tick": esom.engine.gpu_tick,
+                              "apply_command": lambda self, c: None})
+    e = Eng()
+    rng = Rng(seed)
+    ds = esom.Dataset.from_points(points)
+    model = init_model(ds.points, rng, grid)
+    e.state = types.SimpleNamespace(dataset=ds, model=model, mode="som", som_cfg=esom.SomConfig(),
+                                    km_cfg=esom.KmeansConfig(), rng=rng, training_paused=False, chunk_cursor=0,
+                                    frame_id=0, color_dim=0, edges=G.EdgeSet.empty(),
+                                    embed_params=EmbedParams(k=_nearest_pow2_k(k, model.g)))
+    e._queue, e._errors, e._colors, e.chunk_size, e.backend = [], [], None, chunk_size, "bitonic"
+    e._positions = np.zeros((ds.n, 2), np.float32)
+    return e
+
+
+def test_installed_gpu_tick_vs_reference_engine(gf):
+    e = _fake_reference_engine(gf["col_points"], META["engine"]["seed"], tuple(META["engine"]["grid"]), 16)
+    ext = float(np.ptp(gf["eng_lo"], axis=0).max())
+    for t, tk in enumerate(META["engine"]["ticks"]):
+        p = e.tick()
+        assert p.frame_id == tk["frame_id"] and isinstance(p.positions, np.ndarray)
+        np.testing.assert_allclose(e.state.model.hi, gf[f"eng_hi{t + 1}"], rtol=1e-5, atol=1e-6)
+        assert np.abs(p.positions - gf[f"eng_pos{t}"]).max() <= 1e-4 * ext
+        assert np.array_equal(p.colors, gf["eng_colors"])
+
+
+def test_installed_gpu_tick_round_robin_chunks():
+    pts = datagen.extruded_s(3000, seed=6)
+    full = _fake_reference_engine(pts, 5, (6, 6), 16)
+    rr = _fake_reference_engine(pts, 5, (6, 6), 16, chunk_size=1024)
+    rr.full_reprojection = False
+    full.state.training_paused = rr.state.training_paused = True  # fixed model: chunks converge to the full frame
+    want = full.tick().positions
+    got = [rr.tick().positions for _ in range(3)]
+    assert np.array_equal(got[0][1024:], np.zeros((3000 - 1024, 2), np.float32))
+    assert rr.state.chunk_cursor == 0
+    assert np.array_equal(got[2], want)
