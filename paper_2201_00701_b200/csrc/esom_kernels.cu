@@ -160,8 +160,12 @@ __global__ void check_finite_kernel(const float* __restrict__ v, int64_t count, 
 // reference keeps the pair (hd2 >= 1e-12 with hd2 = sum_c (f64)(e*e), e =
 // hi[v,c] - hi[u,c] in f32, ref: projection.py:332-340), else -1.  hd2 is
 // symmetric (f32 subtraction is sign-symmetric), so one triangle suffices.
-__global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, float* __restrict__ T) {
+// *tmax (zeroed by the caller) = max kept T: the model-wide bound the
+// projection uses to decide which points need f64 squared distances.
+__global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, float* __restrict__ T,
+                                  float* __restrict__ tmax) {
     const int64_t total = (int64_t)g * g;
+    float tm = 0.0f;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int u = (int)(e / g), v = (int)(e % g);
         if (v <= u) continue;
@@ -172,8 +176,13 @@ __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, fl
             const float df = __fsub_rn(hv[c], hu[c]);
             hd2 = __dadd_rn(hd2, (double)__fmul_rn(df, df));
         }
-        T[(int64_t)u * (2 * (int64_t)g - u - 1) / 2 + (v - u - 1)] = hd2 < kPairEps ? -1.0f : (float)(0.5 / hd2);
+        const float t = hd2 < kPairEps ? -1.0f : (float)(0.5 / hd2);
+        T[(int64_t)u * (2 * (int64_t)g - u - 1) / 2 + (v - u - 1)] = t;
+        tm = fmaxf(tm, t);
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+    if ((threadIdx.x & 31) == 0 && tm > 0.0f) atomicMax(reinterpret_cast<int*>(tmax), __float_as_int(tm));
 }
 
 // Landmark centroid c (f64 mean, rounded to f32; dims >= d are 0): the
@@ -1274,7 +1283,9 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     pack_landmarks_kernel<<<grid_for((int64_t)p.ntiles * p.dp * kTile, 256), 256, 0, stream>>>(hi, g, d, p.dp, p.ntiles,
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
-    pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T);
+    float* tmax = reinterpret_cast<float*>(ws + m.lstats) + 2;
+    cudaMemsetAsync(tmax, 0, 4, stream);
+    pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T, tmax);
     if (int e = cuda_check("pair_table")) return e;
     if (tc_eligible(1 << 20, d, g, k))
         if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
@@ -1342,6 +1353,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         q.g = g;
         q.lo = lo;
         q.T = T;
+        q.tmax = reinterpret_cast<const float*>(mws + ml.lstats) + 2;
         q.xy = xy + 2 * s;
         q.X = X + s * d;
         q.hi = hi;

@@ -98,6 +98,64 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return r;
 }
 
+// Squared distances that the law of cosines can trust far from the landmarks.
+// dnum/hd2 = 1/2 + (s_u - s_v) T_uv needs s_u - s_v to ~1e-7 hd2, but the
+// reference's f32 sums carry ~sqrt(d) eps32 s of rounding: once s T (kappa)
+// is large -- points far from a trained SOM's tightly packed landmarks --
+// that error dominates.  Recomputing the k distances in f64 (O(kd), rows from
+// L1) and keeping them as f32 OFFSETS e_j = fl(s_j - s_0) from the nearest
+// makes e_u - e_v = s_u - s_v up to eps32 (|s_u - s_0| + |s_v - s_0|): the
+// rounding now scales with the spread of the neighbour distances, not with
+// their size, and the f32 pair loop stays valid far out (kKappaMax64 bounds
+// (s_{k-1} - s_0) T_max before the exact x-based f64 loop takes over).
+constexpr double kKappaMax64 = 1e5;
+
+template <int KP>
+__device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, const float* __restrict__ hi,
+                                            const int (&jj)[KP], int k, float (&qe)[KP]) {
+    constexpr int QC = KP < 8 ? KP : 8;  // neighbours per pass (bounds the live f64 accumulators)
+    double s0 = 0.0;
+#pragma unroll
+    for (int q0 = 0; q0 < KP; q0 += QC) {
+        double acc[QC];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) acc[q] = 0.0;
+        if ((d & 3) == 0) {
+            for (int c = 0; c < d; c += 4) {
+                const float4 xv = __ldg(reinterpret_cast<const float4*>(x + c));
+#pragma unroll
+                for (int q = 0; q < QC; ++q) {
+                    if (q0 + q < k) {
+                        const float4 hv = __ldg(reinterpret_cast<const float4*>(hi + (int64_t)jj[q0 + q] * d + c));
+                        double t = (double)xv.x - (double)hv.x;
+                        acc[q] = fma(t, t, acc[q]);
+                        t = (double)xv.y - (double)hv.y;
+                        acc[q] = fma(t, t, acc[q]);
+                        t = (double)xv.z - (double)hv.z;
+                        acc[q] = fma(t, t, acc[q]);
+                        t = (double)xv.w - (double)hv.w;
+                        acc[q] = fma(t, t, acc[q]);
+                    }
+                }
+            }
+        } else {
+            for (int c = 0; c < d; ++c) {
+                const double xc = (double)__ldg(x + c);
+#pragma unroll
+                for (int q = 0; q < QC; ++q) {
+                    if (q0 + q < k) {
+                        const double t = xc - (double)__ldg(hi + (int64_t)jj[q0 + q] * d + c);
+                        acc[q] = fma(t, t, acc[q]);
+                    }
+                }
+            }
+        }
+        if (q0 == 0) s0 = acc[0];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) qe[q0 + q] = q0 + q < k ? (float)(acc[q] - s0) : 0.0f;
+    }
+}
+
 // f64 law-of-cosines accumulation over all pairs (fallback for ill-conditioned
 // f32 systems), same pair rules as the register kernels.
 static __device__ __noinline__ void pairs_cos_f64(int k, const int* J, const float* SQ, const float* SC, int st,
@@ -116,7 +174,8 @@ static __device__ __noinline__ void pairs_cos_f64(int k, const int* J, const flo
             const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
             if (!(tv >= 0.0f) || !(ld2 >= kLd2Min)) continue;
             const double G1 = (double)ex / (double)ld2, G2 = (double)ey / (double)ld2;
-            const double h = 0.5 + (double)(SQ[u * st] - SQ[v * st]) * (double)tv + G1 * (double)lu.x + G2 * (double)lu.y;
+            const double h = 0.5 + ((double)SQ[u * st] - (double)SQ[v * st]) * (double)tv + G1 * (double)lu.x +
+                             G2 * (double)lu.y;
             const double W = w;
             a11 = fma(W * G1, G1, a11);
             a12 = fma(W * G1, G2, a12);
@@ -165,7 +224,7 @@ __device__ __forceinline__ void ref_scores_f64(int k, const float (&sq)[KP], flo
 }
 
 // strided form (rows in shared memory, one column per thread)
-static __device__ __noinline__ void ref_scores_f64_strided(int k, const float* sq, int st, float* out) {
+static __device__ __noinline__ void ref_scores_f64_strided(int k, const float* sq, int st, float* out, int ost) {
     double sigma = 0.0, dk = 0.0;
     for (int q = 0; q < k; ++q) {
         const double dq = (double)__fsqrt_rn(sq[q * st]);
@@ -180,12 +239,12 @@ static __device__ __noinline__ void ref_scores_f64_strided(int k, const float* s
         for (int q = 0; q < k; ++q) {
             const double dq = (double)__fsqrt_rn(sq[q * st]);
             const double v = exp(dq * dq * inv) - tail;
-            out[q * st] = v > 0.0 ? (float)v : 0.0f;
+            out[q * ost] = v > 0.0 ? (float)v : 0.0f;
             if (q == 0) uniform = v < kScoreEps;
         }
     }
     if (uniform)
-        for (int q = 0; q < k; ++q) out[q * st] = q < k - 1 ? 1.0f : 0.0f;
+        for (int q = 0; q < k; ++q) out[q * ost] = q < k - 1 ? 1.0f : 0.0f;
 }
 
 template <int KP>
@@ -194,12 +253,13 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
-    // layout: lo [g] float2 | RB [g] int | J [KP][PT] int | S [KP][PT] f32 | Q [KP][PT] f32 | (T table)
+    // layout: lo [g] float2 | RB [g] int | J [KP][PT] int | S [KP][PT] f32 | Q, QB [KP][PT] f32 | (T table)
     float2* LO = reinterpret_cast<float2*>(smem_raw);
     int* RB = reinterpret_cast<int*>(LO + g);
     int* J = RB + g;
     float* S = reinterpret_cast<float*>(J + KP * PT);
     float* Q = S + KP * PT;
+    const float tmax_model = a.tmax ? __ldg(a.tmax) : 0.0f;
     const float* Ts = a.T;
     if (a.t_smem) {
         float* tsm = Q + KP * PT;
@@ -226,7 +286,7 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
             sig += sqrt_approx(sq);
             J[q * PT + tid] = __ldg(irow + q);
             Q[q * PT + tid] = sq;
-            sqk = sq;
+            sqk = sq;  // rows ascending: the last is the largest
         }
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
@@ -245,6 +305,23 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         if (uniform)
             for (int q = 0; q < k; ++q) S[q * PT + tid] = q == k - 1 ? 0.0f : 1.0f;
 
+        // far from the landmarks (kappa bound large): Q <- f64 squared distances as
+        // f32 offsets from the nearest (precise_sqd; the reference's sq are re-read for scores)
+        const bool prec = 2.0f * sqk * tmax_model > (float)kKappaMax;
+        if (prec) {
+            const float* x = a.X + i * a.d;
+            double s0 = 0.0;
+            for (int q = 0; q < k; ++q) {
+                const float* h = a.hi + (int64_t)J[q * PT + tid] * a.d;
+                double acc = 0.0;
+                for (int c = 0; c < a.d; ++c) {
+                    const double t = (double)__ldg(x + c) - (double)__ldg(h + c);
+                    acc = fma(t, t, acc);
+                }
+                if (q == 0) s0 = acc;
+                Q[q * PT + tid] = (float)(acc - s0);
+            }
+        }
         // pairs in f32 about o = lo[idx0] (see project_reg2_kernel), solved in f64
         const float2 o = LO[J[tid]];
         float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f;
@@ -270,7 +347,7 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
                 const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
                 const float w = su * sv;
                 const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
-                kappa = keep ? fmaxf(kappa, (squ + sqv) * tv) : kappa;
+                kappa = keep ? fmaxf(kappa, (prec ? fabsf(squ) + fabsf(sqv) : squ + sqv) * tv) : kappa;
                 const float rr = keep ? rcp_approx(ld2) : 0.0f;
                 const float g1 = ex * rr, g2 = ey * rr, wr = w * rr;
                 const float h = fmaf(squ - sqv, tv, 0.5f) + fmaf(g1, lux, g2 * luy);
@@ -284,10 +361,11 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         }
         double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
-        if (kappa > (float)kKappaMax || illc) {
+        const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
+        if (far || illc) {
             double o5[5];
-            ref_scores_f64_strided(k, Q + tid, PT, S + tid);  // the reference's f64 scores
-            if (kappa > (float)kKappaMax)
+            ref_scores_f64_strided(k, drow, 1, S + tid, PT);  // the reference's f64 scores from its own sq
+            if (far)
                 pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, J + tid, S + tid, PT, o5);
             else
                 pairs_cos_f64(k, J + tid, Q + tid, S + tid, PT, LO, Ts, g, o5);
@@ -505,6 +583,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
     __syncthreads();
     const float* T = TSMEM ? tsm : a.T;
     const bool vec = (k == KP) && ((KP & 3) == 0);
+    const float tmax_model = a.tmax ? __ldg(a.tmax) : 0.0f;
 
     for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
         const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
@@ -565,14 +644,23 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
             for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
         }
 
+        // far from the landmarks: f64 squared distances as double-float pairs (precise_sqd)
+        float qe[KP];
+        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;
+        if (prec) {
+            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi, jj, k, qe);
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) qe[q] = sq[q];
+        }
         float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
         int pj[KP], prb[KP];
-        float psq[KP], psc[KP], plx[KP], ply[KP];
+        float pqe[KP], psc[KP], plx[KP], ply[KP];
 #pragma unroll
         for (int q = 0; q < KP; ++q) {
             pj[q] = jj[q];
             prb[q] = rb[q];
-            psq[q] = sq[q];
+            pqe[q] = qe[q];
             psc[q] = sc[q];
             plx[q] = lx[q];
             ply[q] = ly[q];
@@ -581,19 +669,19 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         for (int r = 1; r <= KP / 2; ++r) {
             {
                 const int j0 = pj[0], b0 = prb[0];
-                const float s0 = psq[0], c0 = psc[0], x0 = plx[0], y0 = ply[0];
+                const float s0 = pqe[0], c0 = psc[0], x0 = plx[0], y0 = ply[0];
 #pragma unroll
                 for (int q = 0; q < KP - 1; ++q) {
                     pj[q] = pj[q + 1];
                     prb[q] = prb[q + 1];
-                    psq[q] = psq[q + 1];
+                    pqe[q] = pqe[q + 1];
                     psc[q] = psc[q + 1];
                     plx[q] = plx[q + 1];
                     ply[q] = ply[q + 1];
                 }
                 pj[KP - 1] = j0;
                 prb[KP - 1] = b0;
-                psq[KP - 1] = s0;
+                pqe[KP - 1] = s0;
                 psc[KP - 1] = c0;
                 plx[KP - 1] = x0;
                 ply[KP - 1] = y0;
@@ -612,7 +700,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
                 const float wr = w * rr;
                 const float g1 = ex * rr, g2 = ey * rr;
                 // dnum/hd2 by the law of cosines + g . (lo_u - o)
-                const float h = fmaf(sq[u] - psq[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
+                const float h = fmaf(qe[u] - pqe[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
                 const float wg1 = wr * ex, wg2 = wr * ey;  // w g
                 a11 = fmaf(wg1, g1, a11);
                 a12 = fmaf(wg1, g2, a12);
@@ -622,20 +710,29 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
             }
         }
         double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
-        const float kappa = 2.0f * sqmax * tmax;
+        float spread = sqmax;  // prec: the error of qe_u - qe_v scales with the offsets' spread
+        if (prec) {
+            spread = 0.0f;
+#pragma unroll
+            for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
+        }
+        const float kappa = 2.0f * spread * tmax;
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
-        if (kappa > (float)kKappaMax || illc) {
+        const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
+        if (far || illc) {
             double o5[5];
-            float fsc[KP];
-            ref_scores_f64<KP>(k, sq, fsc);
-            if (kappa > (float)kKappaMax) {
+            float fsc[KP], rsq[KP];  // the reference's sq, re-read (keeps sq dead across the pair loop)
+#pragma unroll
+            for (int q = 0; q < KP; ++q) rsq[q] = q < k ? __ldg(a.sqd + i * k + q) : 0.0f;
+            ref_scores_f64<KP>(k, rsq, fsc);
+            if (far) {
                 // far outlier: exact x-based f64 pair loop (absolute layout coordinates)
                 pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, fsc, 1, o5);
                 // shift to the local origin: c -= A o
                 o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
                 o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
             } else {
-                pairs_cos_f64(k, jj, sq, fsc, 1, LO, T, g, o5);
+                pairs_cos_f64(k, jj, qe, fsc, 1, LO, T, g, o5);
                 o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
                 o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
             }
@@ -702,7 +799,7 @@ static __device__ __noinline__ void pairs_rec_f64(int k, const int* J, const flo
             const float ex = __fsub_rn(lo[2 * J[v]], lo[2 * J[u]]), ey = __fsub_rn(lo[2 * J[v] + 1], lo[2 * J[u] + 1]);
             const double ld2 = (double)__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
             const double G1 = (double)ex / ld2, G2 = (double)ey / ld2;
-            const double h = 0.5 + (double)(SQ[u] - SQ[v]) * (double)r.x + G1 * (double)lo[2 * J[u]] +
+            const double h = 0.5 + ((double)SQ[u] - (double)SQ[v]) * (double)r.x + G1 * (double)lo[2 * J[u]] +
                              G2 * (double)lo[2 * J[u] + 1];
             const double W = w;
             a11 = fma(W * G1, G1, a11);
@@ -726,6 +823,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
     const int g = a.g, k = a.k;
     const bool vec = (k == KP) && ((KP & 3) == 0);
     const float4* __restrict__ rec = a.rec;
+    const float tmax_model = a.tmax ? __ldg(a.tmax) : 0.0f;
 
     for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
         const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
@@ -776,27 +874,35 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
             for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
         }
 
+        float qe[KP];
+        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;
+        if (prec) {
+            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi, jj, k, qe);
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) qe[q] = sq[q];
+        }
         float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
         int pj[KP];
-        float psq[KP], psc[KP];
+        float pqe[KP], psc[KP];
 #pragma unroll
         for (int q = 0; q < KP; ++q) {
             pj[q] = jj[q];
-            psq[q] = sq[q];
+            pqe[q] = qe[q];
             psc[q] = sc[q];
         }
         for (int r = 1; r <= KP / 2; ++r) {  // ring schedule: round r pairs slot u with u + r mod KP
             {
                 const int j0 = pj[0];
-                const float s0 = psq[0], c0 = psc[0];
+                const float s0 = pqe[0], c0 = psc[0];
 #pragma unroll
                 for (int q = 0; q < KP - 1; ++q) {
                     pj[q] = pj[q + 1];
-                    psq[q] = psq[q + 1];
+                    pqe[q] = pqe[q + 1];
                     psc[q] = psc[q + 1];
                 }
                 pj[KP - 1] = j0;
-                psq[KP - 1] = s0;
+                pqe[KP - 1] = s0;
                 psc[KP - 1] = c0;
             }
             const bool half = r == KP / 2;
@@ -807,7 +913,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
                 const bool keep = (w > 0.0f) & (rc.x >= 0.0f);
                 tmax = keep ? fmaxf(tmax, rc.x) : tmax;
                 const float wk = keep ? w : 0.0f;
-                const float h = fmaf(sq[u] - psq[u], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
+                const float h = fmaf(qe[u] - pqe[u], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
                 const float wg1 = wk * rc.y, wg2 = wk * rc.z;
                 a11 = fmaf(wg1, rc.y, a11);
                 a12 = fmaf(wg1, rc.z, a12);
@@ -817,16 +923,25 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
             }
         }
         double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
-        const float kappa = 2.0f * sqmax * tmax;
+        float spread = sqmax;  // prec: the error of qe_u - qe_v scales with the offsets' spread
+        if (prec) {
+            spread = 0.0f;
+#pragma unroll
+            for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
+        }
+        const float kappa = 2.0f * spread * tmax;
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
-        if (kappa > (float)kKappaMax || illc) {
+        const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
+        if (far || illc) {
             double o5[5];
-            float fsc[KP];
-            ref_scores_f64<KP>(k, sq, fsc);
-            if (kappa > (float)kKappaMax)
+            float fsc[KP], rsq[KP];  // the reference's sq, re-read (keeps sq dead across the pair loop)
+#pragma unroll
+            for (int q = 0; q < KP; ++q) rsq[q] = q < k ? __ldg(a.sqd + i * k + q) : 0.0f;
+            ref_scores_f64<KP>(k, rsq, fsc);
+            if (far)
                 pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, fsc, 1, o5);
             else
-                pairs_rec_f64(k, jj, sq, fsc, rec, a.lo, g, o5);
+                pairs_rec_f64(k, jj, qe, fsc, rec, a.lo, g, o5);
             A11 = o5[0];
             A12 = o5[1];
             A22 = o5[2];

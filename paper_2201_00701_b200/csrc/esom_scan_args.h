@@ -37,6 +37,7 @@ struct ProjArgs {
     int d;
     const int32_t* perm;     // optional visiting order (nullable)
     const float4* rec;       // g x g pair records {T, g1, g2, g.lo_u} (project_reg3_kernel; nullable)
+    const float* tmax;       // device scalar: max kept T of the model (f64-distance decision)
 };
 
 // tensor-core screened k-NN (esom_tc.cuh)

@@ -219,3 +219,25 @@ def test_host_pipeline_equals_device():
     a = esom.embed(host, model, esom.EmbedParams(k=16))
     b = esom.embed(torch.from_numpy(pts[:600_000]).cuda(), model, esom.EmbedParams(k=16)).cpu().numpy()
     assert isinstance(a, np.ndarray) and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("grid,k", [((16, 16), 16), ((32, 32), 16), ((16, 16), 32), ((16, 16), 8)])
+def test_embed_on_trained_som_vs_oracle(grid, k):
+    """A trained SOM packs the landmarks tightly in hi-space while points stay
+    far from them (kappa = 2 max sqd max T in the hundreds to thousands): the
+    projection must keep the tolerance there without the exact f64 pair loop
+    (f64 neighbour distances as offsets, esom_project.cuh precise_sqd)."""
+    pts = datagen.gaussians(16, 1 << 15, 32, seed=1)[0].astype(np.float32)
+    eng = esom.FrameEngine(pts, seed=7, k=16, grid=grid)
+    for _ in range(12):
+        eng.tick()
+    hi, lo = eng.model.hi, eng.model.lo
+    model = esom.LandmarkModel.create(hi, lo)
+    xy = esom.embed(pts, model, esom.EmbedParams(k=k))
+    ref = oracle.embed(pts, hi, lo, k, threads=oracle.host_cores())
+    assert_xy_close(xy, ref, lo, f"trained {grid} k={k}")
+    # the far-point regime is really exercised
+    h = hi.astype(np.float64)
+    hd2 = ((h[:, None, :] - h[None, :, :]) ** 2).sum(-1)[np.triu_indices(len(h), 1)]
+    _, sqd = oracle.knn(pts[:2000], hi, k)
+    assert np.median(2 * sqd.max(1) * 0.5 / hd2.min()) > 256
