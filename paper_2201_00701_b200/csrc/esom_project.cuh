@@ -290,12 +290,17 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         }
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
+        // far from the landmarks (kappa bound large): f64 paths below
+        const bool prec = 2.0f * sqk * tmax_model > (float)kKappaMax;
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);
+            const double dk = (double)__fsqrt_rn(sqk);
             for (int q = 0; q < k; ++q) {
                 const float sq = Q[q * PT + tid];
-                const float dl = (sqk - sq) * inv;
+                // far points: the exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
+                const double dq = (double)__fsqrt_rn(sq);
+                const float dl = prec ? (float)((dk * dk - dq * dq) * (double)inv) : (sqk - sq) * inv;
                 const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
                                                                        1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
                 S[q * PT + tid] = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
@@ -305,9 +310,8 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         if (uniform)
             for (int q = 0; q < k; ++q) S[q * PT + tid] = q == k - 1 ? 0.0f : 1.0f;
 
-        // far from the landmarks (kappa bound large): Q <- f64 squared distances as
-        // f32 offsets from the nearest (precise_sqd; the reference's sq are re-read for scores)
-        const bool prec = 2.0f * sqk * tmax_model > (float)kKappaMax;
+        // far points: Q <- f64 squared distances as f32 offsets from the nearest
+        // (precise_sqd; the reference's sq are re-read for the f64 score fallback)
         if (prec) {
             const float* x = a.X + i * a.d;
             double s0 = 0.0;
@@ -625,12 +629,25 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         // precision where the reference's e_q - tail cancels (far outliers).
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
+        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);
+            float dls[KP];
+            if (prec) {  // far points: exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
+                const double dk = (double)__fsqrt_rn(sqk);
+#pragma unroll
+                for (int q = 0; q < KP; ++q) {
+                    const double dq = (double)__fsqrt_rn(sq[q]);
+                    dls[q] = q < k ? (float)((dk * dk - dq * dq) * (double)inv) : 0.0f;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < KP; ++q) dls[q] = q < k ? (sqk - sq[q]) * inv : 0.0f;
+            }
 #pragma unroll
             for (int q = 0; q < KP; ++q) {
-                const float dl = q < k ? (sqk - sq[q]) * inv : 0.0f;  // >= 0 (rows ascending); 0 at q = k-1
+                const float dl = dls[q];  // >= 0 (rows ascending); 0 at q = k-1
                 const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
                                                                        1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
                 const float e = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
@@ -646,7 +663,6 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
 
         // far from the landmarks: f64 squared distances as double-float pairs (precise_sqd)
         float qe[KP];
-        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;
         if (prec) {
             precise_sqd<KP>(a.X + i * a.d, a.d, a.hi, jj, k, qe);
         } else {
@@ -857,12 +873,25 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
         // scores as in v2 (scale-free f32 expm1 form)
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
+        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);
+            float dls[KP];
+            if (prec) {  // far points: exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
+                const double dk = (double)__fsqrt_rn(sqk);
+#pragma unroll
+                for (int q = 0; q < KP; ++q) {
+                    const double dq = (double)__fsqrt_rn(sq[q]);
+                    dls[q] = q < k ? (float)((dk * dk - dq * dq) * (double)inv) : 0.0f;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < KP; ++q) dls[q] = q < k ? (sqk - sq[q]) * inv : 0.0f;
+            }
 #pragma unroll
             for (int q = 0; q < KP; ++q) {
-                const float dl = q < k ? (sqk - sq[q]) * inv : 0.0f;
+                const float dl = dls[q];
                 const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
                                                                        1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
                 sc[q] = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
@@ -875,7 +904,6 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
         }
 
         float qe[KP];
-        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;
         if (prec) {
             precise_sqd<KP>(a.X + i * a.d, a.d, a.hi, jj, k, qe);
         } else {

@@ -236,7 +236,9 @@ def test_embed_on_trained_som_vs_oracle(grid, k):
     xy = esom.embed(pts, model, esom.EmbedParams(k=k))
     ref = oracle.embed(pts, hi, lo, k, threads=oracle.host_cores())
     assert_xy_close(xy, ref, lo, f"trained {grid} k={k}")
-    # the far-point regime is really exercised
+    if grid != (16, 16) or k != 16:
+        return
+    # the far-point regime is really exercised (C3 shape)
     h = hi.astype(np.float64)
     hd2 = ((h[:, None, :] - h[None, :, :]) ** 2).sum(-1)[np.triu_indices(len(h), 1)]
     _, sqd = oracle.knn(pts[:2000], hi, k)
