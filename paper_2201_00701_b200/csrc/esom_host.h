@@ -10,4 +10,7 @@ int cuda_check(const char* where, int launches = 1);  // also counts our kernel 
 int num_sms();
 int max_smem_optin();
 size_t resident_limit();
+// esom_train.cu: on-chip (cluster) online tick; -1 = shape needs the global-memory kernel
+int launch_online_tick_cluster(bool som, const float* X, int d, const int64_t* sample, int B, float* hi,
+                               const float* lo, int g, double sigma, double alpha, cudaStream_t st);
 }  // namespace esom_host

@@ -1434,6 +1434,11 @@ static int online_tick(bool som, const float* X, int32_t d, const int64_t* sampl
                        cudaStream_t stream) {
     if (B < 0 || g < 1 || d < 1) return set_err(ESOM_ERR_PARAM, "bad tick shape%s", "");
     if (ws_bytes < esom_tick_workspace_bytes(g, d)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
+    if (B == 0) return ESOM_OK;
+    {
+        const int r = launch_online_tick_cluster(som, X, d, sample_idx, B, hi_inout, lo, g, sigma, alpha, stream);
+        if (r >= 0) return r;
+    }
     const size_t smem = ((size_t)d + g) * 8;
     if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g + d too large%s", "");
     auto kern = som ? online_tick_kernel<true> : online_tick_kernel<false>;
