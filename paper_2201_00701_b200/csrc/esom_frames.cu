@@ -198,6 +198,72 @@ __global__ void __launch_bounds__(kStatThreads) dim_partial_kernel(const float* 
     }
 }
 
+
+// Vectorised form for d in {4, 8, 16, 32, 64, 128}: a thread owns 4 adjacent
+// columns (one 16-byte load per row), tpr = d/4 threads cover a row, so a warp
+// streams 32/tpr whole rows per load (512 contiguous bytes) and every thread
+// carries 4 independent f64 chains.  Same fixed combination order
+// (row slot, then block) -> deterministic.
+template <bool DEV>
+__global__ void __launch_bounds__(kStatThreads) dim_partial4_kernel(const float* __restrict__ X, int64_t n, int d,
+                                                                    int64_t rows_per_block,
+                                                                    const double* __restrict__ mean,
+                                                                    double* __restrict__ part) {
+    extern __shared__ double sp[];  // 3 x RB x d
+    const int tpr = d >> 2, RB = kStatThreads / tpr;
+    const int t = threadIdx.x, g4 = t % tpr, rs = t / tpr;
+    const int c = 4 * g4;
+    const int64_t r0 = blockIdx.x * rows_per_block;
+    const int64_t r1 = min(n, r0 + rows_per_block);
+    double s[4] = {0.0, 0.0, 0.0, 0.0}, mn[4], mx[4], mu[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        mn[q] = INFINITY;
+        mx[q] = -INFINITY;
+        mu[q] = DEV ? mean[c + q] : 0.0;
+    }
+#pragma unroll 4
+    for (int64_t r = r0 + rs; r < r1; r += RB) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(X + r * d + c));
+        const double x[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (DEV) {
+                const double u = __dsub_rn(x[q], mu[q]);
+                s[q] = __dadd_rn(s[q], __dmul_rn(u, u));
+            } else {
+                s[q] = __dadd_rn(s[q], x[q]);
+                mn[q] = fmin(mn[q], x[q]);
+                mx[q] = fmax(mx[q], x[q]);
+            }
+        }
+    }
+    double* S = sp;
+    double* A = sp + RB * d;
+    double* Z = sp + 2 * RB * d;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        S[rs * d + c + q] = s[q];
+        A[rs * d + c + q] = mn[q];
+        Z[rs * d + c + q] = mx[q];
+    }
+    __syncthreads();
+    for (int cc = t; cc < d; cc += kStatThreads) {
+        double ts = S[cc], ta = A[cc], tz = Z[cc];
+        for (int q = 1; q < RB; ++q) {
+            ts = __dadd_rn(ts, S[q * d + cc]);
+            ta = fmin(ta, A[q * d + cc]);
+            tz = fmax(tz, Z[q * d + cc]);
+        }
+        double* p = part + (int64_t)blockIdx.x * 3 * d;
+        p[cc] = ts;
+        p[d + cc] = ta;
+        p[2 * d + cc] = tz;
+    }
+}
+
+bool stats_vec4(int d) { return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128; }
+
 // one thread per column: combine the block partials in block order.
 template <bool DEV>
 __global__ void dim_final_kernel(const double* __restrict__ part, int nblocks, int64_t n, int d, double* mn,
@@ -239,6 +305,23 @@ struct ColXf {
     int32_t kind;
     double p, q;  // minmax: (min, span); zscore: (mean, sd); affine: (a, b)
 };
+
+__device__ __forceinline__ float xform1(const ColXf& t, float xf) {
+    const double x = (double)xf;
+    double y;
+    if (t.kind == 0) y = x;
+    else if (t.kind == 1) y = t.q <= 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(x, t.p), t.q);
+    else if (t.kind == 2) y = t.q <= 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(x, t.p), t.q);
+    else y = __dadd_rn(__dmul_rn(t.p, x), t.q);
+    return __double2float_rn(y);
+}
+
+// d % 4 == 0: one float4 (4 adjacent columns of one row) per thread-step
+__global__ void transform4_kernel(const float4* __restrict__ X, int64_t n4, int d, const int32_t* __restrict__ kind,
+                                  const double* __restrict__ pa, const double* __restrict__ pb,
+                                  const double* __restrict__ mn, const double* __restrict__ mx,
+                                  const double* __restrict__ mean, const double* __restrict__ sd,
+                                  float4* __restrict__ out, int32_t* flag);
 
 __global__ void transform_kernel(const float* __restrict__ X, int64_t n, int d, const int32_t* __restrict__ kind,
                                  const double* __restrict__ pa, const double* __restrict__ pb,
@@ -405,6 +488,48 @@ __global__ void fit_hi_kernel(const float* __restrict__ hi, const float* __restr
     }
 }
 
+
+__global__ void transform4_kernel(const float4* __restrict__ X, int64_t n4, int d, const int32_t* __restrict__ kind,
+                                  const double* __restrict__ pa, const double* __restrict__ pb,
+                                  const double* __restrict__ mn, const double* __restrict__ mx,
+                                  const double* __restrict__ mean, const double* __restrict__ sd,
+                                  float4* __restrict__ out, int32_t* flag) {
+    extern __shared__ ColXf cx4[];
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        ColXf t;
+        t.kind = kind[c];
+        if (t.kind == 1) {
+            t.p = mn[c];
+            t.q = __dsub_rn(mx[c], mn[c]);
+        } else if (t.kind == 2) {
+            t.p = mean[c];
+            t.q = sd[c];
+        } else {
+            t.p = pa ? pa[c] : 1.0;
+            t.q = pb ? pb[c] : 0.0;
+        }
+        cx4[c] = t;
+    }
+    __syncthreads();
+    bool bad = false;
+    const int d4 = d >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int cstep = (int)(stride % d4);
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int c4 = (int)(e % d4);
+    for (; e < n4; e += stride, c4 = (c4 + cstep >= d4) ? c4 + cstep - d4 : c4 + cstep) {
+        const float4 v = __ldg(X + e);
+        const int c = 4 * c4;
+        float4 o;
+        o.x = xform1(cx4[c], v.x);
+        o.y = xform1(cx4[c + 1], v.y);
+        o.z = xform1(cx4[c + 2], v.z);
+        o.w = xform1(cx4[c + 3], v.w);
+        bad |= !finite_f(o.x) | !finite_f(o.y) | !finite_f(o.z) | !finite_f(o.w);
+        out[e] = o;
+    }
+    flag_nonfinite(flag, bad);
+}
 }  // namespace
 
 extern "C" {
@@ -461,9 +586,13 @@ int esom_dim_stats(const float* X, int64_t n, int32_t d, double* mn, double* mx,
     const int64_t rows = (n + nb - 1) / nb;
     double* part = reinterpret_cast<double*>(workspace);
     const int fb = (d + 127) / 128;
-    dim_partial_kernel<false><<<nb, kStatThreads, 0, stream>>>(X, n, d, rows, nullptr, part);
+    const bool v4 = stats_vec4(d) && (((uintptr_t)X) & 15) == 0;
+    const size_t sm4 = v4 ? (size_t)3 * (kStatThreads / (d / 4)) * d * 8 : 0;
+    if (v4) dim_partial4_kernel<false><<<nb, kStatThreads, sm4, stream>>>(X, n, d, rows, nullptr, part);
+    else dim_partial_kernel<false><<<nb, kStatThreads, 0, stream>>>(X, n, d, rows, nullptr, part);
     dim_final_kernel<false><<<fb, 128, 0, stream>>>(part, nb, n, d, mn, mx, mean, sd);
-    dim_partial_kernel<true><<<nb, kStatThreads, 0, stream>>>(X, n, d, rows, mean, part);
+    if (v4) dim_partial4_kernel<true><<<nb, kStatThreads, sm4, stream>>>(X, n, d, rows, mean, part);
+    else dim_partial_kernel<true><<<nb, kStatThreads, 0, stream>>>(X, n, d, rows, mean, part);
     dim_final_kernel<true><<<fb, 128, 0, stream>>>(part, nb, n, d, mn, mx, mean, sd);
     return cuda_check("dim_stats", 4);
 }
@@ -475,6 +604,13 @@ int esom_apply_transform(const float* X, int64_t n, int32_t d, const int32_t* ki
     if (n == 0) return ESOM_OK;
     const size_t smem = (size_t)d * sizeof(ColXf);
     if (smem > 48 * 1024) return set_err(ESOM_ERR_UNSUPPORTED, "d=%lld too large for the transform kernel%s", "", d);
+    if ((d & 3) == 0 && !(((uintptr_t)X) & 15) && !(((uintptr_t)out) & 15)) {
+        const int64_t n4 = n * d / 4;
+        transform4_kernel<<<stream_grid(n4, 256), 256, smem, stream>>>(reinterpret_cast<const float4*>(X), n4, d, kind,
+                                                                       a, b, mn, mx, mean, sd,
+                                                                       reinterpret_cast<float4*>(out), nonfinite_flag);
+        return cuda_check("transform4_kernel");
+    }
     transform_kernel<<<stream_grid(n * d, 256), 256, smem, stream>>>(X, n, d, kind, a, b, mn, mx, mean, sd, out,
                                                                      nonfinite_flag);
     return cuda_check("transform_kernel");
