@@ -331,9 +331,174 @@ __global__ void __launch_bounds__(kTickThreads) online_tick_reg_kernel(const flo
     if (cs > 1) cluster_sync_all();
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-per-thread variant (d <= 64): thread t of cluster CTA r owns landmark
+// j = r*T + t with its whole f64 row in registers.  The distance is a
+// per-thread f64 FMA sum (4 interleaved partial chains, no shuffles); only
+// the argmin crosses lanes (5 shuffle levels per warp + W-entry CTA reduce +
+// the cluster exchange); h_j is one exp per thread; the update touches only
+// the thread's own registers.  The f64 work per sample (5 g d ops) is spread
+// over CS SMs with T = 32 W threads each.
+// ---------------------------------------------------------------------------
+template <bool SOM, int DP, int W>
+__global__ void __launch_bounds__(32 * W) online_tick_row_kernel(const float* __restrict__ X, int d,
+                                                                 const int64_t* __restrict__ sample, int B,
+                                                                 float* __restrict__ hi_f32, const float* __restrict__ lo,
+                                                                 int g, double sigma, double alpha) {
+    constexpr int T = 32 * W;
+    constexpr int SB = 128;  // staged samples per chunk
+    __shared__ __align__(16) double xs[SB * DP];
+    __shared__ double red_v[2][W];
+    __shared__ int red_j[2][W];
+    __shared__ double cand_v[2];
+    __shared__ int cand_j[2];
+    extern __shared__ double2 LOs[];  // g layout positions (f64), SOM only
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t rank = cluster_rank(), cs = cluster_size();
+    const int j = (int)rank * T + tid;
+    const bool own = j < g;
+    double h[DP];
+#pragma unroll
+    for (int c = 0; c < DP; ++c) h[c] = (own && c < d) ? (double)hi_f32[(int64_t)j * d + c] : 0.0;
+    double2 lj = make_double2(0.0, 0.0);
+    if (SOM) {
+        for (int q = tid; q < g; q += T) LOs[q] = make_double2((double)lo[2 * q], (double)lo[2 * q + 1]);
+        if (own) lj = make_double2((double)lo[2 * j], (double)lo[2 * j + 1]);
+    }
+    const double denom = 2.0 * sigma * sigma;
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+
+    for (int s0 = 0; s0 < B; s0 += SB) {
+        const int nb = min(SB, B - s0);
+        __syncthreads();
+        for (int e = tid; e < nb * DP; e += T) {
+            const int r = e / DP, c = e % DP;
+            xs[e] = c < d ? (double)__ldg(X + sample[s0 + r] * d + c) : 0.0;
+        }
+        __syncthreads();
+        for (int s = 0; s < nb; ++s) {
+            const int par = s & 1;
+            const double2* x2 = reinterpret_cast<const double2*>(xs + s * DP);
+            double p[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int c2 = 0; c2 < DP / 2; ++c2) {
+                const double2 xv = x2[c2];  // broadcast
+                const double t0 = h[2 * c2] - xv.x, t1 = h[2 * c2 + 1] - xv.y;
+                p[(2 * c2) & 3] = fma(t0, t0, p[(2 * c2) & 3]);
+                p[(2 * c2 + 1) & 3] = fma(t1, t1, p[(2 * c2 + 1) & 3]);
+            }
+            double bv = own ? (p[0] + p[1]) + (p[2] + p[3]) : inf;
+            int bj = own ? j : 0x7fffffff;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                if (lex_less(ov, oj, bv, bj)) bv = ov, bj = oj;
+            }
+            if (lane == 0) red_v[par][warp] = bv, red_j[par][warp] = bj;
+            __syncthreads();
+            bv = red_v[par][0];
+            bj = red_j[par][0];
+#pragma unroll
+            for (int w = 1; w < W; ++w)
+                if (lex_less(red_v[par][w], red_j[par][w], bv, bj)) bv = red_v[par][w], bj = red_j[par][w];
+            if (cs > 1) {
+                if (tid == 0) cand_v[par] = bv, cand_j[par] = bj;
+                cluster_sync_all();
+                bv = inf;
+                bj = 0x7fffffff;
+                if (lane < (int)cs) {
+                    bv = ld_peer_f64(map_peer(&cand_v[par], lane));
+                    bj = ld_peer_s32(map_peer(&cand_j[par], lane));
+                }
+#pragma unroll
+                for (int o = 4; o; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                    if (lex_less(ov, oj, bv, bj)) bv = ov, bj = oj;
+                }
+                bj = __shfl_sync(0xffffffffu, bj, 0);
+            }
+            const int b = bj;
+            const double* xr = xs + s * DP;
+            if (SOM) {
+                const double2 lb = LOs[b];
+                const double dx = lj.x - lb.x, dy = lj.y - lb.y;
+                const double l2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+                const double a = __dmul_rn(alpha, exp(__ddiv_rn(-l2, denom)));
+#pragma unroll
+                for (int c = 0; c < DP; ++c) h[c] = __dadd_rn(h[c], __dmul_rn(a, __dsub_rn(xr[c], h[c])));
+            } else if (j == b) {
+#pragma unroll
+                for (int c = 0; c < DP; ++c) h[c] = __dadd_rn(h[c], __dmul_rn(alpha, __dsub_rn(xr[c], h[c])));
+            }
+        }
+    }
+    if (own)
+#pragma unroll
+        for (int c = 0; c < DP; ++c)
+            if (c < d) hi_f32[(int64_t)j * d + c] = (float)h[c];
+    if (cs > 1) cluster_sync_all();
+}
+
 }  // namespace
 
 namespace esom_host {
+
+template <bool SOM, int DP, int W>
+int launch_row(int cs, const float* X, int d, const int64_t* sample, int B, float* hi, const float* lo, int g,
+               double sigma, double alpha, cudaStream_t st) {
+    auto kern = online_tick_row_kernel<SOM, DP, W>;
+    const size_t smem = SOM ? (size_t)g * 16 : 0;
+    if (smem > 160 * 1024) return -1;
+    if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, 1, 1);
+    cfg.blockDim = dim3(32 * W, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, d, sample, B, hi, lo, g, sigma, alpha);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(ESOM_ERR_CUDA, "online_tick_row_kernel launch: %s", cudaGetErrorString(e));
+    }
+    return cuda_check("online_tick_row_kernel");
+}
+
+// W warps per CTA (landmarks per CTA = 32 W), cs = ceil(g / 32 W) <= 8
+template <bool SOM, int DP>
+int launch_row_w(const float* X, int d, const int64_t* sample, int B, float* hi, const float* lo, int g, double sigma,
+                 double alpha, cudaStream_t st) {
+    static const int wpref = getenv("ESOM_TICK_W") ? atoi(getenv("ESOM_TICK_W")) : 0;
+    int w = wpref ? wpref : (g <= 128 ? 1 : (g <= 256 ? 2 : (g <= 512 ? 4 : 8)));
+    while (w < 8 && (g + 32 * w - 1) / (32 * w) > 8) w *= 2;
+    const int cs = (g + 32 * w - 1) / (32 * w);
+    if (cs > 8) return -1;
+    switch (w) {
+        case 1: return launch_row<SOM, DP, 1>(cs, X, d, sample, B, hi, lo, g, sigma, alpha, st);
+        case 2: return launch_row<SOM, DP, 2>(cs, X, d, sample, B, hi, lo, g, sigma, alpha, st);
+        case 4: return launch_row<SOM, DP, 4>(cs, X, d, sample, B, hi, lo, g, sigma, alpha, st);
+        case 8: return launch_row<SOM, DP, 8>(cs, X, d, sample, B, hi, lo, g, sigma, alpha, st);
+        default: return -1;
+    }
+}
+
+template <bool SOM>
+int launch_row_any(const float* X, int d, const int64_t* sample, int B, float* hi, const float* lo, int g,
+                   double sigma, double alpha, cudaStream_t st) {
+    if (d <= 8) return launch_row_w<SOM, 8>(X, d, sample, B, hi, lo, g, sigma, alpha, st);
+    if (d <= 16) return launch_row_w<SOM, 16>(X, d, sample, B, hi, lo, g, sigma, alpha, st);
+    if (d <= 32) return launch_row_w<SOM, 32>(X, d, sample, B, hi, lo, g, sigma, alpha, st);
+    return -1;
+}
 
 template <bool SOM, int M, int Q>
 int launch_reg(int cs, int gs, const float* X, int d, const int64_t* sample, int B, float* hi, const float* lo, int g,
@@ -394,6 +559,11 @@ int launch_reg_any(const float* X, int d, const int64_t* sample, int B, float* h
 int launch_online_tick_cluster(bool som, const float* X, int d, const int64_t* sample, int B, float* hi,
                                const float* lo, int g, double sigma, double alpha, cudaStream_t st) {
     if (getenv("ESOM_TICK_GLOBAL")) return -1;  // A/B switches (measurement only)
+    if (!getenv("ESOM_TICK_SMEM") && !getenv("ESOM_TICK_REG")) {
+        const int r = som ? launch_row_any<true>(X, d, sample, B, hi, lo, g, sigma, alpha, st)
+                          : launch_row_any<false>(X, d, sample, B, hi, lo, g, sigma, alpha, st);
+        if (r >= 0) return r;
+    }
     if (!getenv("ESOM_TICK_SMEM")) {
         const int r = som ? launch_reg_any<true>(X, d, sample, B, hi, lo, g, sigma, alpha, st)
                           : launch_reg_any<false>(X, d, sample, B, hi, lo, g, sigma, alpha, st);

@@ -122,3 +122,26 @@ def test_frame_loop_trains_and_embeds():
     xy_loop = loop.frame().clone()
     xy_ref = esom.embed(X, esom.LandmarkModel.create(hi_now.cpu().numpy(), lo), esom.EmbedParams(k=16))
     assert torch.equal(xy_loop, xy_ref)
+
+
+@pytest.mark.parametrize("g,d", [(4, 4), (64, 32), (256, 32), (1024, 32), (300, 48), (256, 64), (512, 100)])
+@pytest.mark.parametrize("variant", ["auto", "ESOM_TICK_REG", "ESOM_TICK_SMEM", "ESOM_TICK_GLOBAL"])
+def test_online_tick_kernels_vs_oracle(g, d, variant, monkeypatch):
+    """Every online-tick kernel (row-per-thread / register / shared-memory
+    cluster / global) against the C restatement of som_tick / kmeans_tick."""
+    if variant != "auto":
+        monkeypatch.setenv(variant, "1")
+    pts = datagen.gaussians(8, 20000, d, seed=3)[0].astype(np.float32)
+    gen = np.random.default_rng(g * 131 + d)
+    hi = pts[gen.choice(len(pts), g, replace=False)].copy()
+    lo = gen.uniform(0, 6, size=(g, 2)).astype(np.float32)
+    model = esom.LandmarkModel.create(hi, lo)
+    X = torch.from_numpy(pts).cuda()
+    cfg = esom.SomConfig(sigma=0.9, alpha=0.3, batch_size=200)
+    got = esom.som_tick(X, model, cfg, Rng(5)).cpu().numpy()
+    want = oracle.som_tick(pts, hi, lo, Rng(5).integers(0, len(pts), size=200), 0.9, 0.3)
+    assert close(got, want, f"som g={g} d={d} {variant}") > 0.5
+    kcfg = esom.KmeansConfig(alpha_km=0.2, batch_size=200)
+    got = esom.kmeans_tick(X, model, kcfg, Rng(6)).cpu().numpy()
+    want = oracle.kmeans_tick(pts, hi, Rng(6).integers(0, len(pts), size=200), 0.2)
+    assert close(got, want, f"kmeans g={g} d={d} {variant}") > 0.9
