@@ -478,7 +478,10 @@ template <bool SOM, int DP>
 int launch_row_w(const float* X, int d, const int64_t* sample, int B, float* hi, const float* lo, int g, double sigma,
                  double alpha, cudaStream_t st) {
     static const int wpref = getenv("ESOM_TICK_W") ? atoi(getenv("ESOM_TICK_W")) : 0;
-    int w = wpref ? wpref : (g <= 128 ? 1 : (g <= 256 ? 2 : (g <= 512 ? 4 : 8)));
+    // measured (B200, C3/C4 shapes, 256 samples): g <= 256 one 256-thread CTA
+    // (0.34 ms; a cluster barrier per sample costs more than it saves), larger g
+    // the narrowest CTAs that fit 8 per cluster (g = 1024: W = 4, 0.45 ms)
+    int w = wpref ? wpref : (g <= 256 ? 8 : 1);
     while (w < 8 && (g + 32 * w - 1) / (32 * w) > 8) w *= 2;
     const int cs = (g + 32 * w - 1) / (32 * w);
     if (cs > 8) return -1;
