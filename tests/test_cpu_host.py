@@ -118,6 +118,51 @@ def test_sharded_batch_som_gloo_world2(tmp_path, golden):
     np.testing.assert_allclose(sharded, full, rtol=1e-6, atol=1e-7)
 
 
+def _gloo_gather_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(ROOT))
+    from paper_2201_00701_b200.core import Rng
+    from paper_2201_00701_b200.sharded import gather_sample_rows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = np.load(ROOT / "tests" / "golden" / "golden.npz")
+    pts = g["small_points"].copy()
+    pts[3, 1] = -0.0  # signed zeros must survive the sum
+    bounds = np.linspace(0, pts.shape[0], world + 1).astype(int)
+    idx = Rng(11).integers(0, pts.shape[0], size=256)  # the same draw on every rank
+    rows = gather_sample_rows(torch.from_numpy(pts[bounds[rank]:bounds[rank + 1]]), int(bounds[rank]),
+                              np.concatenate([idx, [3]]))
+    if rank == 0:
+        np.save(result_path, rows.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_online_tick_rows_gloo_world2(tmp_path, golden):
+    """Online ticks over sharded points: one all-reduce assembles the sampled
+    rows bit-exactly on every rank."""
+    import torch.multiprocessing as mp
+    from oracle import oracle
+    from paper_2201_00701_b200.core import Rng
+
+    port = 30500 + (os.getpid() % 1000)
+    out = tmp_path / "rows.npy"
+    mp.spawn(_gloo_gather_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    rows = np.load(out)
+    pts = golden["small_points"].copy()
+    pts[3, 1] = -0.0
+    idx = Rng(11).integers(0, pts.shape[0], size=256)
+    want = pts[np.concatenate([idx, [3]])]
+    assert rows.tobytes() == want.tobytes()
+    hi, lo = golden["small_hi0"], golden["small_lo"]
+    a = oracle.som_tick(rows[:256], hi, lo, np.arange(256), 0.9, 0.3)
+    b = oracle.som_tick(pts, hi, lo, idx, 0.9, 0.3)
+    assert np.array_equal(a, b)
+
+
 def test_bench_reference_arm_runs_on_cpu():
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
                           "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)

@@ -145,3 +145,17 @@ def test_online_tick_kernels_vs_oracle(g, d, variant, monkeypatch):
     got = esom.kmeans_tick(X, model, kcfg, Rng(6)).cpu().numpy()
     want = oracle.kmeans_tick(pts, hi, Rng(6).integers(0, len(pts), size=200), 0.2)
     assert close(got, want, f"kmeans g={g} d={d} {variant}") > 0.9
+
+
+def test_sharded_online_ticks_single_rank_equal_plain():
+    from paper_2201_00701_b200.sharded import kmeans_tick_sharded, som_tick_sharded
+
+    pts, hi, lo = c2_inputs()
+    model = esom.LandmarkModel.create(hi, lo)
+    X = torch.from_numpy(pts).cuda()
+    a = som_tick_sharded(X, 0, X.shape[0], model, esom.SomConfig(), Rng(4)).cpu().numpy()
+    b = esom.som_tick(X, model, esom.SomConfig(), Rng(4)).cpu().numpy()
+    assert np.array_equal(a, b)
+    a = kmeans_tick_sharded(X, 0, X.shape[0], model, esom.KmeansConfig(), Rng(5)).cpu().numpy()
+    b = esom.kmeans_tick(X, model, esom.KmeansConfig(), Rng(5)).cpu().numpy()
+    assert np.array_equal(a, b)
