@@ -649,6 +649,7 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
     mbar_wait(&bar_load, 0);
     const f2 nz2 = f2_pack(-0.0f, -0.0f);
     const int d4 = (d16 + 3) >> 2;
+    const bool full = d4 == 8 && !a.exact_v1;  // A/B switch (ESOM_EXACT_V1)
     double qe_local = 0.0;
     int slow_local = 0;
     for (int64_t pos = blockIdx.x * (int64_t)kExactBitsThreads + tid; pos < a.n;
@@ -709,6 +710,38 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                 for (int u = 0; u < 4; ++u) lr[u] = reinterpret_cast<const float4*>(Ls + (size_t)jq[u] * ls);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) s4[u] = 0.0f;
+                if (full) {
+                    // d16 == 32: no per-chunk guard, so the row loads of the next
+                    // chunk are issued while the current one is summed (one-chunk
+                    // register prefetch hides the shared-memory latency)
+                    float4 cur[4], nxt[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) cur[u] = lr[u][0];
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        if (c4 < 7) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) nxt[u] = lr[u][c4 + 1];
+                        }
+                        const f2 x01 = f2_pack(x[4 * c4], x[4 * c4 + 1]);
+                        const f2 x23 = f2_pack(x[4 * c4 + 2], x[4 * c4 + 3]);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float4 l4 = cur[u];
+                            const f2 q01 = f2_sq(f2_sub(x01, f2_pack(l4.x, l4.y)), nz2);
+                            const f2 q23 = f2_sq(f2_sub(x23, f2_pack(l4.z, l4.w)), nz2);
+                            float a0, a1, a2, a3;
+                            f2_unpack(q01, a0, a1);
+                            f2_unpack(q23, a2, a3);
+                            s4[u] = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s4[u], a0), a1), a2), a3);
+                        }
+                        if (c4 < 7) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+                        }
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int c4 = 0; c4 < 8; ++c4) {
                     if (c4 < d4) {
@@ -832,6 +865,8 @@ int launch_exact_bits_t(Tc2Args a, cudaStream_t st) {
     if (smem > (size_t)esom_host::max_smem_optin())
         return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact rows exceed shared memory%s", "");
     auto kern = knn_exact_bits_kernel<KP>;
+    static const int v1 = getenv("ESOM_EXACT_V1") ? 1 : 0;
+    a.exact_v1 = v1;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t grid = (a.n + kExactBitsThreads - 1) / kExactBitsThreads;
     if (grid > esom_host::num_sms()) grid = esom_host::num_sms();
