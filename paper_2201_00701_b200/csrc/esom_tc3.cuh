@@ -657,13 +657,26 @@ __global__ void __launch_bounds__(kT3GWarps * 32) knn_exact_group_kernel(T3Exact
 #pragma unroll
                 for (int p = 0; p < kT3GP; ++p) acc[sl][p] = 0.0f;
             const bool two = U > 32, three = U > 64;  // warp-uniform slot counts
+            // landmark rows stream from L2: the next 8-dim chunk is loaded while the
+            // current one is accumulated (one-chunk register prefetch)
+            float4 la[3], lb[3];
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl) {
+                la[sl] = lb[sl] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (sl == 0 || (sl == 1 && two) || (sl == 2 && three)) {
+                    la[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl]));
+                    lb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + 4));
+                }
+            }
             for (int c = 0; c < d; c += 8) {
-                float4 la[3], lb[3];
+                float4 na[3], nb[3];
 #pragma unroll
                 for (int sl = 0; sl < 3; ++sl) {
-                    if (sl == 0 || (sl == 1 && two) || (sl == 2 && three)) {
-                        la[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c));
-                        lb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 4));
+                    na[sl] = la[sl];
+                    nb[sl] = lb[sl];
+                    if (c + 8 < d && (sl == 0 || (sl == 1 && two) || (sl == 2 && three))) {
+                        na[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 8));
+                        nb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 12));
                     }
                 }
 #pragma unroll
@@ -674,6 +687,11 @@ __global__ void __launch_bounds__(kT3GWarps * 32) knn_exact_group_kernel(T3Exact
                     acc[0][p] = acc8f(acc[0][p], la[0], lb[0], xa, xb, nz);
                     if (two) acc[1][p] = acc8f(acc[1][p], la[1], lb[1], xa, xb, nz);
                     if (three) acc[2][p] = acc8f(acc[2][p], la[2], lb[2], xa, xb, nz);
+                }
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl) {
+                    la[sl] = na[sl];
+                    lb[sl] = nb[sl];
                 }
             }
             // ---- per point: rank (distance, index) over U, write the k-NN row ----
