@@ -240,3 +240,35 @@ def test_installed_gpu_tick_round_robin_chunks():
     assert np.array_equal(got[0][1024:], np.zeros((3000 - 1024, 2), np.float32))
     assert rr.state.chunk_cursor == 0
     assert np.array_equal(got[2], want)
+
+
+def test_installed_gpu_tick_graph_mode():
+    """Graph mode through the installed tick: k-means trainer, k_g-NN graph
+    rebuild, device force layout (ref: engine.py:356-375), then the embed."""
+    from oracle import oracle as O
+    from paper_2201_00701_b200 import graphmodel as G
+
+    pts = datagen.extruded_s(3000, seed=8)
+    e = _fake_reference_engine(pts, 3, (6, 6), 16)
+    st = e.state
+    st.mode, st.k_g = "graph", 3
+    st.layout = G.LayoutState.for_count(st.model.g)
+    e._edges_dirty, e._ticks_since_rebuild = True, 0
+
+    def rebuild(self=e):
+        self.state.edges = G.build_knn_graph(self.state.model.hi, min(self.state.k_g, self.state.model.g - 1))
+        self._edges_dirty, self._ticks_since_rebuild = False, 0
+
+    e._rebuild_edges = rebuild
+    hi0, lo0 = st.model.hi.copy(), st.model.lo.copy()
+    rng_copy = esom.Rng(3)
+    esom.engine.init_model(pts, rng_copy, (6, 6))  # advance past the init draw like the engine did
+    p = e.tick()
+    want_hi = O.kmeans_tick(pts, hi0, rng_copy.integers(0, len(pts), size=256), 0.05)
+    np.testing.assert_allclose(st.model.hi, want_hi, rtol=1e-5, atol=1e-6)
+    edges = G.build_knn_graph(want_hi, 3)
+    lay = G.LayoutState.for_count(len(lo0))
+    want_lo, _ = F.layout_tick(lo0, edges.pairs, edges.rest, lay.velocities, lay.stiffness, lay.repulsion, 1e-3,
+                               lay.damping, lay.dt)
+    assert np.max(np.abs(st.model.lo - want_lo)) <= 1e-5
+    assert len(p.edges) == len(edges) and np.all(np.isfinite(p.positions))
