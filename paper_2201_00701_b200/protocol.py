@@ -14,6 +14,7 @@ PCIe (mapped memory: no device staging buffer, no separate copy).
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -77,6 +78,22 @@ def pack_frame_points(xy: torch.Tensor, colors: torch.Tensor, frame_id: int, buf
     return nbytes
 
 
+_tls = threading.local()
+
+
+def _cached_buffer(nbytes: int, dev) -> FrameBuffer:
+    """Per-(thread, device) pinned buffer, grown on demand (page-locking is
+    expensive; the synchronous encoder reuses it call after call)."""
+    cache = getattr(_tls, "frames", None)
+    if cache is None:
+        cache = _tls.frames = {}
+    key = dev.index if isinstance(dev, torch.device) else int(dev)
+    buf = cache.get(key)
+    if buf is None or buf.capacity < nbytes:
+        buf = cache[key] = FrameBuffer(max(nbytes, 1 << 16), dev)
+    return buf
+
+
 def encode_frame_points(frame_id: int, positions, colors) -> bytes:
     """``protocol.encode(FramePoints(frame_id, positions, colors))`` computed on
     the device (ref: protocol.py:205-210, 216-218)."""
@@ -87,7 +104,7 @@ def encode_frame_points(frame_id: int, positions, colors) -> bytes:
             col = colors.detach().to(device=dev, dtype=torch.uint8).contiguous()
         else:
             col = torch.from_numpy(np.ascontiguousarray(colors, dtype=np.uint8)).to(dev)
-        buf = FrameBuffer(frame_points_bytes(xy.shape[0]), dev)
+        buf = _cached_buffer(frame_points_bytes(xy.shape[0]), dev)
         nbytes = pack_frame_points(xy, col, frame_id, buf)
         buf.event.synchronize()
         return bytes(buf.host[:nbytes].numpy())
