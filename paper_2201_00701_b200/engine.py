@@ -14,8 +14,7 @@ dataset is uploaded ONCE per dataset object and stays in HBM; per frame:
                                                         straight into pinned host memory
 
 ``DeviceSession`` holds that state for one dataset; ``FrameEngine`` is the
-reference Engine's construction + SOM/k-means tick without the command
-plane; ``gpu_tick`` is a drop-in replacement for ``embedview.engine.Engine.tick``
+reference Engine's construction + SOM-mode tick without the command plane; ``gpu_tick`` is a drop-in replacement for ``embedview.engine.Engine.tick``
 (installed by ``paper_2201_00701_b200.install``) that keeps the reference's
 command handling, graph layout and packet type and moves the rest here.
 """
@@ -180,8 +179,13 @@ class DeviceSession:
                 self._pos_host = torch.empty((self.n, 2), dtype=torch.float32, pin_memory=True)
             self._pos_host.copy_(self.positions, non_blocking=True)
             torch.cuda.current_stream(self.device).synchronize()
-            _dev.raise_if_nonfinite(self.flag)
+            self._check_flag()
             return self._pos_host.numpy().copy()
+
+    def _check_flag(self) -> None:
+        if int(self.flag.item()):
+            self.flag.zero_()  # report once; the next frame starts clean
+            raise InputError("non-finite input")
 
     def frame_record(self, frame_id: int, color_dim: int) -> memoryview:
         """The FramePoints wire record of the current positions, packed by the
@@ -193,7 +197,7 @@ class DeviceSession:
                 self._frame = FrameBuffer(frame_points_bytes(self.n), self.device)
             nbytes = pack_frame_points(self.positions, col, frame_id, self._frame)
             self._frame.event.synchronize()
-            _dev.raise_if_nonfinite(self.flag)
+            self._check_flag()
             return memoryview(self._frame.host.numpy())[:nbytes]
 
 
@@ -211,10 +215,10 @@ class DeviceFrame:
 
 @dataclass
 class FrameEngine:
-    """The reference Engine's construction and SOM / k-means tick with the
+    """The reference Engine's construction and SOM-mode tick with the
     dataset, model and frame resident on the B200 (ref: engine.py:163-199,
-    347-399).  Graph-mode layout and the command plane stay with the
-    reference Engine (see ``gpu_tick``)."""
+    347-399).  Graph mode (k-means + layout) and the command plane run
+    through the reference Engine with ``gpu_tick`` installed."""
 
     dataset: object
     seed: int
