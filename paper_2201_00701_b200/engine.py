@@ -14,9 +14,10 @@ dataset is uploaded ONCE per dataset object and stays in HBM; per frame:
                                                         straight into pinned host memory
 
 ``DeviceSession`` holds that state for one dataset; ``FrameEngine`` is the
-reference Engine's construction + SOM-mode tick without the command plane; ``gpu_tick`` is a drop-in replacement for ``embedview.engine.Engine.tick``
+reference Engine's construction + SOM-mode tick without the command plane;
+``gpu_tick`` is a drop-in replacement for ``embedview.engine.Engine.tick``
 (installed by ``paper_2201_00701_b200.install``) that keeps the reference's
-command handling, graph layout and packet type and moves the rest here.
+command handling, graph bookkeeping and packet type and moves the rest here.
 """
 
 from __future__ import annotations
