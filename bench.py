@@ -237,6 +237,13 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         loop.frame()
     barrier()
+    # one frame = one CUDA-graph launch (single rank, or no collective in the frame;
+    # NCCL inside captured graphs is left out of the multi-rank training loop)
+    use_graph = not args.no_graph and (world == 1 or not train)
+    if use_graph:
+        loop.capture()
+        loop.frame()
+        barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     from paper_2201_00701_b200 import _lib as _lc
@@ -251,6 +258,8 @@ def run_ours(args):
             ev[s][1].record(stream)
         barrier()
     launches_timed = _lc.load().esom_launch_count() - launches0  # our kernels inside the timed region
+    if use_graph:  # replays bypass the host-side counter: kernels captured per frame x frames
+        launches_timed = loop.graph_launches * args.steps
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = sum(step_ms) / len(step_ms)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -271,7 +280,7 @@ def run_ours(args):
     flush.zero_()
     torch.cuda.synchronize(dev)
     L.esom_timing_begin(1)
-    loop.frame()
+    loop._eager_frame()  # eager: the timing hooks record events around each launch
     torch.cuda.synchronize(dev)
     ktimes = {}
     for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "knn_gemm_kernel", "knn_exact_group_kernel",
@@ -359,7 +368,8 @@ def run_ours(args):
             "data": "synthetic Gaussian mixture (reference datagen.gaussians restated), SOM-initialised landmarks",
             "config": {"workload": desc, "n_per_rank": n, "d": d, "g": g, "k": k, "train": train,
                        "parallelism": f"points sharded x{world}, landmarks replicated",
-                       "l2": "flushed between timed steps (256 MiB write outside the events); X = 128 MiB/rank"},
+                       "l2": "flushed between timed steps (256 MiB write outside the events); X = 128 MiB/rank",
+                       "cuda_graph": use_graph},
             "roofline": roofline,
             "compute_roofline": compute_roofline,
             "clocks": clocks,
@@ -382,6 +392,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch each frame's kernels eagerly (no CUDA graph)")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for single-GPU dry runs")
     args = ap.parse_args()
     if args.impl == "reference":

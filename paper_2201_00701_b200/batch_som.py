@@ -123,7 +123,32 @@ class FrameLoop:
         embed = _lib.load().esom_embed_launches(n, g, d, self.model.k)
         return embed + (4 if self.train else 0)
 
+    def capture(self) -> "FrameLoop":
+        """Record one frame as a CUDA graph (after a warm frame: workspaces
+        allocated, kernel attributes set); frame() then replays it -- one
+        graph launch instead of ~5-15 kernel launches and host calls per
+        frame.  The library's launch counter only advances at capture, so the
+        kernels per replay are kept in ``graph_launches``."""
+        from . import _lib as L
+
+        self._eager_frame()
+        torch.cuda.synchronize(self.dev)
+        n0 = L.load().esom_launch_count()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.device(self.dev), torch.cuda.graph(g):
+            self._eager_frame()
+        self.graph_launches = L.load().esom_launch_count() - n0
+        self.graph = g
+        return self
+
     def frame(self) -> torch.Tensor:
+        g = getattr(self, "graph", None)
+        if g is not None:
+            g.replay()
+            return self.xy
+        return self._eager_frame()
+
+    def _eager_frame(self) -> torch.Tensor:
         m = self.model
         g, d = m.hi.shape
         if not self.train:

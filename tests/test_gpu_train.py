@@ -159,3 +159,21 @@ def test_sharded_online_ticks_single_rank_equal_plain():
     a = kmeans_tick_sharded(X, 0, X.shape[0], model, esom.KmeansConfig(), Rng(5)).cpu().numpy()
     b = esom.kmeans_tick(X, model, esom.KmeansConfig(), Rng(5)).cpu().numpy()
     assert np.array_equal(a, b)
+
+
+def test_frame_loop_cuda_graph_replay_equals_eager():
+    """bench.py times one CUDA-graph launch per frame: replaying the captured
+    frame (fused embed + BMU statistics + update + re-preparation) must give
+    bit-identical landmarks and positions to eager frames."""
+    pts, hi, lo = c2_inputs()
+    X = torch.from_numpy(pts[:200_000]).cuda()
+    a = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=1.0, alpha=0.05))
+    b = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=1.0, alpha=0.05))
+    for _ in range(4):
+        a.frame()
+    b.capture()  # capture() runs one eager frame first, then records one
+    for _ in range(2):
+        b.frame()
+    torch.cuda.synchronize()
+    assert torch.equal(a.model.hi, b.model.hi)
+    assert torch.equal(a.xy, b.xy)
