@@ -169,9 +169,9 @@ def test_frame_loop_cuda_graph_replay_equals_eager():
     X = torch.from_numpy(pts[:200_000]).cuda()
     a = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=1.0, alpha=0.05))
     b = FrameLoop(X, hi, lo, 16, BatchSomConfig(sigma=1.0, alpha=0.05))
-    for _ in range(4):
+    for _ in range(3):
         a.frame()
-    b.capture()  # capture() runs one eager frame first, then records one
+    b.capture()  # one eager frame, then one recorded (not executed) frame
     for _ in range(2):
         b.frame()
     torch.cuda.synchronize()
