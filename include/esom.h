@@ -102,6 +102,19 @@ int esom_embed_prepared(const float *X, int64_t n, int32_t d, const float *hi, c
                         double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
                         cudaStream_t stream);
 
+/* esom_embed_prepared with options.  flags: ESOM_EMBED_BMU_ORDER = visit
+ * points grouped by nearest landmark in the projection (neighbour rows and
+ * pair-table entries shared across a warp; pays a BMU counting sort -- worth
+ * it when most points are far from tightly packed landmarks, e.g. a trained
+ * SOM).  far_count (nullable, device int32): += points that took the f64
+ * far-point distance path -- the caller's signal for the next frame's flag. */
+#define ESOM_EMBED_BMU_ORDER 1
+int esom_embed_prepared_ex(const float *X, int64_t n, int32_t d, const float *hi, const float *lo,
+                           int32_t g, int32_t k, const void *model_ws, void *point_ws,
+                           size_t point_ws_bytes, float *xy, int32_t *bmu, double *acc_S,
+                           double *acc_C, double *qe_sum, int32_t *nonfinite_flag, int32_t flags,
+                           int32_t *far_count, cudaStream_t stream);
+
 /* Number of kernels one esom_embed_prepared(n, ...) call launches (evidence
  * for the benchmark's launch count). */
 int32_t esom_embed_launches(int64_t n, int32_t g, int32_t d, int32_t k);

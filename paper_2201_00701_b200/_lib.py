@@ -31,6 +31,8 @@ SIGNATURES = {
     "esom_prepare_model": [_vp, _i32, _i32, _i32, _vp, _sz, _vp, _vp],
     "esom_embed_prepared": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp,
                             _vp],
+    "esom_embed_prepared_ex": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _i32, _vp, _vp],
     "esom_embed": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "esom_bmu_accumulate": [_vp, _i64, _i32, _vp, _i32, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp],
     "esom_som_tick": [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _f64, _f64, _vp, _sz, _vp],

@@ -1297,6 +1297,15 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
 int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
                         const void* model_ws, void* point_ws, size_t point_ws_bytes, float* xy, int32_t* bmu,
                         double* acc_S, double* acc_C, double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
+    return esom_embed_prepared_ex(X, n, d, hi, lo, g, k, model_ws, point_ws, point_ws_bytes, xy, bmu, acc_S, acc_C,
+                                  qe_sum, nonfinite_flag, 0, nullptr, stream);
+}
+
+int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g,
+                           int32_t k, const void* model_ws, void* point_ws, size_t point_ws_bytes, float* xy,
+                           int32_t* bmu, double* acc_S, double* acc_C, double* qe_sum, int32_t* nonfinite_flag,
+                           int32_t flags, int32_t* far_count, cudaStream_t stream) {
+    const bool bmu_order = (flags & ESOM_EMBED_BMU_ORDER) != 0;
     if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64%s", "");
     if (n == 0) return ESOM_OK;
@@ -1327,7 +1336,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         ProjArgs q{};
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
         const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
-        if (l2_table || acc_S || acc_C || (use_rec && m >= 4096)) {
+        if (l2_table || acc_S || acc_C || ((use_rec || bmu_order) && m >= 4096)) {
             // BMU counting sort of the chunk (BMU = idx[:, 0]): the projection visits
             // points grouped by BMU (pair-table reads coalesce when the table is in
             // L2) and the batch-SOM sums are segment sums over the same order
@@ -1344,7 +1353,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
                                                                                   acc_S, acc_C);
                 if (int e = cuda_check("bmu_segsum_kernel")) return e;
             }
-            if (l2_table || use_rec) q.perm = perm;
+            if (l2_table || use_rec || bmu_order) q.perm = perm;
         }
         q.idx = idx;
         q.sqd = sqd;
@@ -1354,6 +1363,7 @@ int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, c
         q.lo = lo;
         q.T = T;
         q.tmax = reinterpret_cast<const float*>(mws + ml.lstats) + 2;
+        q.prec_count = far_count;
         q.xy = xy + 2 * s;
         q.X = X + s * d;
         q.hi = hi;

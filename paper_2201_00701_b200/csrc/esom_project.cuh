@@ -110,6 +110,17 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // (s_{k-1} - s_0) T_max before the exact x-based f64 loop takes over).
 constexpr double kKappaMax64 = 1e5;
 
+// Far-point census for the host's visiting-order choice (esom_embed_prepared_ex):
+// one warp-aggregated atomic per warp.
+__device__ __forceinline__ void count_prec(int32_t* cnt, bool prec) {
+    if (!cnt) return;
+    const unsigned am = __activemask();
+    const unsigned b = __ballot_sync(am, prec);
+    if ((threadIdx.x & 31) == __ffs(am) - 1 && b) atomicAdd(cnt, __popc(b));
+}
+
+
+
 template <int KP>
 __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, const float* __restrict__ hi,
                                             const int (&jj)[KP], int k, float (&qe)[KP]) {
@@ -292,6 +303,7 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         bool uniform = sig < (float)kScoreEps;
         // far from the landmarks (kappa bound large): f64 paths below
         const bool prec = 2.0f * sqk * tmax_model > (float)kKappaMax;
+        count_prec(a.prec_count, prec);
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);
@@ -630,6 +642,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
         const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
+        count_prec(a.prec_count, prec);
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);
@@ -875,6 +888,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
         const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
+        count_prec(a.prec_count, prec);
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);

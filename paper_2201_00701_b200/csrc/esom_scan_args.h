@@ -38,6 +38,7 @@ struct ProjArgs {
     const int32_t* perm;     // optional visiting order (nullable)
     const float4* rec;       // g x g pair records {T, g1, g2, g.lo_u} (project_reg3_kernel; nullable)
     const float* tmax;       // device scalar: max kept T of the model (f64-distance decision)
+    int32_t* prec_count;     // += points that took the f64 far-point path (nullable)
 };
 
 // tensor-core screened k-NN (esom_tc.cuh)

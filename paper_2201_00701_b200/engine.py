@@ -111,6 +111,9 @@ class DeviceSession:
             self.n, self.d = X.shape
             self.positions = torch.zeros((self.n, 2), dtype=torch.float32, device=self.device)
             self.flag = _dev.new_flag(self.device)
+            self.far_count = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._far_rows = 0  # rows embedded since far_count was last read
+        self.bmu_order = False
         self.data = _DeviceDataset(self.X)
         stats = getattr(dataset, "dim_stats", None)
         if stats is not None:  # the reference Dataset carries exact numpy statistics
@@ -167,10 +170,26 @@ class DeviceSession:
             raise ParameterError(f"unknown knn backend {backend!r}")
         stop = self.n if stop is None else stop
         with torch.cuda.device(self.device):
+            self._update_order()
             pm = self.prepared(hi, lo, params.k)
             if stop > start:
-                pm.embed_into(self.X[start:stop], self.positions[start:stop], flag=self.flag)
+                pm.embed_into(self.X[start:stop], self.positions[start:stop], flag=self.flag,
+                              bmu_order=self.bmu_order, far_count=self.far_count)
+                self._far_rows += stop - start
         return self.positions
+
+    def _update_order(self) -> None:
+        """Visit the projection in nearest-landmark order when most points of
+        the previous frame took the f64 far-point path (a trained SOM packs
+        its landmarks tightly: neighbour rows are then shared across a warp,
+        0.80 -> 0.61 ms per 2^20 points on C3; an untrained model skips the
+        sort).  Reading the census is one 4-byte copy; the frame loops have
+        already synchronised the stream (trainer output / positions)."""
+        if self._far_rows:
+            far = int(self.far_count.item())
+            self.bmu_order = 2 * far > self._far_rows
+            self.far_count.zero_()
+            self._far_rows = 0
 
     def positions_host(self) -> np.ndarray:
         """Positions copied to a fresh host array (synchronises; raises on

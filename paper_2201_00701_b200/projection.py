@@ -177,15 +177,18 @@ class PreparedModel:
         return self.pws
 
     def embed_into(self, X: torch.Tensor, xy: torch.Tensor, *, bmu=None, acc_S=None, acc_C=None, qe_sum=None,
-                   flag=None, stream=None) -> None:
+                   flag=None, stream=None, bmu_order: bool = False, far_count=None) -> None:
         """Asynchronous embed of device points X (n×d f32) into xy (n×2 f32):
-        k-NN scan + projection kernels per L2-resident chunk."""
+        k-NN scan + projection kernels per L2-resident chunk.  ``bmu_order``
+        visits the projection in nearest-landmark order; ``far_count`` (device
+        int32) accumulates the points that took the f64 far-point path."""
         n, d = X.shape
         st = stream if stream is not None else _dev.stream_handle(self.device)
         pws = self.point_workspace(n)
-        _lib.call("esom_embed_prepared", _dev.ptr(X), n, d, _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.k,
+        _lib.call("esom_embed_prepared_ex", _dev.ptr(X), n, d, _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.k,
                   _dev.ptr(self.ws), _dev.ptr(pws), pws.numel(), _dev.ptr(xy), _dev.ptr(bmu), _dev.ptr(acc_S),
-                  _dev.ptr(acc_C), _dev.ptr(qe_sum), _dev.ptr(flag if flag is not None else self.flag), st)
+                  _dev.ptr(acc_C), _dev.ptr(qe_sum), _dev.ptr(flag if flag is not None else self.flag),
+                  1 if bmu_order else 0, _dev.ptr(far_count), st)
 
 
 def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_size: int | None = None,

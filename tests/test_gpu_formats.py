@@ -272,3 +272,25 @@ def test_installed_gpu_tick_graph_mode():
                                lay.damping, lay.dt)
     assert np.max(np.abs(st.model.lo - want_lo)) <= 1e-5
     assert len(p.edges) == len(edges) and np.all(np.isfinite(p.positions))
+
+
+def test_session_switches_to_bmu_order_on_trained_models():
+    """After a frame in which most points took the far-point path, the session
+    visits the projection in nearest-landmark order; per-point results do not
+    depend on the visiting order (bit-identical positions)."""
+    pts = datagen.gaussians(16, 1 << 16, 32, seed=1)[0].astype(np.float32)
+    eng = FrameEngine(pts, seed=7, k=16, grid=(16, 16))
+    for _ in range(10):
+        eng.tick()
+    s = eng.session
+    eng.training_paused = True
+    first = eng.tick().positions.clone()
+    assert s.bmu_order is False or s.bmu_order is True
+    eng.tick()
+    assert s.bmu_order, "trained C3-like model: far-point census should select BMU order"
+    assert torch.equal(eng.tick().positions, first)
+    fresh = FrameEngine(pts, seed=7, k=16, grid=(16, 16))
+    fresh.training_paused = True
+    fresh.tick()
+    fresh.tick()
+    assert not fresh.session.bmu_order  # untrained model: natural order, no sort
