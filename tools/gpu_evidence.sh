@@ -21,6 +21,6 @@ PROBE_VARIANTS=w4 timeout 900 ncu --set full --clock-control none --import-sourc
 timeout 600 python tools/bench_rows.py > gpurun_out/r_rows.jsonl 2> gpurun_out/r_rows.err
 timeout 300 python tools/probe_train.py > gpurun_out/r_train.txt 2>&1
 timeout 300 python tools/probe_tick.py > gpurun_out/r_tick.txt 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:online_tick_reg -c 1 -o gpurun_out/r_tick_c3 python tools/probe_train.py > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:online_tick_row -c 1 -o gpurun_out/r_tick_c3 python tools/probe_train.py > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fcs_decode|dim_partial4|transform4|frame_points_pack" -c 4 -o gpurun_out/r_rows python tools/bench_rows.py --rows ingest,engine --steps 2 > /dev/null 2>&1
 ls gpurun_out
