@@ -361,33 +361,46 @@ int bmu_sort(const int32_t* idx, int64_t n, int k, int g, int32_t* cntb, int32_t
 }
 
 // Batch-SOM statistics from a BMU-sorted order (after bmu_scatter, ends[b] is
-// the end of landmark b's segment of perm): one warp per (landmark, 32-dim
-// slice, part of <= kSegPart points) sums its points' coordinates in f64 and
-// adds the partial to S / C (a handful of f64 atomics per address instead of
-// one per point and dimension).
-constexpr int kSegPart = 256;
+// the end of landmark b's segment of perm): one warp per (kSegPart sorted
+// positions, 32-dim slice) sums its points' coordinates in f64 and adds one
+// partial per segment it touches to S / C (~n/64 f64 atomics per address
+// row instead of one per point and dimension; the order of the partials is
+// scheduling dependent in the last f64 bits).
+constexpr int kSegPart = 64;
 
-__global__ void bmu_segsum_kernel(const float* __restrict__ X, int d, const int32_t* __restrict__ perm,
-                                  const int32_t* __restrict__ ends, int g, int parts, double* __restrict__ S,
-                                  double* __restrict__ C) {
+__global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict__ X, int d,
+                                                         const int32_t* __restrict__ perm,
+                                                         const int32_t* __restrict__ ends, int g, int64_t n,
+                                                         double* __restrict__ S, double* __restrict__ C) {
+    // warp w sums sorted positions [w*kSegPart, (w+1)*kSegPart) (times the 32-dim
+    // slices): every launched warp has work; a range crossing a BMU boundary
+    // flushes one partial per segment it touches (binary search for the first)
     const int lane = threadIdx.x & 31;
     const int nsl = (d + 31) / 32;
-    const int64_t nw = (int64_t)g * nsl * parts;
+    const int64_t nch = (n + kSegPart - 1) / kSegPart;
+    const int64_t nw = nch * nsl;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int part = (int)(w % parts);
-        const int sl = (int)((w / parts) % nsl);
-        const int b = (int)(w / ((int64_t)parts * nsl));
+        const int sl = (int)(w % nsl);
+        const int64_t p0 = (w / nsl) * kSegPart;
+        const int64_t p1 = p0 + kSegPart < n ? p0 + kSegPart : n;
         const int c = sl * 32 + lane;
-        const int e1s = ends[b], e0s = b ? ends[b - 1] : 0;
-        double acc = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        int cntp = 0;
-        for (int e0 = e0s + part * kSegPart; e0 < e1s; e0 += parts * kSegPart) {  // parts stride the segment
-            const int e1 = e0 + kSegPart < e1s ? e0 + kSegPart : e1s;
+        // segment of p0: first b with ends[b] > p0
+        int lo_b = 0, hi_b = g - 1;
+        while (lo_b < hi_b) {
+            const int mid = (lo_b + hi_b) >> 1;
+            if (__ldg(ends + mid) > p0) hi_b = mid;
+            else lo_b = mid + 1;
+        }
+        int b = lo_b;
+        int64_t pos = p0;
+        while (pos < p1) {
+            const int64_t e = min((int64_t)__ldg(ends + b), p1);
+            double acc = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
             if (S)
-                for (int base = e0; base < e1; base += 32) {  // 32 perm entries per coalesced load
-                    const int pe = base + lane < e1 ? __ldg(perm + base + lane) : 0;
-                    const int nb = e1 - base < 32 ? e1 - base : 32;
+                for (int64_t base = pos; base < e; base += 32) {  // 32 perm entries per coalesced load
+                    const int pe = base + lane < e ? __ldg(perm + base + lane) : 0;
+                    const int nb = e - base < 32 ? (int)(e - base) : 32;
                     float v[32];  // 32 row loads in flight per lane
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
@@ -402,14 +415,60 @@ __global__ void bmu_segsum_kernel(const float* __restrict__ X, int d, const int3
                         acc3 += (double)v[q + 3];
                     }
                 }
-            cntp += e1 - e0;
+            acc += (acc1 + acc2) + acc3;
+            if (e > pos) {
+                if (S && c < d) atomicAdd(S + (int64_t)b * d + c, acc);
+                if (C && lane == 0 && sl == 0) atomicAdd(C + b, (double)(e - pos));
+            }
+            pos = e;
+            ++b;
         }
-        acc += (acc1 + acc2) + acc3;
-        if (!cntp) continue;
-        if (S && c < d) atomicAdd(S + (int64_t)b * d + c, acc);
-        if (C && lane == 0 && sl == 0) atomicAdd(C + b, (double)cntp);
     }
 }
+
+
+// Batch-SOM statistics straight from the natural point order when the f64
+// table fits one SM (d <= 32, g (d + 1) 8 B <= 200 KB; C3): X streams
+// coalesced, each warp adds 8 points per step into a shared-memory f64 table
+// (lane = dimension, red.shared.add.f64), then one f64 atomic per table entry
+// into S / C.  No BMU sort and no row gather (the sorted-segment kernel above
+// reads X in BMU order: random 128-byte rows, ncu 1.3 TB/s at C3).
+constexpr int kAccThreads = 1024;
+
+__global__ void __launch_bounds__(kAccThreads) bmu_accum_smem_kernel(const float* __restrict__ X, int64_t n, int d,
+                                                                    const int32_t* __restrict__ idx, int k, int g,
+                                                                    double* __restrict__ S, double* __restrict__ C) {
+    extern __shared__ double sS[];  // g x d, then g counts
+    double* sC = sS + (size_t)g * d;
+    for (int e = threadIdx.x; e < g * d + g; e += kAccThreads) sS[e] = 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (kAccThreads / 32) + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * (kAccThreads / 32);
+    for (int64_t i0 = gw * 8; i0 < n; i0 += nwarps * 8) {
+        float v[8];
+        int b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = i0 + u;
+            b[u] = i < n ? __ldg(idx + i * k) : -1;
+            v[u] = (i < n && lane < d) ? __ldg(X + i * d + lane) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (b[u] < 0) continue;
+            if (lane < d) atomicAdd(sS + (size_t)b[u] * d + lane, (double)v[u]);
+            if (lane == 0) atomicAdd(sC + b[u], 1.0);
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < g * d; e += kAccThreads)
+        if (S && sS[e] != 0.0) atomicAdd(S + e, sS[e]);
+    for (int j = threadIdx.x; j < g; j += kAccThreads)
+        if (C && sC[j] != 0.0) atomicAdd(C + j, sC[j]);
+}
+
+bool accum_smem_ok(int g, int d) { return d <= 32 && ((size_t)g * d + g) * 8 <= 200 * 1024; }
 
 // ---------------------------------------------------------------------------
 // Scores (ref: projection.py:38-59).  numba's float(f32) stays f32, so the
@@ -1336,7 +1395,15 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         ProjArgs q{};
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
         const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
-        if (l2_table || acc_S || acc_C || ((use_rec || bmu_order) && m >= 4096)) {
+        const bool need_perm = l2_table || ((use_rec || bmu_order) && m >= 4096);
+        const bool acc_smem = (acc_S || acc_C) && !need_perm && accum_smem_ok(g, d) && !getenv("ESOM_SEGSUM");
+        if (acc_smem) {
+            const size_t smem = ((size_t)g * d + g) * 8;
+            cudaFuncSetAttribute(bmu_accum_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            bmu_accum_smem_kernel<<<num_sms(), kAccThreads, smem, stream>>>(X + s * d, m, d, idx, k, g, acc_S, acc_C);
+            if (int e = cuda_check("bmu_accum_smem_kernel")) return e;
+        }
+        if (need_perm || ((acc_S || acc_C) && !acc_smem)) {
             // BMU counting sort of the chunk (BMU = idx[:, 0]): the projection visits
             // points grouped by BMU (pair-table reads coalesce when the table is in
             // L2) and the batch-SOM sums are segment sums over the same order
@@ -1344,12 +1411,9 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
             int32_t* perm = reinterpret_cast<int32_t*>(base);
             int32_t* cntb = reinterpret_cast<int32_t*>(base + align256((size_t)chunk * 4));
             if (int e = bmu_sort(idx, m, k, g, cntb, perm, stream)) return e;
-            if (acc_S || acc_C) {
-                // parts per landmark sized for the mean segment; long segments loop over parts
-                const int64_t mean = (m + g - 1) / g;
-                const int parts = (int)((4 * mean + kSegPart - 1) / kSegPart) + 1;
-                const int64_t warps = (int64_t)g * ((d + 31) / 32) * parts;
-                bmu_segsum_kernel<<<grid_for(warps * 32, 256), 256, 0, stream>>>(X + s * d, d, perm, cntb, g, parts,
+            if ((acc_S || acc_C) && !acc_smem) {
+                const int64_t warps = (m + kSegPart - 1) / kSegPart * ((d + 31) / 32);
+                bmu_segsum_kernel<<<grid_for(warps * 32, 256), 256, 0, stream>>>(X + s * d, d, perm, cntb, g, m,
                                                                                   acc_S, acc_C);
                 if (int e = cuda_check("bmu_segsum_kernel")) return e;
             }
