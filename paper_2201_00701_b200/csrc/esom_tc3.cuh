@@ -41,7 +41,13 @@ constexpr int kT3LogCap = 64;        // per-thread candidate log in smem
 constexpr int kT3Groups = 64;        // landmark groups of the pass-1 bound
 constexpr uint32_t kT3AChunk = 128u * kT3Kc * 2u;   // one A tile chunk (hi or lo), bytes
 constexpr uint32_t kT3BChunk = 256u * kT3Kc * 2u;   // one B round chunk (hi or lo), bytes
-constexpr uint32_t kT3Stage = 4u * kT3AChunk + 2u * kT3BChunk;
+// MMA N = 128: a 256-landmark round is issued as two half-rounds into
+// alternating TMEM buffers (2 x [2 tiles x 128 columns]), so the MMAs of
+// half-round h + 1 run while the epilogue reads half-round h (one buffer
+// serialised MMA and epilogue: tensor pipe ~54 % active).
+constexpr int kT3N = 128;
+constexpr uint32_t kT3BHalf = kT3BChunk / 2;          // rows [128 h, 128 h + 128) of a round chunk
+constexpr uint32_t kT3Stage = 4u * kT3AChunk + 2u * kT3BHalf;
 
 // Rigorous-by-model bound E on |D~_j - (d_ref_j - |x'|^2)|:
 //  split residual 8 2^-18 S; tensor-core accumulation budgeted at 4 2^-23 (N + 2S)
@@ -114,13 +120,13 @@ __device__ __forceinline__ float kth_of_64(const float (&gm)[kT3Groups], int k) 
 template <int KP>
 __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full[kT3Stages], empty[kT3Stages], tmem_full, tmem_empty;
+    __shared__ __align__(8) uint64_t full[kT3Stages], empty[kT3Stages], tmem_full[2], tmem_empty[2];
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int nkc = a.dk / kT3Kc;                 // K chunks
-    const int R = a.gpad / kT3Rows;               // landmark rounds
+    const int R = a.gpad / kT3N;                  // landmark half-rounds (MMA N = 128)
     const int64_t nsup = (a.n + 255) / 256;       // 256-point super tiles
     unsigned char* stage = smem_raw;
     float* logv = reinterpret_cast<float*>(smem_raw + kT3Stages * kT3Stage);
@@ -131,8 +137,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(&tmem_full, 1);
-        mbar_init(&tmem_empty, kT3Epi);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmem_full[b], 1);
+            mbar_init(&tmem_empty[b], kT3Epi);
+        }
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -164,34 +172,36 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                                 if (!hi_only)
                                     tma_bulk_g2s(sb + (2 * t + 1) * kT3AChunk, a.Alo + ao, kT3AChunk, &full[s]);
                             }
-                            const size_t bo = ((size_t)r * nkc + kc) * (kT3BChunk / 2);
-                            tma_bulk_g2s(sb + 4 * kT3AChunk, a.Bhi + bo, kT3BChunk, &full[s]);
+                            const size_t bo = ((size_t)(r >> 1) * nkc + kc) * (kT3BChunk / 2) +
+                                              (size_t)(r & 1) * (kT3BHalf / 2);  // bf16 elements
+                            tma_bulk_g2s(sb + 4 * kT3AChunk, a.Bhi + bo, kT3BHalf, &full[s]);
                             if (!hi_only)
-                                tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BChunk, a.Blo + bo, kT3BChunk, &full[s]);
+                                tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BHalf, a.Blo + bo, kT3BHalf, &full[s]);
                         }
         }
     } else if (warp == kT3Epi / 32 + 1) {
         // ---------------- MMA issuer ----------------
         if ((tid & 31) == 0) {
             uint32_t q = 0, rr = 0;
-            const uint32_t idesc = umma_idesc_bf16(128, kT3Rows);
+            const uint32_t idesc = umma_idesc_bf16(128, kT3N);
             const uint32_t sboA = (kT3Kc / 8) * 128, sboB = (kT3Kc / 8) * 128, lbo = 128;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
                 for (int pass = 2 - a.passes; pass < 2; ++pass)
                     for (int r = 0; r < R; ++r, ++rr) {
-                        mbar_wait(&tmem_empty, (rr & 1u) ^ 1u);  // epilogue has read the previous round
+                        const uint32_t buf = rr & 1u;
+                        mbar_wait(&tmem_empty[buf], ((rr >> 1) & 1u) ^ 1u);  // epilogue read this buffer's last use
                         tc_fence_after();
                         for (int kc = 0; kc < nkc; ++kc, ++q) {
                             const int s = (int)(q % kT3Stages);
                             mbar_wait(&full[s], (q / kT3Stages) & 1u);
                             tc_fence_after();
                             const uint32_t sb = smem_u32(stage + (size_t)s * kT3Stage);
-                            const uint32_t bh = sb + 4 * kT3AChunk, bl = bh + kT3BChunk;
+                            const uint32_t bh = sb + 4 * kT3AChunk, bl = bh + kT3BHalf;
                             for (int ks = 0; ks < kT3Kc / 16; ++ks) {
                                 const uint32_t ko = (uint32_t)ks * 256u;
                                 for (int t = 0; t < 2; ++t) {
                                     const uint32_t ah = sb + (2 * t) * kT3AChunk, al = ah + kT3AChunk;
-                                    const uint32_t dcol = tmem + (uint32_t)(kT3Rows * t);
+                                    const uint32_t dcol = tmem + buf * 256u + (uint32_t)(kT3N * t);
                                     const uint32_t acc0 = (kc | ks) ? 1u : 0u;
                                     umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
                                               acc0);
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                             }
                             umma_commit(&empty[s]);  // stage reusable once these MMAs retire
                         }
-                        umma_commit(&tmem_full);
+                        umma_commit(&tmem_full[buf]);
                     }
         }
     } else {
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
         const int t = tid >> 7;              // tile within the super tile
         const int lane_row = tid & 127;
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-        const uint32_t tcol = tmem + lane_off + (uint32_t)(kT3Rows * t);
+        const uint32_t tcol0 = tmem + lane_off + (uint32_t)(kT3N * t);
         const float lmax = __ldg(a.lstats), lnmax = __ldg(a.lstats + 1);
         float* lv = logv + tid;
         unsigned short* lj = logj + tid;
@@ -229,11 +239,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             for (int q = 0; q < kT3Groups; ++q) gm[q] = kInf;
             // ---- pass 1 (two-pass mode): group minima over all rounds ----
             for (int r = 0; r < (a.passes == 2 ? R : 0); ++r, ++rr) {
-                mbar_wait(&tmem_full, rr & 1u);
+                const uint32_t buf = rr & 1u, tcol = tcol0 + buf * 256u;
+                mbar_wait(&tmem_full[buf], (rr >> 1) & 1u);
                 tc_fence_after();
-                const float* lnr = a.ln + (size_t)r * kT3Rows;
+                const float* lnr = a.ln + (size_t)r * kT3N;
 #pragma unroll 1
-                for (int c0 = 0; c0 < kT3Rows; c0 += 64) {
+                for (int c0 = 0; c0 < kT3N; c0 += 64) {
                     uint32_t v0[32], v1[32];
                     tmem_ld32_async(tcol + (uint32_t)c0, v0);
                     tmem_ld32_async(tcol + (uint32_t)(c0 + 32), v1);
@@ -245,7 +256,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&tmem_empty);
+                mbar_arrive(&tmem_empty[buf]);
             }
             // one-pass mode: no bound yet (every landmark is logged until the first
             // compaction sets the cut to the k-th smallest logged D~ + 2E)
@@ -262,11 +273,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             int cnt = 0;
             bool ovf = false;
             for (int r = 0; r < R; ++r, ++rr) {
-                mbar_wait(&tmem_full, rr & 1u);
+                const uint32_t buf = rr & 1u, tcol = tcol0 + buf * 256u;
+                mbar_wait(&tmem_full[buf], (rr >> 1) & 1u);
                 tc_fence_after();
-                const float* lnr = a.ln + (size_t)r * kT3Rows;
+                const float* lnr = a.ln + (size_t)r * kT3N;
 #pragma unroll 1
-                for (int c0 = 0; c0 < kT3Rows; c0 += 32) {
+                for (int c0 = 0; c0 < kT3N; c0 += 32) {
                     uint32_t v0[32];
                     tmem_ld32_async(tcol + (uint32_t)c0, v0);
                     tmem_wait_ld();
@@ -282,14 +294,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                             }
                             if (cnt < kT3LogCap && v <= tcut) {
                                 lv[cnt * kT3Epi] = v;
-                                lj[cnt * kT3Epi] = (unsigned short)(r * kT3Rows + c0 + q);
+                                lj[cnt * kT3Epi] = (unsigned short)(r * kT3N + c0 + q);
                                 ++cnt;
                             }
                         }
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&tmem_empty);
+                mbar_arrive(&tmem_empty[buf]);
             }
             if (!valid) continue;
             // ---- refine and hand the candidates to the exact kernel ----
