@@ -1,0 +1,97 @@
+// esom_faithful.cuh -- the reference's scores and projection op for op
+// (SURVEY.md Appendix A.2/A.3), shared by the faithful kernels
+// (esom_kernels.cu: scores_kernel, project_kernel) and the fast projection
+// kernels' fallback for ill-conditioned systems (esom_project.cuh).
+#pragma once
+#include <stdint.h>
+
+#include "esom_common.cuh"
+
+namespace esom {
+
+// Scores (ref: projection.py:38-59).  numba's float(f32) stays f32, so the
+// root is sqrtf, widened; the rest is f64.  `exp` is CUDA's (<= 1 ulp from
+// glibc); everything else is correctly rounded like the reference.
+template <typename Get>
+__device__ __forceinline__ void score_row_dev(int k, Get sqd_at, double* out) {
+    double sigma = 0.0;
+    for (int t = 0; t < k; ++t) {
+        out[t] = (double)__fsqrt_rn(sqd_at(t));
+        sigma = __dadd_rn(sigma, out[t]);
+    }
+    sigma = __ddiv_rn(sigma, (double)k);
+    if (sigma < kScoreEps) {
+        for (int t = 0; t < k - 1; ++t) out[t] = 1.0;
+        out[k - 1] = 0.0;
+        return;
+    }
+    const double denom = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+    const double tail = exp(__ddiv_rn(-__dmul_rn(out[k - 1], out[k - 1]), denom));
+    for (int t = 0; t < k; ++t) {
+        const double v = __dsub_rn(exp(__ddiv_rn(-__dmul_rn(out[t], out[t]), denom)), tail);
+        out[t] = v > 0.0 ? v : 0.0;
+    }
+    if (out[0] < kScoreEps) {
+        for (int t = 0; t < k - 1; ++t) out[t] = 1.0;
+        out[k - 1] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Faithful projection (ref: projection.py:68-121), the mixed f32/f64 typing
+// of SURVEY Appendix A.3 with every operation separately rounded.
+// ---------------------------------------------------------------------------
+static __device__ __noinline__ void project_row_faithful(const float* __restrict__ x, const float* __restrict__ hi,
+                                     const float* __restrict__ lo, const int32_t* __restrict__ nbr,
+                                     const double* __restrict__ sc, int d, int k, float* out) {
+    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
+    for (int u = 0; u < k; ++u) {
+        const double su = sc[u];
+        if (su <= 0.0) continue;
+        const int ju = nbr[u];
+        const float* hu = hi + (int64_t)ju * d;
+        for (int v = u + 1; v < k; ++v) {
+            const double w = __dmul_rn(su, sc[v]);
+            if (w <= 0.0) continue;
+            const int jv = nbr[v];
+            const float* hv = hi + (int64_t)jv * d;
+            double hd2 = 0.0, dnum = 0.0;
+            for (int c = 0; c < d; ++c) {
+                const float lu = hu[c];
+                const float e = __fsub_rn(hv[c], lu);
+                hd2 = __dadd_rn(hd2, (double)__fmul_rn(e, e));
+                dnum = __dadd_rn(dnum, (double)__fmul_rn(__fsub_rn(x[c], lu), e));
+            }
+            if (hd2 < kPairEps) continue;
+            const float lux = lo[2 * ju], luy = lo[2 * ju + 1];
+            const float ex = __fsub_rn(lo[2 * jv], lux);
+            const float ey = __fsub_rn(lo[2 * jv + 1], luy);
+            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            if ((double)ld2 < kPairEps) continue;
+            const float g1 = __fdiv_rn(ex, ld2);
+            const float g2 = __fdiv_rn(ey, ld2);
+            const double h = __dadd_rn(__dadd_rn(__ddiv_rn(dnum, hd2), (double)__fmul_rn(g1, lux)),
+                                       (double)__fmul_rn(g2, luy));
+            const double G1 = g1, G2 = g2;
+            a11 = __dadd_rn(a11, __dmul_rn(__dmul_rn(w, G1), G1));
+            a12 = __dadd_rn(a12, __dmul_rn(__dmul_rn(w, G1), G2));
+            a22 = __dadd_rn(a22, __dmul_rn(__dmul_rn(w, G2), G2));
+            c1 = __dadd_rn(c1, __dmul_rn(__dmul_rn(w, h), G1));
+            c2 = __dadd_rn(c2, __dmul_rn(__dmul_rn(w, h), G2));
+        }
+    }
+    const double det = __dsub_rn(__dmul_rn(a11, a22), __dmul_rn(a12, a12));
+    const double tr = __dadd_rn(a11, a22);
+    if (det < __dadd_rn(__dmul_rn(__dmul_rn(kDetRel, tr), tr), kDetAbs)) {
+        const int nearest = nbr[0];
+        out[0] = lo[2 * nearest];
+        out[1] = lo[2 * nearest + 1];
+    } else {
+        out[0] = (float)__ddiv_rn(__dsub_rn(__dmul_rn(c1, a22), __dmul_rn(c2, a12)), det);
+        out[1] = (float)__ddiv_rn(__dsub_rn(__dmul_rn(a11, c2), __dmul_rn(a12, c1)), det);
+    }
+}
+
+
+
+}  // namespace esom

@@ -13,12 +13,14 @@
 //
 // Accuracy: the law of cosines has absolute error ~ u*sqrt(d)*(sqd_u+sqd_v)
 // in dnum; points whose kappa = max (sqd_u+sqd_v)*T_uv exceeds kKappaMax
-// (far outliers, where that error would matter) are redone with the exact
-// x-based f64 pair loop.  Checked against the reference to <= 1e-4 x extent.
+// recompute their k distances in f64 (precise_sqd), and the rare far
+// outliers and ill-conditioned systems run the reference's own arithmetic
+// (faithful_point).  Checked against the reference to <= 1e-4 x extent.
 #pragma once
 #include <stdlib.h>
 
 #include "esom_common.cuh"
+#include "esom_faithful.cuh"
 #include "esom_host.h"
 #include "esom_scan_args.h"
 
@@ -167,95 +169,15 @@ __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, 
     }
 }
 
-// f64 law-of-cosines accumulation over all pairs (fallback for ill-conditioned
-// f32 systems), same pair rules as the register kernels.
-static __device__ __noinline__ void pairs_cos_f64(int k, const int* J, const float* SQ, const float* SC, int st,
-                                                  const float2* __restrict__ LO, const float* __restrict__ T, int g,
-                                                  double* out5) {
-    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-    for (int u = 0; u < k; ++u) {
-        if (!(SC[u * st] > 0.0f)) continue;
-        for (int v = u + 1; v < k; ++v) {
-            const float w = SC[u * st] * SC[v * st];
-            if (!(w > 0.0f)) continue;
-            const int lo_j = min(J[u * st], J[v * st]), hi_j = max(J[u * st], J[v * st]);
-            const float tv = T[((lo_j * (2 * g - 1 - lo_j)) >> 1) + hi_j - lo_j - 1];
-            const float2 lu = LO[J[u * st]], lv = LO[J[v * st]];
-            const float ex = __fsub_rn(lv.x, lu.x), ey = __fsub_rn(lv.y, lu.y);
-            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-            if (!(tv >= 0.0f) || !(ld2 >= kLd2Min)) continue;
-            const double G1 = (double)ex / (double)ld2, G2 = (double)ey / (double)ld2;
-            const double h = 0.5 + ((double)SQ[u * st] - (double)SQ[v * st]) * (double)tv + G1 * (double)lu.x +
-                             G2 * (double)lu.y;
-            const double W = w;
-            a11 = fma(W * G1, G1, a11);
-            a12 = fma(W * G1, G2, a12);
-            a22 = fma(W * G2, G2, a22);
-            c1 = fma(W * h, G1, c1);
-            c2 = fma(W * h, G2, c2);
-        }
-    }
-    out5[0] = a11;
-    out5[1] = a12;
-    out5[2] = a22;
-    out5[3] = c1;
-    out5[4] = c2;
-}
-
-// The reference's scores exactly as it forms them (f32 sqrt widened, f64
-// sigma and exp; ref: projection.py:38-59), parked as f32 weights.  Used on
-// the rare f64 paths: for far outliers the reference's own d^2 != sqd rounding
-// is visible at the 1e-4 level in the weights.
-template <int KP>
-__device__ __forceinline__ void ref_scores_f64(int k, const float (&sq)[KP], float (&out)[KP]) {
-    double d[KP];
-    double sigma = 0.0, dk = 0.0;
-#pragma unroll
-    for (int q = 0; q < KP; ++q) {
-        d[q] = q < k ? (double)__fsqrt_rn(sq[q]) : 0.0;
-        sigma += d[q];
-        if (q == k - 1) dk = d[q];
-    }
-    sigma /= (double)k;
-    bool uniform = sigma < kScoreEps;
-    if (!uniform) {
-        const double inv = -1.0 / (2.0 * sigma * sigma);
-        const double tail = exp(dk * dk * inv);
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const double v = q < k ? exp(d[q] * d[q] * inv) - tail : 0.0;
-            out[q] = v > 0.0 ? (float)v : 0.0f;
-            if (q == 0) uniform = v < kScoreEps;
-        }
-    }
-    if (uniform) {
-#pragma unroll
-        for (int q = 0; q < KP; ++q) out[q] = q < k - 1 ? 1.0f : 0.0f;
-    }
-}
-
-// strided form (rows in shared memory, one column per thread)
-static __device__ __noinline__ void ref_scores_f64_strided(int k, const float* sq, int st, float* out, int ost) {
-    double sigma = 0.0, dk = 0.0;
-    for (int q = 0; q < k; ++q) {
-        const double dq = (double)__fsqrt_rn(sq[q * st]);
-        sigma += dq;
-        dk = dq;
-    }
-    sigma /= (double)k;
-    bool uniform = sigma < kScoreEps;
-    if (!uniform) {
-        const double inv = -1.0 / (2.0 * sigma * sigma);
-        const double tail = exp(dk * dk * inv);
-        for (int q = 0; q < k; ++q) {
-            const double dq = (double)__fsqrt_rn(sq[q * st]);
-            const double v = exp(dq * dq * inv) - tail;
-            out[q * ost] = v > 0.0 ? (float)v : 0.0f;
-            if (q == 0) uniform = v < kScoreEps;
-        }
-    }
-    if (uniform)
-        for (int q = 0; q < k; ++q) out[q * ost] = q < k - 1 ? 1.0f : 0.0f;
+// Ill-conditioned systems (tr^2 > kCondMax det: the solution amplifies every
+// rounding) and far outliers: the reference's own scores and projection op
+// for op (esom_faithful.cuh) -- bit-faithful given the scores, so even the
+// wild solutions of near-singular systems match (fuzz: kappa ~ 5e5).  Rare.
+static __device__ __noinline__ void faithful_point(const ProjArgs& a, int64_t i) {
+    double sc[64];
+    const float* row = a.sqd + i * a.k;
+    score_row_dev(a.k, [&](int t) { return __ldg(row + t); }, sc);
+    project_row_faithful(a.X + i * a.d, a.hi, a.lo, a.idx + i * a.k, sc, a.d, a.k, a.xy + 2 * i);
 }
 
 template <int KP>
@@ -265,9 +187,11 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
     // layout: lo [g] float2 | RB [g] int | J [KP][PT] int | S [KP][PT] f32 | Q, QB [KP][PT] f32 | (T table)
+    // 16-byte aligned regions (the T table below is copied with float4 stores;
+    // odd g used to misalign it: fuzz test)
     float2* LO = reinterpret_cast<float2*>(smem_raw);
-    int* RB = reinterpret_cast<int*>(LO + g);
-    int* J = RB + g;
+    int* RB = reinterpret_cast<int*>(smem_raw + (((size_t)g * 8 + 15) & ~(size_t)15));
+    int* J = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(RB) + (((size_t)g * 4 + 15) & ~(size_t)15));
     float* S = reinterpret_cast<float*>(J + KP * PT);
     float* Q = S + KP * PT;
     const float tmax_model = a.tmax ? __ldg(a.tmax) : 0.0f;
@@ -379,17 +303,8 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
         const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
         if (far || illc) {
-            double o5[5];
-            ref_scores_f64_strided(k, drow, 1, S + tid, PT);  // the reference's f64 scores from its own sq
-            if (far)
-                pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, J + tid, S + tid, PT, o5);
-            else
-                pairs_cos_f64(k, J + tid, Q + tid, S + tid, PT, LO, Ts, g, o5);
-            A11 = o5[0];
-            A12 = o5[1];
-            A22 = o5[2];
-            C1 = o5[3] - (o5[0] * (double)o.x + o5[1] * (double)o.y);
-            C2 = o5[4] - (o5[1] * (double)o.x + o5[2] * (double)o.y);
+            faithful_point(a, i);
+            continue;
         }
         const double det = A11 * A22 - A12 * A12;
         const double tr = A11 + A22;
@@ -618,7 +533,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         } else {
 #pragma unroll
             for (int q = 0; q < KP; ++q) {
-                jj[q] = q < k ? __ldg(irow + q) : q;  // padding slots: distinct dummy landmarks, zero weight
+                jj[q] = q < k ? __ldg(irow + q) : q % g;  // padding slots: valid dummy landmarks, zero weight
                 sq[q] = q < k ? __ldg(drow + q) : 0.0f;
             }
         }
@@ -750,27 +665,8 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
         const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
         if (far || illc) {
-            double o5[5];
-            float fsc[KP], rsq[KP];  // the reference's sq, re-read (keeps sq dead across the pair loop)
-#pragma unroll
-            for (int q = 0; q < KP; ++q) rsq[q] = q < k ? __ldg(a.sqd + i * k + q) : 0.0f;
-            ref_scores_f64<KP>(k, rsq, fsc);
-            if (far) {
-                // far outlier: exact x-based f64 pair loop (absolute layout coordinates)
-                pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, fsc, 1, o5);
-                // shift to the local origin: c -= A o
-                o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
-                o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
-            } else {
-                pairs_cos_f64(k, jj, qe, fsc, 1, LO, T, g, o5);
-                o5[3] -= o5[0] * (double)o.x + o5[1] * (double)o.y;
-                o5[4] -= o5[1] * (double)o.x + o5[2] * (double)o.y;
-            }
-            A11 = o5[0];
-            A12 = o5[1];
-            A22 = o5[2];
-            C1 = o5[3];
-            C2 = o5[4];
+            faithful_point(a, i);
+            continue;
         }
         const double det = A11 * A22 - A12 * A12;
         const double tr = A11 + A22;
@@ -814,40 +710,8 @@ __global__ void pair_record_kernel(const float* __restrict__ T, const float* __r
     }
 }
 
-// f64 pair accumulation from the records (ill-conditioned f32 systems)
-static __device__ __noinline__ void pairs_rec_f64(int k, const int* J, const float* SQ, const float* SC,
-                                                  const float4* __restrict__ rec, const float* __restrict__ lo, int g,
-                                                  double* out5) {
-    double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-    for (int u = 0; u < k; ++u) {
-        if (!(SC[u] > 0.0f)) continue;
-        for (int v = u + 1; v < k; ++v) {
-            const float w = SC[u] * SC[v];
-            if (!(w > 0.0f)) continue;
-            const float4 r = __ldg(rec + (int64_t)J[u] * g + J[v]);
-            if (!(r.x >= 0.0f)) continue;
-            const float ex = __fsub_rn(lo[2 * J[v]], lo[2 * J[u]]), ey = __fsub_rn(lo[2 * J[v] + 1], lo[2 * J[u] + 1]);
-            const double ld2 = (double)__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-            const double G1 = (double)ex / ld2, G2 = (double)ey / ld2;
-            const double h = 0.5 + ((double)SQ[u] - (double)SQ[v]) * (double)r.x + G1 * (double)lo[2 * J[u]] +
-                             G2 * (double)lo[2 * J[u] + 1];
-            const double W = w;
-            a11 = fma(W * G1, G1, a11);
-            a12 = fma(W * G1, G2, a12);
-            a22 = fma(W * G2, G2, a22);
-            c1 = fma(W * h, G1, c1);
-            c2 = fma(W * h, G2, c2);
-        }
-    }
-    out5[0] = a11;
-    out5[1] = a12;
-    out5[2] = a22;
-    out5[3] = c1;
-    out5[4] = c2;
-}
-
 template <int KP>
-__global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
+__global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a) {
     constexpr int PT = kRegThreads;
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
@@ -976,20 +840,8 @@ __global__ void __launch_bounds__(kRegThreads) project_reg3_kernel(ProjArgs a) {
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
         const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
         if (far || illc) {
-            double o5[5];
-            float fsc[KP], rsq[KP];  // the reference's sq, re-read (keeps sq dead across the pair loop)
-#pragma unroll
-            for (int q = 0; q < KP; ++q) rsq[q] = q < k ? __ldg(a.sqd + i * k + q) : 0.0f;
-            ref_scores_f64<KP>(k, rsq, fsc);
-            if (far)
-                pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, fsc, 1, o5);
-            else
-                pairs_rec_f64(k, jj, qe, fsc, rec, a.lo, g, o5);
-            A11 = o5[0];
-            A12 = o5[1];
-            A22 = o5[2];
-            C1 = o5[3];
-            C2 = o5[4];
+            faithful_point(a, i);
+            continue;
         }
         const double det = A11 * A22 - A12 * A12;
         const double tr = A11 + A22;
