@@ -899,7 +899,10 @@ int launch_tc2_w(Tc2Args a, int W, cudaStream_t st) {
 // pipelined screen (esom_tc2.cuh); ESOM_ERR_UNSUPPORTED when the shape does not fit
 int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st) {
     const int W = tc2_warpgroups();
-    if (W <= 0 || !m.ls || p.kp > 16) return ESOM_ERR_UNSUPPORTED;
+    // the non-empty-word mask of the candidate bitmaps is one 32-bit word:
+    // gpad <= 1024 (larger g: the round-streaming esom_tc.cuh screen; the
+    // randomised parity test caught the fused kernel being picked at g = 1500)
+    if (W <= 0 || !m.ls || p.kp > 16 || m.gpad > 1024) return ESOM_ERR_UNSUPPORTED;
     Tc2Args a{};
     a.X = s.X;
     a.n = s.n;

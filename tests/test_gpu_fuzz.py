@@ -15,10 +15,11 @@ pytestmark = pytest.mark.gpu
 def _shapes():
     gen = np.random.default_rng(20261017)
     out = []
-    for _ in range(24):
-        d = int(gen.choice([1, 2, 3, 5, 8, 13, 16, 24, 31, 32, 33, 40, 64, 96]))
-        g = int(gen.choice([4, 9, 31, 33, 64, 100, 255, 256, 257, 300, 513, 1000, 1024]))
-        k = int(gen.choice([3, 4, 5, 8, 12, 16, 20, 32]))
+    for t in range(48):
+        d = int(gen.choice([1, 2, 3, 5, 8, 13, 16, 24, 31, 32, 33, 40, 64, 96, 130]))
+        g = int(gen.choice([4, 9, 31, 33, 64, 100, 255, 256, 257, 300, 513, 1000, 1024]
+                           + ([1500, 2048, 4097] if t >= 24 else [])))
+        k = int(gen.choice([3, 4, 5, 8, 12, 16, 20, 32, 48, 64]))
         k = min(k, g)
         n = int(gen.choice([1, 7, 100, 1500, 5000, 20000]))
         out.append((n, d, g, k, int(gen.integers(1 << 30))))
