@@ -45,3 +45,39 @@ def test_fuzz_knn_and_embed(n, d, g, k, seed):
         ref = oracle.embed(pts, hi, lo, k, threads=oracle.host_cores())
         ext = float(np.ptp(lo, axis=0).max())
         assert np.abs(xy - ref).max() <= 1e-4 * ext, (n, d, g, k)
+
+
+def _train_shapes():
+    gen = np.random.default_rng(777)
+    out = []
+    for _ in range(16):
+        d = int(gen.choice([1, 3, 8, 17, 32, 33, 64, 65, 100]))
+        g = int(gen.choice([4, 7, 36, 64, 200, 256, 257, 700, 1024, 2000]))
+        B = int(gen.choice([1, 2, 63, 64, 65, 200, 256, 300]))
+        out.append((d, g, B, int(gen.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("d,g,B,seed", _train_shapes())
+def test_fuzz_trainers(d, g, B, seed):
+    """Online SOM / k-means ticks (every on-chip / global kernel variant the
+    shape selects) and the batch-SOM step against the C restatements."""
+    from paper_2201_00701_b200.core import Rng
+
+    gen = np.random.default_rng(seed)
+    n = 5000
+    centers = gen.uniform(0, 10, size=(5, d))
+    pts = (centers[gen.integers(0, 5, n)] + gen.normal(0, 0.5, size=(n, d))).astype(np.float32)
+    hi = pts[gen.choice(n, g, replace=g > n)].copy()
+    lo = gen.uniform(0, 6, size=(g, 2)).astype(np.float32)
+    model = esom.LandmarkModel.create(hi, lo)
+    X = torch.from_numpy(pts).cuda()
+    got = esom.som_tick(X, model, esom.SomConfig(sigma=0.9, alpha=0.3, batch_size=B), Rng(seed)).cpu().numpy()
+    want = oracle.som_tick(pts, hi, lo, Rng(seed).integers(0, n, size=B), 0.9, 0.3)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5, err_msg=f"som {d} {g} {B}")
+    got = esom.kmeans_tick(X, model, esom.KmeansConfig(alpha_km=0.2, batch_size=B), Rng(seed + 1)).cpu().numpy()
+    want = oracle.kmeans_tick(pts, hi, Rng(seed + 1).integers(0, n, size=B), 0.2)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5, err_msg=f"kmeans {d} {g} {B}")
+    got = esom.batch_som_step(X, model, esom.BatchSomConfig(sigma=1.1, alpha=0.2)).cpu().numpy()
+    want = oracle.batch_som_step(pts, hi, lo, 1.1, 0.2)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5, err_msg=f"batch {d} {g}")
