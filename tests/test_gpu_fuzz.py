@@ -81,3 +81,42 @@ def test_fuzz_trainers(d, g, B, seed):
     got = esom.batch_som_step(X, model, esom.BatchSomConfig(sigma=1.1, alpha=0.2)).cpu().numpy()
     want = oracle.batch_som_step(pts, hi, lo, 1.1, 0.2)
     np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5, err_msg=f"batch {d} {g}")
+
+
+def _api_shapes():
+    gen = np.random.default_rng(4242)
+    out = []
+    for _ in range(14):
+        d = int(gen.choice([1, 2, 7, 32, 50, 200]))
+        g = int(gen.choice([1, 2, 5, 65, 130, 300, 1100]))
+        k = int(gen.choice([1, 2, 3, 17, 65, 100]))
+        k = max(1, min(k, g))
+        n = int(gen.choice([0, 1, 3, 999, 4097]))
+        out.append((n, d, g, k, int(gen.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("n,d,g,k,seed", _api_shapes())
+def test_fuzz_api_paths(n, d, g, k, seed):
+    """knn / knn_bitonic / project_neighbors / chunked embed on odd shapes
+    (k > 64 sort path, k < 3, g = 1, n = 0, float64 and strided inputs)."""
+    gen = np.random.default_rng(seed)
+    pts64 = gen.normal(0, 3, size=(n, d))
+    pts = pts64.astype(np.float32)
+    hi = gen.normal(0, 3, size=(g, d)).astype(np.float32)
+    lo = gen.uniform(0, 5, size=(g, 2)).astype(np.float32)
+    nb = esom.knn(pts64, hi, k, backend="base")  # float64 in: coerced like the reference
+    wi, wd = oracle.knn(pts, hi, k) if n else (np.zeros((0, k), np.int32), np.zeros((0, k), np.float32))
+    assert np.array_equal(nb.indices, wi) and np.array_equal(nb.sqdists, wd)
+    if k in (4, 8, 16, 32, 64):
+        nb2 = esom.knn_bitonic(np.asfortranarray(pts), hi, k)  # strided input
+        assert np.array_equal(nb2.indices, wi) and np.array_equal(nb2.sqdists, wd)
+    if k >= 3 and n:
+        model = esom.LandmarkModel.create(hi, lo)
+        xy = esom.project_neighbors(pts, model, nb)
+        ref = oracle.project(pts, hi, lo, wi, oracle.scores(wd))
+        ext = max(float(np.ptp(lo, axis=0).max()), 1e-30)
+        assert np.abs(xy - ref).max() <= 1e-4 * ext
+        full = esom.embed(pts, model, esom.EmbedParams(k=k), backend="base")
+        chunked = esom.embed(pts, model, esom.EmbedParams(k=k), backend="base", chunk_size=max(1, n // 3))
+        assert np.array_equal(full, chunked)  # chunk invariance (ref: tests:test_projection.py:217-223)
