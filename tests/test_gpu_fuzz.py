@@ -120,3 +120,70 @@ def test_fuzz_api_paths(n, d, g, k, seed):
         full = esom.embed(pts, model, esom.EmbedParams(k=k), backend="base")
         chunked = esom.embed(pts, model, esom.EmbedParams(k=k), backend="base", chunk_size=max(1, n // 3))
         assert np.array_equal(full, chunked)  # chunk invariance (ref: tests:test_projection.py:217-223)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_formats_and_landmark_ops(seed):
+    """FCS images (random n, d, byte order, header/TEXT offsets), transforms,
+    colours, frame records, graph + layout + fit_hi on random inputs vs the
+    numpy restatements (oracle/formats.py)."""
+
+    from oracle import formats as F
+    from paper_2201_00701_b200.engine import DeviceSession
+    from paper_2201_00701_b200.io import TransformSpec, apply_transform, parse_fcs
+
+    gen = np.random.default_rng(9000 + seed)
+    n, d = int(gen.integers(1, 3000)), int(gen.integers(1, 40))
+    pts = (gen.normal(0, 1, size=(n, d)) * gen.uniform(0.1, 100, size=d)).astype(np.float32)
+    big = bool(gen.integers(2))
+    text_offsets = bool(gen.integers(2))
+    kws = [("$PAR", str(d)), ("$TOT", str(n)), ("$DATATYPE", "F"), ("$BYTEORD", "4,3,2,1" if big else "1,2,3,4"),
+           ("$MODE", "L")] + [(f"$P{i + 1}B", "32") for i in range(d)] + [(f"$P{i + 1}N", f"c/{i}") for i in range(d)]
+    pad = int(gen.integers(0, 7))  # unaligned DATA offsets
+    def text(b0, b1):
+        extra = [("$BEGINDATA", f"{b0:010d}"), ("$ENDDATA", f"{b1:010d}")] if text_offsets else []
+        return b"/" + b"".join(k.encode().replace(b"/", b"//") + b"/" + v.encode().replace(b"/", b"//") + b"/"
+                               for k, v in kws + extra)
+    t = text(0, 0)
+    d0 = 58 + len(t) + pad
+    d1 = d0 + 4 * n * d - 1
+    t = text(d0, d1)
+    hdr = (b"FCS3.1    " + b"".join(f"{v:>8d}".encode() for v in
+                                      (58, 58 + len(t) - 1, 0 if text_offsets else d0, 0 if text_offsets else d1, 0, 0)))
+    raw = hdr + t + b"\0" * pad + pts.astype(">f4" if big else "<f4").tobytes()
+    ds = parse_fcs(raw)
+    assert np.array_equal(ds.points.cpu().numpy(), pts)
+    assert ds.dim_names == tuple(f"c/{i}" for i in range(d))
+    spec = tuple(gen.choice(["none", "minmax", "zscore"]) for _ in range(d))
+    out = apply_transform(ds, TransformSpec(entries=spec)).points.cpu().numpy()
+    st = ds.dim_stats
+    want = F.apply_transform(pts, spec, (st.min, st.max, st.mean, st.sd))
+    assert np.array_equal(out, want)  # bit-exact given the statistics
+    sess = DeviceSession(pts)
+    c = int(gen.integers(d))
+    assert np.array_equal(sess.colors(c).cpu().numpy(), F.color_channel(pts, pts.min(0), pts.max(0), c))
+    xy = gen.normal(0, 5, size=(n, 2)).astype(np.float32)
+    sess.positions.copy_(torch.from_numpy(xy))
+    fid = int(gen.integers(0, 2**32))
+    assert bytes(sess.frame_record(fid, c)) == F.frame_points_record(fid, xy, sess.colors(c).cpu().numpy())
+    # landmark-side ops
+    g = int(gen.integers(5, 300))
+    hi = gen.normal(0, 2, size=(g, d)).astype(np.float32)
+    lo = gen.uniform(0, 6, size=(g, 2)).astype(np.float32)
+    kg = int(gen.integers(1, min(8, g - 1) + 1))
+    e = esom.build_knn_graph(hi, kg)
+    from paper_2201_00701_b200.graphmodel import symmetrize_neighbors
+    wi, wd = oracle.knn(hi, hi, kg + 1)
+    e2 = symmetrize_neighbors(wi, wd, kg)
+    assert np.array_equal(e.pairs, e2.pairs) and np.array_equal(e.rest, e2.rest)
+    lay = esom.LayoutState(velocities=gen.normal(0, 0.1, size=(g, 2)))
+    pinned = sorted(set(gen.integers(0, g, size=3).tolist()))
+    new_lo, vel = esom.layout_tick(lo, e, lay, pinned)
+    wlo, wvel = F.layout_tick(lo, e.pairs, e.rest, lay.velocities, lay.stiffness, lay.repulsion, 1e-3, lay.damping,
+                              lay.dt, pinned)
+    np.testing.assert_allclose(vel, wvel, rtol=1e-9, atol=1e-12)
+    assert np.max(np.abs(new_lo - wlo)) <= 1e-5
+    model = esom.LandmarkModel.create(hi, lo)
+    p = gen.uniform(-1, 7, size=2)
+    np.testing.assert_allclose(esom.fit_hi_for_new_landmark(p, model), F.fit_hi_for_new_landmark(p, hi, lo),
+                               rtol=1e-6, atol=1e-6)
