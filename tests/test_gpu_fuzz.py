@@ -187,3 +187,18 @@ def test_fuzz_formats_and_landmark_ops(seed):
     p = gen.uniform(-1, 7, size=2)
     np.testing.assert_allclose(esom.fit_hi_for_new_landmark(p, model), F.fit_hi_for_new_landmark(p, hi, lo),
                                rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("n,d,g,k", [((1 << 20) + 77, 32, 300, 16), ((1 << 18) + 123, 40, 600, 20),
+                                     ((1 << 18) + 1, 130, 257, 32)])
+def test_chunk_boundaries_vs_scan(n, d, g, k, monkeypatch):
+    """Screens that work in chunks (split tc2: 2^20 points; GEMM screen: <= 2^18)
+    with a ragged last chunk, bit-exact against the CUDA-core scan."""
+    gen = np.random.default_rng(n + d)
+    centers = gen.uniform(0, 10, size=(8, d)).astype(np.float32)
+    X = torch.from_numpy(centers[gen.integers(0, 8, n)] + gen.normal(0, 0.5, size=(n, d)).astype(np.float32)).cuda()
+    H = torch.from_numpy(centers[gen.integers(0, 8, g)] + gen.normal(0, 0.7, size=(g, d)).astype(np.float32)).cuda()
+    a = esom.knn_base(X, H, k)
+    monkeypatch.setenv("ESOM_TC", "0")
+    b = esom.knn_base(X, H, k)
+    assert torch.equal(a.indices, b.indices) and torch.equal(a.sqdists, b.sqdists)
