@@ -88,6 +88,13 @@ def color_channel(dataset, color_dim: int):
     return out if _dev.is_device_tensor(pts) else out.cpu().numpy()
 
 
+class _TrainModel:
+    """hi (host or device) + lo, the two fields the trainers read."""
+
+    def __init__(self, hi, lo):
+        self.hi, self.lo = hi, lo
+
+
 class _DeviceDataset:
     """Duck-typed dataset whose points are the session's device matrix."""
 
@@ -252,6 +259,8 @@ class FrameEngine:
     km_cfg: KmeansConfig = field(default_factory=KmeansConfig)
     training_paused: bool = False
 
+    pipelined: bool = True
+
     def __post_init__(self):
         if self.mode not in (MODE_SOM, MODE_GRAPH):
             raise ParameterError(f"unknown mode {self.mode!r}")
@@ -260,23 +269,72 @@ class FrameEngine:
                                  "with gpu_tick installed")
         self.rng = Rng(self.seed)
         self.session = DeviceSession(self.dataset)
-        self.model = init_model(self.session.X, self.rng, self.grid, self.random_g)
-        self.embed_params = EmbedParams(k=_nearest_pow2_k(self.k, self.model.g))
+        self._model = init_model(self.session.X, self.rng, self.grid, self.random_g)
+        self.embed_params = EmbedParams(k=_nearest_pow2_k(self.k, self._model.g))
         self.frame_id = 0
-        self._hi_dev = None
+        self._hi_dev = None   # device hi after the last training tick
+        self._stale = False   # _model.hi lags _hi_dev
+        self._spec = None     # speculative next tick (key, hi, done event, rng state)
+        self._side = torch.cuda.Stream(self.session.device) if self.pipelined else None
+
+    # the reference-facing model (numpy hi materialised on demand: one sync)
+    @property
+    def model(self) -> LandmarkModel:
+        if self._stale:
+            self._model = self._model.with_hi(self._hi_dev.cpu().numpy())
+            self._stale = False
+        return self._model
+
+    @model.setter
+    def model(self, m: LandmarkModel) -> None:
+        self._drop_spec()
+        self._model, self._hi_dev, self._stale = m, None, False
+
+    def _train_input(self):
+        hi = self._hi_dev if self._hi_dev is not None else self._model.hi
+        return _TrainModel(hi, self._model.lo)
+
+    def _drop_spec(self) -> None:
+        """Discard a speculative tick: wait for it, rewind the Rng to before its draw."""
+        if self._spec is not None:
+            _, _, done, state = self._spec
+            done.synchronize()
+            self.rng._gen.bit_generator.state = state
+            self._spec = None
 
     def tick(self) -> DeviceFrame:
         s = self.session
         if not self.training_paused:
-            trainer = MODE_SOM if self.mode == MODE_SOM else "kmeans"
-            cfg = self.som_cfg if self.mode == MODE_SOM else self.km_cfg
-            self._hi_dev = s.train(trainer, self.model, cfg, self.rng)
-            self.model = self.model.with_hi(self._hi_dev.cpu().numpy())
-        hi = self._hi_dev if self._hi_dev is not None else self.model.hi
-        s.embed(hi, self.model.lo, self.embed_params, self.backend)
+            hi_new = None
+            spec = self._spec
+            key = spec[0] if spec is not None else None
+            if key is not None and key[0] is self._hi_dev and key[1] == self.som_cfg and key[2] is self._model.lo:
+                self._spec = None
+                torch.cuda.current_stream(s.device).wait_event(spec[2])
+                hi_new = spec[1]
+            else:
+                self._drop_spec()
+                hi_new = s.train(MODE_SOM, self._train_input(), self.som_cfg, self.rng)
+            self._hi_dev, self._stale = hi_new, True
+        hi = self._hi_dev if self._hi_dev is not None else self._model.hi
+        s.embed(hi, self._model.lo, self.embed_params, self.backend)
+        if self._side is not None and not self.training_paused and self._spec is None:
+            # the next tick's training depends only on this tick's hi: run it on a
+            # side stream (one SM cluster) while the embed fills the GPU; same draws,
+            # same order, rewound if anything changes before it is consumed
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(s.device))
+            state = self.rng._gen.bit_generator.state
+            with torch.cuda.stream(self._side):
+                self._side.wait_event(ready)
+                nxt = s.train(MODE_SOM, self._train_input(), self.som_cfg, self.rng)
+                done = torch.cuda.Event()
+                done.record(self._side)
+            nxt.record_stream(torch.cuda.current_stream(s.device))
+            self._spec = ((self._hi_dev, self.som_cfg, self._model.lo), nxt, done, state)
         self.frame_id += 1
-        return DeviceFrame(frame_id=self.frame_id, positions=s.positions, landmarks_lo=self.model.lo,
-                           landmark_ids=self.model.ids, colors=s.colors(self.color_dim))
+        return DeviceFrame(frame_id=self.frame_id, positions=s.positions, landmarks_lo=self._model.lo,
+                           landmark_ids=self._model.ids, colors=s.colors(self.color_dim))
 
     def frame_record(self) -> memoryview:
         """Wire bytes of the last frame (protocol.encode(FramePoints(...)))."""

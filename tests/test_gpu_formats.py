@@ -294,3 +294,20 @@ def test_session_switches_to_bmu_order_on_trained_models():
     fresh.tick()
     fresh.tick()
     assert not fresh.session.bmu_order  # untrained model: natural order, no sort
+
+
+def test_frame_engine_pipelined_equals_sequential():
+    """The speculative next-tick training on a side stream produces the same
+    landmarks, positions and Rng stream as the sequential tick, also across a
+    config change (the speculation is rewound)."""
+    import dataclasses
+
+    pts = datagen.gaussians(16, 1 << 15, 32, seed=3)[0].astype(np.float32)
+    a = FrameEngine(pts, seed=5, k=16, grid=(8, 8), pipelined=True)
+    b = FrameEngine(pts, seed=5, k=16, grid=(8, 8), pipelined=False)
+    for t in range(6):
+        if t == 3:  # change the trainer config between ticks: the speculation must be discarded
+            a.som_cfg = b.som_cfg = dataclasses.replace(a.som_cfg, alpha=0.3)
+        fa, fb = a.tick(), b.tick()
+        assert torch.equal(fa.positions, fb.positions), t
+        assert np.array_equal(a.model.hi, b.model.hi), t
