@@ -354,6 +354,23 @@ def _session(engine) -> DeviceSession:
     return sess
 
 
+def _spec_key(st, som: bool, sess) -> tuple:
+    """What a speculative tick depended on: the hi array (and lo for SOM), the
+    config, the mode and the dataset (compared by identity / equality)."""
+    return (st.model.hi, st.model.lo if som else None, st.som_cfg if som else st.km_cfg, som, sess)
+
+
+def _same_key(a, b) -> bool:
+    return (a[0] is b[0] and a[1] is b[1] and a[2] == b[2] and a[3] == b[3] and a[4] is b[4])
+
+
+def _rewind_spec(engine, spec) -> None:
+    spec[2].synchronize()
+    engine.state.rng._gen.bit_generator.state = spec[3]
+    engine._b200_spec = None
+    return None
+
+
 def gpu_tick(self):
     """``Engine.tick`` with the dataset resident in HBM and a FULL
     re-projection every frame (ref: engine.py:347-399).  Command handling,
@@ -362,6 +379,9 @@ def gpu_tick(self):
     round-robin instead."""
     mod = sys.modules[type(self).__module__]
     st = self.state
+    spec = getattr(self, "_b200_spec", None)
+    if spec is not None and self._queue:
+        spec = _rewind_spec(self, spec)  # commands may draw from st.rng: restore the draw order first
     for cmd in self._queue:
         try:
             self.apply_command(cmd)
@@ -370,12 +390,34 @@ def gpu_tick(self):
     self._queue.clear()
 
     sess = _session(self)
+    som = st.mode == mod.MODE_SOM
     if not st.training_paused:
-        if st.mode == mod.MODE_SOM:
-            hi = sess.train(MODE_SOM, st.model, st.som_cfg, st.rng)
+        if spec is not None and _same_key(spec[0], _spec_key(st, som, sess)):
+            self._b200_spec = None
+            torch.cuda.current_stream(sess.device).wait_event(spec[2])
+            hi = spec[1]
         else:
-            hi = sess.train("kmeans", st.model, st.km_cfg, st.rng)
+            if spec is not None:
+                _rewind_spec(self, spec)
+            hi = sess.train(MODE_SOM if som else "kmeans", st.model, st.som_cfg if som else st.km_cfg, st.rng)
         st.model = st.model.with_hi(hi.cpu().numpy())
+        if getattr(self, "pipelined", True):
+            # the next tick's training needs only this hi: run it on a side stream
+            # during this frame's embed (rewound if a command or change intervenes)
+            side = getattr(self, "_b200_side", None)
+            if side is None:
+                side = self._b200_side = torch.cuda.Stream(sess.device)
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(sess.device))
+            state = st.rng._gen.bit_generator.state
+            with torch.cuda.stream(side):
+                side.wait_event(ready)
+                nxt = sess.train(MODE_SOM if som else "kmeans", _TrainModel(hi, st.model.lo),
+                                 st.som_cfg if som else st.km_cfg, st.rng)
+                done = torch.cuda.Event()
+                done.record(side)
+            nxt.record_stream(torch.cuda.current_stream(sess.device))
+            self._b200_spec = (_spec_key(st, som, sess), nxt, done, state)
 
     if st.mode == mod.MODE_GRAPH:
         if self._edges_dirty or self._ticks_since_rebuild >= mod.graphmodel.REBUILD_CADENCE:

@@ -311,3 +311,27 @@ def test_frame_engine_pipelined_equals_sequential():
         fa, fb = a.tick(), b.tick()
         assert torch.equal(fa.positions, fb.positions), t
         assert np.array_equal(a.model.hi, b.model.hi), t
+
+
+def test_installed_gpu_tick_pipelined_equals_sequential():
+    """Installed Engine.tick with the speculative next-tick training: commands
+    that draw from the session Rng and config changes between ticks rewind it,
+    so frames equal the sequential tick's."""
+    import dataclasses
+
+    pts = datagen.extruded_s(4000, seed=11)
+    engines = [_fake_reference_engine(pts, 21, (6, 6), 16) for _ in range(2)]
+    engines[1].pipelined = False
+    for e in engines:  # a command that consumes the session Rng (like DuplicateLandmark)
+        type(e).apply_command = lambda self, c: self.state.rng.uniform(0.0, 1.0)
+    outs = [[], []]
+    for t in range(6):
+        for i, e in enumerate(engines):
+            if t == 2:
+                e._queue.append("draw")
+            if t == 4:
+                e.state.som_cfg = dataclasses.replace(e.state.som_cfg, sigma=0.7)
+            p = e.tick()
+            outs[i].append((p.positions.copy(), e.state.model.hi.copy()))
+    for (pa, ha), (pb, hb) in zip(*outs):
+        assert np.array_equal(pa, pb) and np.array_equal(ha, hb)
