@@ -202,3 +202,27 @@ def test_chunk_boundaries_vs_scan(n, d, g, k, monkeypatch):
     monkeypatch.setenv("ESOM_TC", "0")
     b = esom.knn_base(X, H, k)
     assert torch.equal(a.indices, b.indices) and torch.equal(a.sqdists, b.sqdists)
+
+
+@pytest.mark.parametrize("n,d,g,k,seed", [(3000, 5, 40, 8, 1), (50000, 32, 256, 16, 2), (20000, 32, 1024, 16, 3),
+                                          (8000, 48, 300, 32, 4), (4097, 2, 9, 4, 5), (12000, 70, 100, 16, 6)])
+def test_fuzz_frame_loop(n, d, g, k, seed):
+    """Batch-SOM FrameLoop (fused embed + statistics via the shared-memory or
+    sorted-segment kernel + update + re-preparation) for two frames vs the C
+    restatements: positions of each frame under that frame's model, hi after."""
+    from paper_2201_00701_b200.batch_som import BatchSomConfig, FrameLoop
+
+    gen = np.random.default_rng(seed)
+    centers = gen.uniform(0, 10, size=(6, d))
+    pts = (centers[gen.integers(0, 6, n)] + gen.normal(0, 0.5, size=(n, d))).astype(np.float32)
+    hi = pts[gen.choice(n, g, replace=False)].copy()
+    lo = gen.uniform(0, 6, size=(g, 2)).astype(np.float32)
+    loop = FrameLoop(torch.from_numpy(pts).cuda(), hi, lo, k, BatchSomConfig(sigma=1.0, alpha=0.1))
+    ext = float(np.ptp(lo, axis=0).max())
+    h = hi
+    for _ in range(2):
+        xy = loop.frame().cpu().numpy()
+        ref = oracle.embed(pts, h, lo, k, threads=oracle.host_cores())
+        assert np.abs(xy - ref).max() <= 1e-4 * ext
+        h = oracle.batch_som_step(pts, h, lo, 1.0, 0.1)
+        np.testing.assert_allclose(loop.model.hi.cpu().numpy(), h, rtol=1e-5, atol=1e-5)
