@@ -186,6 +186,43 @@ __global__ void pair_table_kernel(const float* __restrict__ hi, int g, int d, fl
     if ((threadIdx.x & 31) == 0 && tm > 0.0f) atomicMax(reinterpret_cast<int*>(tmax), __float_as_int(tm));
 }
 
+
+// Tiled form for d <= 64: a 32 x 32 block of (u, v) pairs stages its 64 rows in
+// shared memory once (the row-per-pair kernel above re-reads 2 d floats per
+// pair from L1/L2).  Same per-pair arithmetic and order -> identical table.
+constexpr int kPairTile = 32;
+
+__global__ void __launch_bounds__(256) pair_table_tiled_kernel(const float* __restrict__ hi, int g, int d,
+                                                               float* __restrict__ T, float* __restrict__ tmax) {
+    __shared__ float Ru[kPairTile][65], Rv[kPairTile][65];
+    const int tu = blockIdx.y, tv = blockIdx.x;
+    if (tv < tu) return;  // upper triangle of tiles
+    const int u0 = tu * kPairTile, v0 = tv * kPairTile;
+    for (int e = threadIdx.x; e < kPairTile * d; e += blockDim.x) {
+        const int r = e / d, c = e % d;
+        Ru[r][c] = u0 + r < g ? hi[(int64_t)(u0 + r) * d + c] : 0.0f;
+        Rv[r][c] = v0 + r < g ? hi[(int64_t)(v0 + r) * d + c] : 0.0f;
+    }
+    __syncthreads();
+    float tm = 0.0f;
+    for (int e = threadIdx.x; e < kPairTile * kPairTile; e += blockDim.x) {
+        const int ru = e / kPairTile, rv = e % kPairTile;  // lanes walk v: conflict-free rows (stride 65)
+        const int u = u0 + ru, v = v0 + rv;
+        if (u >= g || v >= g || v <= u) continue;
+        double hd2 = 0.0;
+        for (int c = 0; c < d; ++c) {
+            const float df = __fsub_rn(Rv[rv][c], Ru[ru][c]);
+            hd2 = __dadd_rn(hd2, (double)__fmul_rn(df, df));
+        }
+        const float t = hd2 < kPairEps ? -1.0f : (float)(0.5 / hd2);
+        T[(int64_t)u * (2 * (int64_t)g - u - 1) / 2 + (v - u - 1)] = t;
+        tm = fmaxf(tm, t);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+    if ((threadIdx.x & 31) == 0 && tm > 0.0f) atomicMax(reinterpret_cast<int*>(tmax), __float_as_int(tm));
+}
+
 // Landmark centroid c (f64 mean, rounded to f32; dims >= d are 0): the
 // tensor-core screens work on x - c and l - c, whose norms (and so the error
 // bounds) are several times smaller than those of x and l.
@@ -1268,7 +1305,12 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     if (int e = cuda_check("pack_landmarks")) return e;
     float* tmax = reinterpret_cast<float*>(ws + m.lstats) + 2;
     cudaMemsetAsync(tmax, 0, 4, stream);
-    pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T, tmax);
+    if (d <= 64 && !getenv("ESOM_PAIR_V1")) {
+        const int nt = (g + kPairTile - 1) / kPairTile;
+        pair_table_tiled_kernel<<<dim3(nt, nt), 256, 0, stream>>>(hi, g, d, T, tmax);
+    } else {
+        pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T, tmax);
+    }
     if (int e = cuda_check("pair_table")) return e;
     if (tc_eligible(1 << 20, d, g, k))
         if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
