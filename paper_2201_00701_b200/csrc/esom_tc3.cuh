@@ -545,9 +545,9 @@ __global__ void __launch_bounds__(kT3ExactWarps * 32) knn_exact_warp_kernel(T3Ex
 // read once per group, 8 sequential f32 chains per landmark).  U contains
 // every point's true top k, so the top k of U by (distance, index) is exact.
 // ---------------------------------------------------------------------------
-constexpr int kT3GP = 8;       // points per warp group
+constexpr int kT3GP = 4;       // points per warp group
 constexpr int kT3UMax = 96;    // union capacity (three landmark slots per lane)
-constexpr int kT3GWarps = 6;   // warps per CTA (two CTAs per SM at d = 512)
+constexpr int kT3GWarps = 8;   // warps per CTA (two CTAs per SM at d = 512)
 
 __device__ __forceinline__ float acc8f(float s, const float4& la, const float4& lb, const float4& xa, const float4& xb,
                                        f2 nz) {
@@ -565,7 +565,7 @@ __host__ __device__ constexpr int t3_group_stride(int dpad, int g) {  // floats 
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kT3GWarps * 32) knn_exact_group_kernel(T3ExactArgs a) {
+__global__ void __launch_bounds__(kT3GWarps * 32, 2) knn_exact_group_kernel(T3ExactArgs a) {
     extern __shared__ __align__(16) float sm_all[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int d = a.d, k = a.k, dpad = a.dpad;
