@@ -227,18 +227,28 @@ __global__ void __launch_bounds__(256) pair_table_tiled_kernel(const float* __re
 // tensor-core screens work on x - c and l - c, whose norms (and so the error
 // bounds) are several times smaller than those of x and l.
 __global__ void center_kernel(const float* __restrict__ hi, int g, int d, int dpad, float* __restrict__ cen) {
-    // one block per 32 dims: 8 row phases x 32 dims, f64 partial sums
-    __shared__ double part[8][32];
+    // one block per 32 dims: 32 row phases x 32 dims (1024 threads), f64
+    // partial sums, 4 rows in flight per thread; any centre is valid (the
+    // screens' bounds use the centred vectors actually formed), this one is
+    // the rounded mean
+    __shared__ double part[32][33];
     const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
     const int c0 = blockIdx.x * 32;
     double s = 0.0;
-    if (c0 + c < d)
-        for (int j = r0; j < g; j += 8) s += (double)hi[(int64_t)j * d + c0 + c];
+    if (c0 + c < d) {
+        int j = r0;
+        for (; j + 96 < g; j += 128) {
+            const float a0 = __ldg(hi + (int64_t)j * d + c0 + c), a1 = __ldg(hi + (int64_t)(j + 32) * d + c0 + c);
+            const float a2 = __ldg(hi + (int64_t)(j + 64) * d + c0 + c), a3 = __ldg(hi + (int64_t)(j + 96) * d + c0 + c);
+            s += ((double)a0 + (double)a1) + ((double)a2 + (double)a3);
+        }
+        for (; j < g; j += 32) s += (double)__ldg(hi + (int64_t)j * d + c0 + c);
+    }
     part[r0][c] = s;
     __syncthreads();
     if (r0 == 0 && c0 + c < dpad) {
         double t = 0.0;
-        for (int q = 0; q < 8; ++q) t += part[q][c];
+        for (int q = 0; q < 32; ++q) t += part[q][c];
         cen[c0 + c] = c0 + c < d ? (float)(t / g) : 0.0f;
     }
 }
@@ -904,7 +914,7 @@ bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1
 int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cudaStream_t st) {
     cudaMemsetAsync(ws + m.lstats, 0, 8, st);
     float* cen = reinterpret_cast<float*>(ws + m.lstats + 128);
-    center_kernel<<<(m.d16 + 31) / 32, 256, 0, st>>>(hi, g, d, m.d16, cen);
+    center_kernel<<<(m.d16 + 31) / 32, 1024, 0, st>>>(hi, g, d, m.d16, cen);
     tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
         hi, g, d, m.d16, m.gpad, cen, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
         reinterpret_cast<float*>(ws + m.ln), reinterpret_cast<float*>(ws + m.lstats));
@@ -1055,7 +1065,7 @@ int prepare_tc3(const float* hi, int g, int d, const ModelLayout& m, char* ws, i
     if (!m.t3) return ESOM_OK;
     cudaMemsetAsync(ws + m.ls3, 0, 8, st);
     float* cen = reinterpret_cast<float*>(ws + m.cen3);
-    center_kernel<<<(m.dk + 31) / 32, 256, 0, st>>>(hi, g, d, m.dk, cen);
+    center_kernel<<<(m.dk + 31) / 32, 1024, 0, st>>>(hi, g, d, m.dk, cen);
     if (int e = cuda_check("center_kernel")) return e;
     return t3_split(hi, g, m.gp3, d, m.dk, cen, -2.0f, 256, reinterpret_cast<uint16_t*>(ws + m.b3hi),
                     reinterpret_cast<uint16_t*>(ws + m.b3lo), reinterpret_cast<float*>(ws + m.ln3), 1,
