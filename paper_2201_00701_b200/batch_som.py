@@ -135,7 +135,9 @@ class FrameLoop:
         torch.cuda.synchronize(self.dev)
         n0 = L.load().esom_launch_count()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.device(self.dev), torch.cuda.graph(g):
+        # thread_local: the NCCL watchdog thread (multi-rank runs) may touch the
+        # CUDA runtime while this thread captures
+        with torch.cuda.device(self.dev), torch.cuda.graph(g, capture_error_mode="thread_local"):
             self._eager_frame()
         self.graph_launches = L.load().esom_launch_count() - n0
         self.graph = g
