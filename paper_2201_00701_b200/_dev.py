@@ -44,6 +44,13 @@ def to_f32(a, dev: torch.device) -> torch.Tensor:
     return torch.from_numpy(arr).to(dev)
 
 
+def to_dev_async(arr: np.ndarray, dev: torch.device) -> torch.Tensor:
+    """Small host array -> device without blocking the host: staged through
+    page-locked memory (torch's caching host allocator keeps the staging
+    buffer alive until the copy on the current stream has run)."""
+    return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory().to(dev, non_blocking=True)
+
+
 def to_i32(a, dev: torch.device) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.detach().to(device=dev, dtype=torch.int32).contiguous()

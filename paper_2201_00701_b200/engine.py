@@ -120,6 +120,7 @@ class DeviceSession:
             self.flag = _dev.new_flag(self.device)
             self.far_count = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._far_rows = 0  # rows embedded since far_count was last read
+        self._far_host, self._far_ev, self._far_n = None, None, 0
         self.bmu_order = False
         self.data = _DeviceDataset(self.X)
         stats = getattr(dataset, "dim_stats", None)
@@ -190,13 +191,20 @@ class DeviceSession:
         the previous frame took the f64 far-point path (a trained SOM packs
         its landmarks tightly: neighbour rows are then shared across a warp,
         0.80 -> 0.61 ms per 2^20 points on C3; an untrained model skips the
-        sort).  Reading the census is one 4-byte copy; the frame loops have
-        already synchronised the stream (trainer output / positions)."""
-        if self._far_rows:
-            far = int(self.far_count.item())
-            self.bmu_order = 2 * far > self._far_rows
+        sort).  The census travels by an asynchronous 4-byte copy and is
+        read once it has landed: the host never waits for it."""
+        if self._far_rows and self._far_ev is None:
+            st = torch.cuda.current_stream(self.device)
+            if self._far_host is None:
+                self._far_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            self._far_host.copy_(self.far_count, non_blocking=True)
             self.far_count.zero_()
-            self._far_rows = 0
+            self._far_ev = torch.cuda.Event()
+            self._far_ev.record(st)
+            self._far_n, self._far_rows = self._far_rows, 0
+        if self._far_ev is not None and self._far_ev.query():
+            self.bmu_order = 2 * int(self._far_host.item()) > self._far_n
+            self._far_ev = None
 
     def positions_host(self) -> np.ndarray:
         """Positions copied to a fresh host array (synchronises; raises on

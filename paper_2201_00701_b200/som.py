@@ -60,13 +60,14 @@ def _online_tick(kind: str, dataset, model, sample_idx, a: float, sigma: float =
         g, d = hi.shape
         if X.shape[1] != d:
             raise InputError(f"points have d={X.shape[1]}, model has d={d}")
-        sidx = torch.as_tensor(np.ascontiguousarray(sample_idx, np.int64)).to(dev) if not isinstance(
+        sidx = _dev.to_dev_async(np.asarray(sample_idx, np.int64), dev) if not isinstance(
             sample_idx, torch.Tensor) else sample_idx.to(device=dev, dtype=torch.int64).contiguous()
         nb = _lib.load().esom_tick_workspace_bytes(g, d)
         ws = _dev.workspace(dev, nb, slot="tick")
         st = _dev.stream_handle(dev)
         if kind == "som":
-            lo = _dev.to_f32(model.lo, dev)
+            lo = (_dev.to_f32(model.lo, dev) if isinstance(model.lo, torch.Tensor)
+                  else _dev.to_dev_async(np.asarray(model.lo, np.float32), dev))
             _lib.call("esom_som_tick", _dev.ptr(X), d, _dev.ptr(sidx), sidx.numel(), _dev.ptr(hi), _dev.ptr(lo), g,
                       float(sigma), float(a), _dev.ptr(ws), ws.numel(), st)
         else:

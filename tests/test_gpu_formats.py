@@ -335,3 +335,4 @@ def test_installed_gpu_tick_pipelined_equals_sequential():
             outs[i].append((p.positions.copy(), e.state.model.hi.copy()))
     for (pa, ha), (pb, hb) in zip(*outs):
         assert np.array_equal(pa, pb) and np.array_equal(ha, hb)
+
