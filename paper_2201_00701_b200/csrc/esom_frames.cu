@@ -527,6 +527,21 @@ __global__ void transform4_kernel(const float4* __restrict__ X, int64_t n4, int 
     const int cstep = (int)(stride % d4);
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int c4 = (int)(e % d4);
+    if (cstep == 0) {  // the grid stride is a multiple of the row: this thread's 4 columns never change
+        const ColXf t0 = cx4[4 * c4], t1 = cx4[4 * c4 + 1], t2 = cx4[4 * c4 + 2], t3 = cx4[4 * c4 + 3];
+        for (; e < n4; e += stride) {
+            const float4 v = __ldg(X + e);
+            float4 o;
+            o.x = xform1(t0, v.x);
+            o.y = xform1(t1, v.y);
+            o.z = xform1(t2, v.z);
+            o.w = xform1(t3, v.w);
+            bad |= !finite_f(o.x) | !finite_f(o.y) | !finite_f(o.z) | !finite_f(o.w);
+            out[e] = o;
+        }
+        flag_nonfinite(flag, bad);
+        return;
+    }
     for (; e < n4; e += stride, c4 = (c4 + cstep >= d4) ? c4 + cstep - d4 : c4 + cstep) {
         const float4 v = __ldg(X + e);
         const int c = 4 * c4;
