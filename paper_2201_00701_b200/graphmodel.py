@@ -143,9 +143,30 @@ def _edge_csr(pairs: np.ndarray, g: int):
     sid = np.concatenate([e, -e - 1])
     rank = np.concatenate([e, e + pairs.shape[0]])
     order = np.lexsort((rank, node))
-    ptr = np.zeros(g + 1, np.int32)
-    np.add.at(ptr, node + 1, 1)
+    ptr = np.zeros(g + 1, np.int64)
+    ptr[1:] = np.bincount(node, minlength=g)[:g]  # (np.add.at here cost ~4 ms at g = 4096)
     return np.cumsum(ptr).astype(np.int32), sid[order].astype(np.int32)
+
+
+_EDGE_CACHE: dict = {}
+
+
+def _edge_device(edges, g: int, dev):
+    """Device copies of an edge set (pairs, rest, CSR), cached while the same
+    EdgeSet arrays are passed again -- the engine rebuilds its graph every
+    REBUILD_CADENCE ticks but lays out every tick."""
+    key = (dev.index if isinstance(dev, torch.device) else int(dev), g)
+    hit = _EDGE_CACHE.get(key)
+    if hit is not None and hit[0] is edges.pairs and hit[1] is edges.rest:
+        return hit[2]
+    pairs = np.ascontiguousarray(edges.pairs, dtype=np.int32).reshape(-1, 2)
+    ptr, sid = _edge_csr(pairs, g)
+    out = (torch.from_numpy(pairs.copy()).to(dev),
+           torch.from_numpy(np.ascontiguousarray(edges.rest, dtype=np.float32)).to(dev),
+           torch.from_numpy(ptr).to(dev), torch.from_numpy(sid).to(dev))
+    _EDGE_CACHE.clear()
+    _EDGE_CACHE[key] = (edges.pairs, edges.rest, out)  # holds the arrays: identity stays valid
+    return out
 
 
 def _layout_dev(lo, edges: EdgeSet, st: LayoutState, pinned_rows, want_forces: bool):
@@ -155,16 +176,12 @@ def _layout_dev(lo, edges: EdgeSet, st: LayoutState, pinned_rows, want_forces: b
     if vel.shape != lo_np.shape:
         raise ParameterError("velocity matrix shape does not match layout")
     dev = _dev.cuda_device(lo)
-    pairs = np.ascontiguousarray(edges.pairs, dtype=np.int32).reshape(-1, 2)
-    ptr, sid = _edge_csr(pairs, g)
     pin = np.zeros(g, np.uint8)
     for r in pinned_rows:
         pin[int(r)] = 1
     with torch.cuda.device(dev):
+        P, R, CP, CE = _edge_device(edges, g, dev)
         L = torch.from_numpy(lo_np).to(dev)
-        P = torch.from_numpy(pairs.copy()).to(dev)
-        R = torch.from_numpy(np.ascontiguousarray(edges.rest, dtype=np.float32)).to(dev)
-        CP, CE = torch.from_numpy(ptr).to(dev), torch.from_numpy(sid).to(dev)
         PN = torch.from_numpy(pin).to(dev)
         V = torch.from_numpy(vel.copy()).to(dev)
         out = torch.empty_like(L)
