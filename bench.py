@@ -1,19 +1,22 @@
 #!/usr/bin/env python
-"""Benchmark of the EmbedSOM hot path on B200 (contract: see DESIGN.md §Measurement).
+"""Benchmark of the EmbedSOM hot path on B200 (contract: see DESIGN.md §4).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4|c5]
+                    [--trained T] [--impl ours|reference]
 
 Default workload = BASELINE.json configs[1] (C2): 2^20 x 32-d synthetic
 Gaussian-mixture points, 16x16 SOM (256 landmarks), k = 16, projection only.
 A step is one full re-projection (one frame) of every point of the rank's
-shard.  N > 1 (torchrun) is weak scaling: each rank owns its own 2^20-point
-shard; landmarks are replicated; projection has no collective.  c3/c4 add
-the batch-SOM training step (fused BMU statistics + one NCCL all-reduce +
-landmark update) to every frame.
+shard.  Every rank holds a contiguous row block of SURVEY §8d's dataset
+``gaussians(c, n_total, d, seed=1)`` (same cluster centres everywhere) and
+the same landmarks, drawn from the whole dataset.  C2/C3/C5 are weak scaling
+(2^20 points per rank); C4 is the 10M-point dataset split over the ranks.
+c3/c4 add the batch-SOM training step (BMU statistics + one NCCL all-reduce
++ landmark update) to every frame.  ``--trained T`` first trains the
+landmarks with T online SOM ticks (the interactive steady state).
 
-Rank 0 prints ONE JSON line.  `--impl reference` times the reference's CPU
-algorithm (the oracle port, oracle/esom_oracle.c, all host threads) on a
-bounded sample of the same workload.
+Rank 0 prints ONE JSON line.  ``--impl reference`` times the reference's
+own ``embedview.embed`` (baseline/_ref, numba) on all host cores.
 """
 
 from __future__ import annotations
@@ -37,16 +40,21 @@ sys.path.insert(0, str(ROOT))
 METRIC = "embedded points/sec & fps (1M–10M pts) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "points/s"
 
+# name: (clusters, n, d, rows, cols, k, train, scaling, description)
+#   weak:   every rank holds n points (the dataset has n x world rows)
+#   strong: the dataset has n rows, split contiguously over the ranks
 WORKLOADS = {
-    # name: (clusters, n per rank, d, rows, cols, k, train, description)
-    "c2": (16, 1 << 20, 32, 16, 16, 16, False,
-           "C2: 2^20x32 Gaussian mixture, 16x16 SOM (256 landmarks), k=16, projection only"),
-    "c3": (16, 1 << 20, 32, 16, 16, 16, True,
-           "C3: 2^20x32, 256 landmarks, k=16, batch-SOM step (BMU stats + all-reduce + update) + re-projection per frame"),
-    "c4": (16, 1_250_000, 32, 32, 32, 16, True,
-           "C4 shard: 1.25M x32 per GPU (10M over 8), 1024 landmarks, k=16, batch-SOM step + re-projection"),
-    "c5": (32, 1 << 20, 512, 64, 64, 32, False,
-           "C5: 2^20x512, 4096 landmarks, k=32, projection only (tcgen05 split-bf16 GEMM screen + exact re-evaluation)"),
+    "c2": (16, 1 << 20, 32, 16, 16, 16, False, "weak",
+           "C2: 2^20x32 Gaussian mixture per GPU, 16x16 SOM (256 landmarks), k=16, projection only"),
+    "c3": (16, 1 << 20, 32, 16, 16, 16, True, "weak",
+           "C3: 2^20x32 per GPU, 256 landmarks, k=16, batch-SOM step (BMU stats + all-reduce + update) "
+           "+ re-projection per frame"),
+    "c4": (16, 10_000_000, 32, 32, 32, 16, True, "strong",
+           "C4: 10M x32 split over the GPUs, 1024 landmarks, k=16, batch-SOM step (one all-reduce) "
+           "+ re-projection per frame"),
+    "c5": (32, 1 << 20, 512, 64, 64, 32, False, "weak",
+           "C5: 2^20x512 per GPU, 4096 landmarks, k=32, projection only (tcgen05 split-bf16 GEMM screen "
+           "+ exact re-evaluation)"),
 }
 
 
@@ -64,15 +72,28 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def make_inputs(workload: str, rank: int):
+def shard_bounds(workload: str, rank: int, world: int):
+    """(n_total, start, stop) of this rank's contiguous slice of the §8d dataset."""
+    c, n, d, rows, cols, k, train, scaling, _ = WORKLOADS[workload]
+    if scaling == "weak":
+        return n * world, rank * n, (rank + 1) * n
+    per, rem = divmod(n, world)
+    start = rank * per + min(rank, rem)
+    return n, start, start + per + (1 if rank < rem else 0)
+
+
+def make_inputs(workload: str, rank: int, world: int):
+    """This rank's rows of SURVEY §8d's dataset ``gaussians(c, n_total, d, seed=1)``
+    (same cluster centres on every rank) and the landmarks every rank shares:
+    the Engine-style model drawn from the WHOLE dataset (lattice lo, hi =
+    Rng(2).choice_distinct rows; ref: engine.py:208-227)."""
     from paper_2201_00701_b200 import datagen
 
-    c, n, d, rows, cols, k, train, _ = WORKLOADS[workload]
-    # the model comes from the seed-1 dataset on every rank (identical landmarks)
-    base = datagen.gaussians_f32(c, n, d, seed=1)
-    hi, lo = datagen.som_model(base, rows, cols, seed=2)
-    pts = base if rank == 0 else datagen.gaussians_f32(c, n, d, seed=1 + rank)
-    return pts, hi, lo, k, train
+    c, n, d, rows, cols, k, train, scaling, _ = WORKLOADS[workload]
+    n_total, start, stop = shard_bounds(workload, rank, world)
+    pick = datagen.som_model_rows(n_total, rows, cols, seed=2)
+    pts, hi = datagen.gaussians_slice(c, n_total, d, 1, start, stop, pick)
+    return pts, hi, datagen.lattice(rows, cols), k, train, n_total
 
 
 # ---------------------------------------------------------------------------
@@ -137,22 +158,12 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic(workload: str, points_per_launch: float):
-    """DRAM bytes per launch of the dominant kernel: the committed ncu capture's
-    bytes/point (profiles/traffic.json) x the points one launch processes here."""
-    p = ROOT / "profiles" / "traffic.json"
-    if p.exists():
-        j = json.loads(p.read_text())
-        v = j.get(workload)
-        if isinstance(v, dict) and v.get("points"):
-            return v["dram_bytes"] / v["points"] * points_per_launch
-    return None
-
-
 # ---------------------------------------------------------------------------
-# CPU arms (oracle port; test infrastructure, never the measured product)
+# CPU arms (test infrastructure / the reference itself; never the measured product)
 # ---------------------------------------------------------------------------
 def cpu_embed_rate(pts, hi, lo, k, n_sample: int, threads: int):
+    """The oracle port (oracle/esom_oracle.c, pthreads, row-sharded) on the
+    first n_sample points: points/s and wall seconds."""
     from oracle import oracle  # checker / CPU baseline only
 
     sub = np.ascontiguousarray(pts[:n_sample])
@@ -163,44 +174,175 @@ def cpu_embed_rate(pts, hi, lo, k, n_sample: int, threads: int):
     return n_sample / dt, dt
 
 
+REF_DIR = ROOT / "baseline" / "_ref"
+_REF_JOB = {}
+
+
+def _ref_worker_init():
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    import embedview  # noqa: F401  (the unmodified reference, baseline/_ref)
+
+
+def _ref_worker(args):
+    import embedview
+
+    s, e, backend = args
+    pts, hi, lo, k = _REF_JOB["pts"], _REF_JOB["hi"], _REF_JOB["lo"], _REF_JOB["k"]
+    model = embedview.LandmarkModel.create(hi, lo)
+    t0 = time.perf_counter()
+    xy = embedview.embed(pts[s:e], model, embedview.EmbedParams(k=k), backend=backend)
+    return s, xy, time.perf_counter() - t0
+
+
+def reference_available() -> bool:
+    if not (REF_DIR / "embedview").exists():
+        return False
+    try:
+        import numba  # noqa: F401
+    except ImportError:
+        return False
+    return True
+
+
+class ReferencePool:
+    """The reference's own ``embedview.embed`` (numba, as shipped) on every
+    host core: one forked worker process per core, each embedding a
+    contiguous row block (the output is chunk-invariant,
+    tests:test_projection.py:217-223; SURVEY §8d CPU timing)."""
+
+    def __init__(self, pts, hi, lo, k, procs: int):
+        import multiprocessing as mp
+
+        sys.path.insert(0, str(REF_DIR))
+        _REF_JOB.update(pts=pts, hi=hi, lo=lo, k=k)
+        self.procs = procs
+        self.pool = mp.get_context("fork").Pool(procs, initializer=_ref_worker_init)
+        # JIT-compile the numba kernels in every worker (cached on disk after the first)
+        self.pool.map(_ref_worker, [(0, 64, "bitonic")] * procs + [(0, 64, "base")] * procs)
+
+    def embed(self, n: int, backend: str = "bitonic"):
+        step = (n + self.procs - 1) // self.procs
+        t0 = time.perf_counter()
+        parts = self.pool.map(_ref_worker, [(s, min(n, s + step), backend) for s in range(0, n, step)])
+        dt = time.perf_counter() - t0
+        xy = np.concatenate([p[1] for p in sorted(parts, key=lambda p: p[0])])
+        return xy, dt
+
+    def close(self):
+        self.pool.terminate()
+
+
 def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path on the
+    box's host cores -- the unmodified ``embedview.embed`` (baseline/_ref,
+    default backend "bitonic") sharded over every core; the oracle port
+    (kind "port") only when the reference cannot be imported."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
     workload = args.workload
-    pts, hi, lo, k, train = make_inputs(workload, 0)
+    world = args.gpus
+    pts, hi, lo, k, train, n_total = make_inputs(workload, 0, 1 if workload == "c4" else world)
     cores = host_cores()
-    c, n, d, rows, cols, k, train, desc = WORKLOADS[workload]
-    # per-step sample sized for ~1 s of wall time on the host's cores
-    per_pt_us = {"c2": 20.0, "c3": 20.0, "c4": 60.0, "c5": 2500.0}[workload]
-    n_sample = int(max(256, min(n, cores * 1e6 / per_pt_us)))
-    for _ in range(max(0, args.warmup)):
-        cpu_embed_rate(pts, hi, lo, k, min(n_sample, 4096), cores)
-    rates, times = [], []
-    for _ in range(args.steps):
-        r, dt = cpu_embed_rate(pts, hi, lo, k, n_sample, cores)
-        rates.append(r)
-        times.append(dt)
-    total_pts = n_sample * args.steps
-    value = total_pts / sum(times)
-    sample = (f"{n_sample} of {n} points per step ({workload}), oracle port of embed (knn_base + scores + "
-              f"projection, ref: projection.py:220-245), {cores} threads, row-sharded")
+    c, n, d, rows, cols, k, train, scaling, desc = WORKLOADS[workload]
+    n_rank = pts.shape[0]
+    # per-step sample: the whole rank-0 workload when it takes <= ~5 s on the host cores
+    # (C2/C3: 2^20 points), else a bounded leading block of it (C4 / C5)
+    per_pt_us = {"c2": 30.0, "c3": 30.0, "c4": 80.0, "c5": 2500.0}[workload]
+    n_sample = int(min(n_rank, max(4096, cores * 5e6 / per_pt_us)))
+    extra = {}
+    if reference_available():
+        kind = "reference"
+        pool = ReferencePool(pts, hi, lo, k, cores)
+        try:
+            for _ in range(max(0, args.warmup)):
+                pool.embed(min(n_sample, 64 * cores))
+            times = [pool.embed(n_sample)[1] for _ in range(args.steps)]
+            _, t_base = pool.embed(n_sample, "base")
+            extra["base_backend_points_per_s"] = n_sample / t_base
+        finally:
+            pool.close()
+        how = (f"unmodified reference embedview.embed (baseline/_ref, numba, backend 'bitonic', ref: "
+               f"projection.py:220-245) over {cores} forked processes, contiguous row blocks")
+        try:
+            r_port, _ = cpu_embed_rate(pts, hi, lo, k, n_sample, cores)
+            extra["oracle_port_points_per_s"] = r_port
+        except Exception as e:  # noqa: BLE001
+            extra["oracle_port_points_per_s"] = f"unavailable: {e}"
+    else:
+        kind = "port"
+        for _ in range(max(0, args.warmup)):
+            cpu_embed_rate(pts, hi, lo, k, min(n_sample, 4096), cores)
+        times = [cpu_embed_rate(pts, hi, lo, k, n_sample, cores)[1] for _ in range(args.steps)]
+        how = (f"oracle port of embed (oracle/esom_oracle.c: knn_base + scores + projection, ref: "
+               f"projection.py:220-245), {cores} threads, row-sharded (reference not importable here)")
+    value = n_sample * args.steps / sum(times)
+    sample = (f"{'all ' if n_sample == n_rank else 'first '}{n_sample} of the {n_rank} rank-0 points per step "
+              f"({workload}); {how}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
-        "data": "synthetic (reference datagen.gaussians restated)",
-        "config": {"workload": desc, "n_per_rank": n, "d": d, "g": rows * cols, "k": k},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (reference datagen.gaussians restated), SOM-initialised landmarks",
+        "config": config_of(workload, world, n_rank, n_total, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample, **extra},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def config_of(workload, world, n_rank, n_total, args):
+    c, n, d, rows, cols, k, train, scaling, desc = WORKLOADS[workload]
+    return {"workload": desc, "n_total": n_total, "n_per_rank": n_rank, "d": d, "g": rows * cols, "k": k,
+            "train": train, "trained_ticks": args.trained,
+            "parallelism": f"points sharded x{world} (contiguous rows), landmarks replicated",
+            "l2": f"inputs larger than L2 (X = {n_rank * d * 4 / 2**20:.0f} MiB/rank) and L2 flushed "
+                  "between timed steps (256 MiB write outside the events)"}
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def train_model(X, hi, lo, ticks: int, world: int):
+    """--trained T: the interactive steady state -- T online SOM ticks of the
+    reference's trainer (SomConfig defaults, 256 samples each, Rng(3); ref:
+    som.py:44-68, engine.py:356-361) on this rank's points, rank 0's result
+    broadcast so every rank projects with the same landmarks."""
+    import torch
+
+    import paper_2201_00701_b200 as esom
+
+    class _D:
+        points = X
+
+    model = esom.LandmarkModel.create(hi, lo)
+    rng = esom.Rng(3)
+    h = None
+    for _ in range(ticks):
+        h = esom.som_tick(_D, model, esom.SomConfig(), rng)
+        model = esom.LandmarkModel.create(h.cpu().numpy(), lo)
+    out = np.ascontiguousarray(model.hi, np.float32)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.from_numpy(out.copy()).to(X.device)
+        dist.broadcast(t, 0)
+        out = t.cpu().numpy()
+    return out
+
+
+def ncu_dominant(workload: str, trained: int):
+    """The committed ncu figures of the workload's dominant kernel
+    (profiles/traffic.json): DRAM bytes and warp instructions per point."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    j = json.loads(p.read_text())
+    v = j.get(f"{workload}_trained" if trained else workload) or j.get(workload)
+    return v if isinstance(v, dict) and v.get("points") else None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -213,18 +355,25 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     if world > 1:
         if args.dist_backend == "nccl":
+            # NCCL's own init log (stderr) records the communicator's rank count and transport
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
 
     import paper_2201_00701_b200 as esom
+    from paper_2201_00701_b200 import _lib
     from paper_2201_00701_b200.batch_som import BatchSomConfig, FrameLoop
 
     workload = args.workload
-    c, n, d, rows, cols, k, train, desc = WORKLOADS[workload]
-    pts, hi, lo, k, train = make_inputs(workload, rank)
+    c, n_cfg, d, rows, cols, k, train, scaling, desc = WORKLOADS[workload]
+    pts, hi, lo, k, train, n_total = make_inputs(workload, rank, world)
+    n = pts.shape[0]
     g = rows * cols
     X = torch.from_numpy(pts).to(dev)
+    if args.trained:
+        hi = train_model(X, hi, lo, args.trained, world)
     loop = FrameLoop(X, hi, lo, k, BatchSomConfig(sigma=1.0, alpha=0.05), train=train)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -237,18 +386,23 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         loop.frame()
     barrier()
-    # one frame = one CUDA-graph launch (single rank, or no collective in the frame;
-    # NCCL inside captured graphs is left out of the multi-rank training loop)
-    use_graph = not args.no_graph and (world == 1 or not train)
+    # one frame = one CUDA-graph launch; with training at N > 1 the graph holds the
+    # NCCL all-reduce of the statistics too (eager frames if capture is refused)
+    use_graph = not args.no_graph
+    graph_note = None
     if use_graph:
-        loop.capture()
-        loop.frame()
-        barrier()
+        try:
+            loop.capture()
+            loop.frame()
+            barrier()
+        except Exception as e:  # noqa: BLE001
+            graph_note = f"capture failed, eager frames: {type(e).__name__}: {e}"[:300]
+            loop.graph = None
+            use_graph = False
+            barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    from paper_2201_00701_b200 import _lib as _lc
-
-    launches0 = _lc.load().esom_launch_count()
+    launches0 = _lib.load().esom_launch_count()
     with ClockSampler(dev.index) as clk:
         barrier()
         for s in range(args.steps):
@@ -257,7 +411,7 @@ def run_ours(args):
             loop.frame()
             ev[s][1].record(stream)
         barrier()
-    launches_timed = _lc.load().esom_launch_count() - launches0  # our kernels inside the timed region
+    launches_timed = _lib.load().esom_launch_count() - launches0  # our kernels inside the timed region
     if use_graph:  # replays bypass the host-side counter: kernels captured per frame x frames
         launches_timed = loop.graph_launches * args.steps
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -266,21 +420,19 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    total_points = n * world
+    total_points = n_total
     value = total_points / (ms_max * 1e-3)
 
-    # ---- dominant kernel of the frame, timed live with CUDA events on the
-    # launching stream (libesom's esom_timing_* hooks around each launch),
-    # one extra L2-flushed frame after the timed region.  Algorithmic work per
-    # point: k-NN kernels 4d (X) + 8k (idx + sqd) bytes, the
-    # d > 32 GEMM screen 2 g d flops (one x.L^T), the projection 8k + 8 bytes.
-    from paper_2201_00701_b200 import _dev as _d, _lib as _l
-
-    L = _l.load()
+    # ---- per-kernel device time inside one frame, timed live with CUDA events on
+    # the launching stream (libesom's esom_timing_* hooks around each launch), one
+    # extra L2-flushed eager frame after the timed region.  Algorithmic work per
+    # point: k-NN kernels 4d (X) + 8k (idx + sqd) bytes, the d > 32
+    # GEMM screen 2gd flops (one x.L^T), the projection 8k + 8 bytes.
+    L = _lib.load()
     flush.zero_()
     torch.cuda.synchronize(dev)
     L.esom_timing_begin(1)
-    loop._eager_frame()  # eager: the timing hooks record events around each launch
+    loop._eager_frame()
     torch.cuda.synchronize(dev)
     ktimes = {}
     for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "knn_gemm_kernel", "knn_exact_group_kernel",
@@ -294,62 +446,71 @@ def run_ours(args):
     hbm_peak, bf16_peak, peak_kind = measured_peaks()
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or 1965.0
-    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # lane-ops/s (T), at the sampled clock
-    dk = (d + 31) // 32 * 32
-    if dom == "knn_gemm_kernel":
+    issue_peak = 148 * 4 * sm_mhz * 1e6  # warp instructions/s (4 schedulers per SM)
+    nc = ncu_dominant(workload, args.trained)
+    roofline = None
+    if dom is not None:
         kms = ktimes[dom]["ms"]
-        alg_flops = 2.0 * n * g * d
-        mma_flops = 2.0 * n * g * dk * 3 * 2  # split-bf16 (3 products) x two passes, as executed
-        roofline = {"bound": "tensor", "achieved": alg_flops / (kms * 1e-3) / 1e12, "peak": bf16_peak,
-                    "unit": "TFLOP/s", "frac": alg_flops / (kms * 1e-3) / 1e12 / bf16_peak,
-                    "traffic": ncu_traffic(workload, n / ktimes[dom]["launches"]), "peak_kind": peak_kind,
-                    "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
-                    "alg_flops_per_point": 2 * g * d,
-                    "executed_mma_TFLOPs": mma_flops / (kms * 1e-3) / 1e12,
-                    "executed_mma_frac_of_bf16_peak": mma_flops / (kms * 1e-3) / 1e12 / bf16_peak,
-                    "note": "achieved = algorithmic 2gd flops/point (one x.L^T); the kernel issues 6x that in "
-                            "bf16 MMAs (x_hi l_hi + x_hi l_lo + x_lo l_hi, group-min pass + candidate pass)"}
-    elif dom is not None:
-        kms = ktimes[dom]["ms"]
-        per_pt = (4 * d + 8 * k) if dom.startswith("knn") else (8 * k + 8)
-        achieved = n * per_pt / (kms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": achieved / hbm_peak, "traffic": ncu_traffic(workload, n / ktimes[dom]["launches"]),
-                    "peak_kind": peak_kind,
-                    "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
-                    "alg_bytes_per_point": per_pt,
-                    "note": "issue-bound exact selection (SURVEY §8d: distance intensity >> HBM ridge); "
-                            "compute_roofline gives the pipe view"}
-    else:
-        roofline = None
-    embed_frac = n * (4 * d + 8) / (ms * 1e-3) / 1e9 / hbm_peak
-    exact_ops = n * 3.0 * g * d / (ms * 1e-3) / 1e12  # exact-path equivalent sub/mul/add per element
-    compute_roofline = {"exact_equiv_Tops": exact_ops, "fp32_peak_Tops_at_sampled_clock": fp32_peak,
-                        "exact_equiv_frac": exact_ops / fp32_peak, "embed_hbm_frac": embed_frac,
-                        "kernels": ktimes,
-                        "note": "exact_equiv = 3*g*d f32 ops per point / frame time (what an exact CUDA-core scan "
-                                "must issue); kernels: per-kernel device ms inside one frame"}
-    # ---- end to end through the public API: pinned host points in, host xy out ----
-    e2e = None
-    if True:  # every rank measures; the slowest rank defines the job's e2e time
-        host = torch.from_numpy(pts).pin_memory()
-        model = esom.LandmarkModel.create(hi, lo)
-        params = esom.EmbedParams(k=k)
-        esom.embed(host, model, params)  # warm
+        pts_launch = n / ktimes[dom]["launches"]
+        traffic = (nc["dram_bytes"] / nc["points"] * pts_launch) if nc else None
+        issue = None
+        if nc and nc.get("inst_executed"):
+            issue = nc["inst_executed"] / nc["points"] * n / (kms * 1e-3) / issue_peak
+        if dom == "knn_gemm_kernel":
+            dk = (d + 31) // 32 * 32
+            alg = 2.0 * n * g * d / (kms * 1e-3) / 1e12
+            mma = 2.0 * n * g * dk * 3 * 2 / (kms * 1e-3) / 1e12
+            roofline = {"bound": "tensor", "achieved": alg, "peak": bf16_peak, "unit": "TFLOP/s",
+                        "frac": alg / bf16_peak, "traffic": traffic, "peak_kind": peak_kind,
+                        "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
+                        "alg_flops_per_point": 2 * g * d, "executed_mma_TFLOPs": mma,
+                        "executed_mma_frac_of_bf16_peak": mma / bf16_peak,
+                        "note": "achieved = algorithmic 2gd flops/point (one x.L^T); the kernel issues 6x that "
+                                "in bf16 MMAs (3 split products, group-min pass + candidate pass)"}
+        else:
+            per_pt = (4 * d + 8 * k) if dom.startswith("knn") else (8 * k + 8)
+            achieved = n * per_pt / (kms * 1e-3) / 1e9
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                        "kernel": dom, "kernel_ms_per_frame": kms, "launches": ktimes[dom]["launches"],
+                        "alg_bytes_per_point": per_pt}
+        roofline["issue_frac"] = issue
+        roofline["issue_note"] = ("issue_frac = ncu warp instructions/point of this kernel (profiles/traffic.json) "
+                                  "x points / (148 SMs x 4 schedulers x sampled SM clock x live kernel time): "
+                                  "the pipe that actually binds an exact k-NN / projection (SURVEY §8d)")
+    frame_bytes = n * (4 * d + 8)
+    frame_view = {"alg_bytes_per_point": 4 * d + 8, "embed_hbm_frac": frame_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+                  "kernels": ktimes,
+                  "note": "whole frame: X read once + xy written (4d + 8 B/point) over the frame time; "
+                          "kernels: per-kernel device ms inside one eager frame"}
+    # ---- end to end through the public API: host points in, host xy out ----
+    host = torch.from_numpy(pts).pin_memory()
+    model = esom.LandmarkModel.create(hi, lo)
+    params = esom.EmbedParams(k=k)
+
+    def e2e_of(inp):
+        esom.embed(inp, model, params)  # warm
         times = []
+        out = None
         for _ in range(max(3, min(args.steps, 10))):
             barrier()
             t0 = time.perf_counter()
-            out = esom.embed(host, model, params)  # H2D, fused kernel, D2H (numpy back)
+            out = esom.embed(inp, model, params)  # H2D, kernels, D2H (numpy back)
             times.append(time.perf_counter() - t0)
-        e2e_s = statistics.median(times)
-        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        et = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": total_points / float(et.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(host.numel() * 4), "d2h_bytes_per_step": int(out.nbytes),
-               "how": "esom.embed(pinned host tensor, model, EmbedParams) incl. model prep, H2D, kernel, D2H; "
-                      "wall clock, median"}
+        return total_points / float(et.item()), out
+
+    v_pin, out = e2e_of(host)
+    e2e = {"value": v_pin, "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
+           "d2h_bytes_per_step": int(out.nbytes),
+           "how": "esom.embed(pinned host tensor, model, EmbedParams): model prep, chunked H2D / kernels / D2H "
+                  "on three streams, numpy xy back; wall clock, median, max over ranks"}
+    v_np, _ = e2e_of(pts)
+    e2e_numpy = {"value": v_np, "unit": UNIT,
+                 "how": "esom.embed(numpy f32 array) -- the reference's calling convention: pageable rows "
+                        "staged by host threads through pinned chunks inside embed"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -361,20 +522,22 @@ def run_ours(args):
                          f"{cores} threads, {dt:.2f} s wall"}
 
     if rank == 0:
+        cfg = config_of(workload, world, n, n_total, args)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max, "fps": 1e3 / ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": ("f32 exact k-NN (bf16x3 tcgen05 screen), f32/f64 projection" if d > 32 else "f32 exact k-NN (bf16x3 tcgen05 screen), f32/f64 projection"),
-            "data": "synthetic Gaussian mixture (reference datagen.gaussians restated), SOM-initialised landmarks",
-            "config": {"workload": desc, "n_per_rank": n, "d": d, "g": g, "k": k, "train": train,
-                       "parallelism": f"points sharded x{world}, landmarks replicated",
-                       "l2": "flushed between timed steps (256 MiB write outside the events); X = 128 MiB/rank",
-                       "cuda_graph": use_graph},
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f32 exact k-NN (bf16x3 tcgen05 screen, exact f32 re-evaluation), f32/f64 projection",
+            "data": "synthetic Gaussian mixture (reference datagen.gaussians restated), SOM-initialised landmarks"
+                    + (f", trained by {args.trained} online SOM ticks" if args.trained else ""),
+            "config": cfg,
             "roofline": roofline,
-            "compute_roofline": compute_roofline,
+            "frame": frame_view,
             "clocks": clocks,
             "gpu_launches": launches_timed,
+            "cuda_graph": use_graph if not graph_note else {"used": False, "note": graph_note},
             "e2e": e2e,
+            "e2e_numpy": e2e_numpy,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -390,6 +553,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--trained", type=int, default=0,
+                    help="online SOM ticks applied to the landmarks before timing (interactive steady state)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch each frame's kernels eagerly (no CUDA graph)")

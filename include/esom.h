@@ -90,16 +90,20 @@ int esom_prepare_model(const float *hi, int32_t g, int32_t d, int32_t k, void *w
  * of one L2-resident chunk of points (scan -> projection). */
 size_t esom_point_workspace_bytes(int64_t n, int32_t d, int32_t k);
 
-/* Embed on a prepared model: exact k-NN scan + scores + projection -> xy
- * (n×2 f32), two kernels per chunk.  Replaces embed (ref:
- * projection.py:220-245).  Optional outputs (NULL to skip): bmu (n int32 =
- * idx[:,0]); batch-SOM statistics acc_S (g×d f64 += x_i per BMU) and acc_C
- * (g f64 += 1); qe_sum (f64 += nearest squared distance, ref: som.py:71-79).
- * k <= 64. */
+/* Embed on a prepared model: exact k-NN + scores + projection -> xy (n×2
+ * f32).  Per chunk of points: the k-NN (d <= 32: tensor-core screen, BMU
+ * sort, exact re-evaluation; d > 32: operand split, GEMM screen, BMU sort,
+ * exact re-evaluation) and the projection kernel -- esom_embed_launches()
+ * counts them.  Replaces embed (ref: projection.py:220-245).  Optional
+ * outputs (NULL to skip): bmu (n int32 = idx[:,0]); batch-SOM statistics in
+ * exact int64 fixed point -- acc_S (g×d: += round(x_i 2^acc_fx_bits) per
+ * BMU) and acc_C (g: += 1) -- so they are independent of accumulation order
+ * and of the split of points over ranks; qe_sum (f64 += nearest squared
+ * distance, ref: som.py:71-79).  k <= 64, 0 <= acc_fx_bits <= 60. */
 int esom_embed_prepared(const float *X, int64_t n, int32_t d, const float *hi, const float *lo,
                         int32_t g, int32_t k, const void *model_ws, void *point_ws,
-                        size_t point_ws_bytes, float *xy, int32_t *bmu, double *acc_S,
-                        double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
+                        size_t point_ws_bytes, float *xy, int32_t *bmu, int64_t *acc_S,
+                        int64_t *acc_C, int32_t acc_fx_bits, double *qe_sum, int32_t *nonfinite_flag,
                         cudaStream_t stream);
 
 /* esom_embed_prepared with options.  flags: ESOM_EMBED_BMU_ORDER = visit
@@ -111,9 +115,9 @@ int esom_embed_prepared(const float *X, int64_t n, int32_t d, const float *hi, c
 #define ESOM_EMBED_BMU_ORDER 1
 int esom_embed_prepared_ex(const float *X, int64_t n, int32_t d, const float *hi, const float *lo,
                            int32_t g, int32_t k, const void *model_ws, void *point_ws,
-                           size_t point_ws_bytes, float *xy, int32_t *bmu, double *acc_S,
-                           double *acc_C, double *qe_sum, int32_t *nonfinite_flag, int32_t flags,
-                           int32_t *far_count, cudaStream_t stream);
+                           size_t point_ws_bytes, float *xy, int32_t *bmu, int64_t *acc_S,
+                           int64_t *acc_C, int32_t acc_fx_bits, double *qe_sum, int32_t *nonfinite_flag,
+                           int32_t flags, int32_t *far_count, cudaStream_t stream);
 
 /* Number of kernels one esom_embed_prepared(n, ...) call launches (evidence
  * for the benchmark's launch count). */
@@ -124,14 +128,15 @@ int32_t esom_embed_launches(int64_t n, int32_t g, int32_t d, int32_t k);
 size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k);
 int esom_embed(const float *X, int64_t n, int32_t d, const float *hi, const float *lo, int32_t g,
                int32_t k, void *workspace, size_t ws_bytes, float *xy, int32_t *bmu,
-               double *acc_S, double *acc_C, double *qe_sum, int32_t *nonfinite_flag,
-               cudaStream_t stream);
+               int64_t *acc_S, int64_t *acc_C, int32_t acc_fx_bits, double *qe_sum,
+               int32_t *nonfinite_flag, cudaStream_t stream);
 
 /* Batch-SOM statistics only (BMU pass, no projection): acc_S/acc_C/qe_sum
  * as in esom_embed_prepared; bmu optional.  Workspace from esom_workspace_bytes(.., 0). */
 int esom_bmu_accumulate(const float *X, int64_t n, int32_t d, const float *hi, int32_t g,
-                        void *workspace, size_t ws_bytes, int32_t *bmu, double *acc_S,
-                        double *acc_C, double *qe_sum, int32_t *nonfinite_flag, cudaStream_t stream);
+                        void *workspace, size_t ws_bytes, int32_t *bmu, int64_t *acc_S,
+                        int64_t *acc_C, int32_t acc_fx_bits, double *qe_sum, int32_t *nonfinite_flag,
+                        cudaStream_t stream);
 
 /* Online trainers: the sample indices are drawn on the host from the
  * caller's Rng (ref: som.py:57, graphmodel.py:96) and applied in order.
@@ -144,12 +149,14 @@ int esom_kmeans_tick(const float *X, int32_t d, const int64_t *sample_idx, int32
                      float *hi_inout, int32_t g, double alpha_km, void *workspace,
                      size_t ws_bytes, cudaStream_t stream);                 /* ref: graphmodel.py:87-102 */
 
-/* Batch-SOM landmark update from (all-reduced) statistics.  NEW -- no
- * reference function.  mode 0 mean-field
- * hi_j += (alpha/B)(num_j - den_j hi_j); mode 1 Kohonen hi_j = num_j/den_j. */
-int esom_batch_som_update(const double *acc_S, const double *acc_C, const float *lo, int32_t g,
-                          int32_t d, double sigma, double alpha, int32_t mode, float *hi_inout,
-                          cudaStream_t stream);
+/* Batch-SOM landmark update from (all-reduced) int64 fixed-point statistics
+ * (S = acc_S 2^-acc_fx_bits, C = acc_C).  NEW -- no reference function
+ * (SURVEY.md §8a T3).  mode 0 mean-field hi_j += (alpha/B)(num_j - den_j
+ * hi_j); mode 1 Kohonen hi_j = num_j/den_j.  Deterministic: a fixed
+ * reduction order per landmark. */
+int esom_batch_som_update(const int64_t *acc_S, const int64_t *acc_C, int32_t acc_fx_bits,
+                          const float *lo, int32_t g, int32_t d, double sigma, double alpha,
+                          int32_t mode, float *hi_inout, cudaStream_t stream);
 
 /* ---- data formats either side of the path ---- */
 

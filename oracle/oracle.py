@@ -147,6 +147,25 @@ def batch_som_step(points, hi, lo, sigma: float, alpha: float, mode: int = 0):
     return batch_som_update(S, Cn, lo, hi, sigma, alpha, mode)
 
 
+def batch_som_accumulate_fx(points, hi, fx: int):
+    """The device's exact statistics (batch_som.py): BMU = exact f32 nearest
+    landmark (knn_base k = 1), S_b = sum of round(x 2^fx) as int64, C_b = count.
+    Integer sums: any split of the points gives the same S, C."""
+    p = _f32(points)
+    g, d = _f32(hi).shape
+    b = knn(p, hi, 1)[0][:, 0].astype(np.int64)
+    q = np.rint(p.astype(np.float64) * np.ldexp(1.0, fx)).astype(np.int64)  # round half even, like __double2ll_rn
+    S = np.zeros((g, d), np.int64)
+    np.add.at(S, b, q)
+    return S, np.bincount(b, minlength=g).astype(np.int64)
+
+
+def batch_som_update_fx(S_int, Cn, fx: int, lo, hi, sigma: float, alpha: float, mode: int = 0):
+    """batch_som_update on the fixed-point statistics (S = S_int 2^-fx, exact in f64 below 2^53)."""
+    return batch_som_update(np.asarray(S_int, np.int64).astype(np.float64) * np.ldexp(1.0, -fx), Cn, lo, hi,
+                            sigma, alpha, mode)
+
+
 def quantization_error(points, hi) -> float:
     p, h = _f32(points), _f32(hi)
     return float(lib().oracle_quantization_error(p, p.shape[0], p.shape[1], h, h.shape[0]))

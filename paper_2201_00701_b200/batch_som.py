@@ -10,12 +10,19 @@ SPEC.md:270).  Semantics:
   5. mean-field: hi_j += (alpha / B)(num_j - den_j hi_j)   (B = sum C; at B = 1
      this is som_tick's update for that sample), or Kohonen: hi_j = num_j / den_j.
 
-Statistics are produced by the same fused scan kernel that embeds the
-frame (its BMU epilogue), so one interactive frame reads the points once.
+The statistics are exact int64 fixed point (``acc_fx_bits`` fractional
+bits, chosen once from the dataset's magnitude and size): integer sums do
+not depend on accumulation order, atomic scheduling or how the points are
+split over ranks, so the landmarks after any number of steps are
+bit-identical at every GPU count (SURVEY §7 hard part 6).  They come from
+the embed's k-NN (BMU = idx[:, 0]) as a separate pass over X: a shared-
+memory table in natural point order when it fits one SM (C3), else segment
+sums over the BMU-sorted order the projection also uses (C4).
 """
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -50,22 +57,58 @@ def _allreduce_(buf: torch.Tensor, group=None) -> None:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
 
 
-def update_landmarks_(hi: torch.Tensor, lo: torch.Tensor, acc: torch.Tensor, cfg: BatchSomConfig) -> None:
-    """In-place landmark update from packed statistics acc = [S (g×d) | C (g)] (f64)."""
+def acc_fx_bits(maxabs: float, n_total: int) -> int:
+    """Fractional bits of the int64 fixed-point statistics: the most (capped at
+    40, i.e. 9e-13 resolution) that keep n_total x max|x| x 2^fx below 2^61.
+    Every rank must pass the GLOBAL max|x| and point count."""
+    bound = float(n_total) * float(maxabs)
+    if not math.isfinite(bound):
+        raise ParameterError("non-finite points")
+    if bound <= 0.0:
+        return 40
+    fx = int(math.floor(61.0 - math.log2(bound)))
+    if fx < 0:
+        raise ParameterError(f"point magnitudes too large for the fixed-point statistics (n x max|x| = {bound:.3g})")
+    return min(40, fx)
+
+
+def dataset_fx_bits(X: torch.Tensor, group=None) -> int:
+    """acc_fx_bits of the points of all ranks (one amax pass + two tiny all-reduces)."""
+    import torch.distributed as dist
+
+    st = torch.stack([X.abs().amax().double() if X.numel() else torch.zeros((), dtype=torch.float64, device=X.device),
+                      torch.tensor(float(X.shape[0]), dtype=torch.float64, device=X.device)])
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        mx, nn = st[:1].clone(), st[1:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(nn, op=dist.ReduceOp.SUM, group=group)
+        st = torch.cat([mx, nn])
+    mx, nn = st.tolist()
+    return acc_fx_bits(mx, int(nn))
+
+
+def new_acc(g: int, d: int, dev) -> torch.Tensor:
+    """Packed statistics [S (g×d) | C (g)], int64 (one all-reduce per step)."""
+    return torch.zeros(g * d + g, dtype=torch.int64, device=dev)
+
+
+def update_landmarks_(hi: torch.Tensor, lo: torch.Tensor, acc: torch.Tensor, fx: int, cfg: BatchSomConfig) -> None:
+    """In-place landmark update from packed int64 statistics acc = [S (g×d) | C (g)]."""
     g, d = hi.shape
     dev = hi.device
-    _lib.call("esom_batch_som_update", _dev.ptr(acc), _dev.ptr(acc) + g * d * 8, _dev.ptr(lo), g, d,
+    _lib.call("esom_batch_som_update", _dev.ptr(acc), _dev.ptr(acc) + g * d * 8, int(fx), _dev.ptr(lo), g, d,
               float(cfg.sigma), float(cfg.alpha), _MODES[cfg.mode], _dev.ptr(hi), _dev.stream_handle(dev))
 
 
-def accumulate(X: torch.Tensor, hi: torch.Tensor, acc: torch.Tensor, qe_sum=None, flag=None) -> None:
+def accumulate(X: torch.Tensor, hi: torch.Tensor, acc: torch.Tensor, fx: int, qe_sum=None, flag=None) -> None:
     """acc += BMU statistics of device points X (no projection)."""
     n, d = X.shape
     g = hi.shape[0]
     dev = X.device
     ws = _dev.workspace(dev, _lib.load().esom_workspace_bytes(g, d, 1, 0), slot="bmu")
     _lib.call("esom_bmu_accumulate", _dev.ptr(X), n, d, _dev.ptr(hi), g, _dev.ptr(ws), ws.numel(), 0,
-              _dev.ptr(acc), _dev.ptr(acc) + g * d * 8, _dev.ptr(qe_sum), _dev.ptr(flag), _dev.stream_handle(dev))
+              _dev.ptr(acc), _dev.ptr(acc) + g * d * 8, int(fx), _dev.ptr(qe_sum), _dev.ptr(flag),
+              _dev.stream_handle(dev))
 
 
 def batch_som_step(dataset, model, cfg: BatchSomConfig, group=None):
@@ -79,12 +122,13 @@ def batch_som_step(dataset, model, cfg: BatchSomConfig, group=None):
         hi = _dev.to_f32(model.hi, dev).clone()
         lo = _dev.to_f32(model.lo, dev)
         g, d = hi.shape
-        acc = torch.zeros(g * d + g, dtype=torch.float64, device=dev)
+        acc = new_acc(g, d, dev)
+        fx = dataset_fx_bits(X, group)
         flag = _dev.new_flag(dev)
-        accumulate(X, hi, acc, flag=flag)
+        accumulate(X, hi, acc, fx, flag=flag)
         _dev.raise_if_nonfinite(flag)
         _allreduce_(acc, group)
-        update_landmarks_(hi, lo, acc, cfg)
+        update_landmarks_(hi, lo, acc, fx, cfg)
         return _dev.out_like(hi, want_numpy)
 
 
@@ -106,9 +150,11 @@ class FrameLoop:
         self.group = group
         self.train = train
         with torch.cuda.device(self.dev):
-            self.model = PreparedModel(hi, lo, k, device=self.dev)
+            # a private copy: training frames update the landmarks in place
+            self.model = PreparedModel(_dev.to_f32(hi, self.dev).clone(), lo, k, device=self.dev)
             g, d = self.model.hi.shape
-            self.acc = torch.zeros(g * d + g, dtype=torch.float64, device=self.dev)
+            self.acc = new_acc(g, d, self.dev)
+            self.fx = dataset_fx_bits(X, group) if train else 0
             self.qe = torch.zeros(1, dtype=torch.float64, device=self.dev)
             self.xy = torch.empty((X.shape[0], 2), dtype=torch.float32, device=self.dev)
             self.flag = _dev.new_flag(self.dev)
@@ -158,8 +204,9 @@ class FrameLoop:
             return self.xy
         self.acc.zero_()
         self.qe.zero_()
-        m.embed_into(self.X, self.xy, acc_S=self.acc, acc_C=self.acc[g * d:], qe_sum=self.qe, flag=self.flag)
+        m.embed_into(self.X, self.xy, acc_S=self.acc, acc_C=self.acc[g * d:], acc_fx=self.fx, qe_sum=self.qe,
+                     flag=self.flag)
         _allreduce_(self.acc, self.group)
-        update_landmarks_(m.hi, m.lo, self.acc, self.cfg)
+        update_landmarks_(m.hi, m.lo, self.acc, self.fx, self.cfg)
         m.update()  # re-pack tiles + pair table for the new landmarks
         return self.xy

@@ -25,6 +25,17 @@ constexpr int kThreads = 128;      // points per CTA iteration (one per thread)
 
 typedef unsigned long long f2;     // two packed f32 lanes (lo = first, hi = second)
 
+// Batch-SOM statistics are exact int64 fixed point (units of 2^-fx, two's
+// complement in unsigned atomics): integer addition is associative, so S and C
+// are independent of the accumulation order, of atomic scheduling and of how
+// the points are split across ranks -- training is bit-identical at any GPU
+// count (SURVEY §7 hard part 6).  x -> round(x 2^fx) is exact f64 arithmetic
+// (a power-of-two scale) followed by one deterministic rounding.
+typedef unsigned long long acc_t;
+__device__ __forceinline__ acc_t acc_fx(float x, double scale) {
+    return (acc_t)__double2ll_rn((double)x * scale);
+}
+
 __device__ __forceinline__ f2 f2_pack(float a, float b) {
     f2 r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));

@@ -563,7 +563,7 @@ extern "C" {
 int esom_color_channel(const float* X, int64_t n, int32_t d, int32_t color_dim, double lo, double span, uint8_t* out,
                        cudaStream_t stream) {
     if (color_dim < 0 || color_dim >= d)
-        return set_err(ESOM_ERR_PARAM, "color_dim=%lld out of range for d=%lld%s", "", color_dim, d);
+        return set_err(ESOM_ERR_PARAM, "color_dim=%lld out of range for d=%lld", (long long)color_dim, (long long)d);
     if (n <= 0) return ESOM_OK;
     color_channel_kernel<<<stream_grid(n, 256), 256, 0, stream>>>(X, n, d, color_dim, lo, span, out);
     return cuda_check("color_channel_kernel");
@@ -583,7 +583,7 @@ void* esom_mapped_device_ptr(void* host_ptr) {
 int esom_frame_points_pack(const float* xy, const uint8_t* colors, int64_t n, uint32_t frame_id, uint8_t* out,
                            cudaStream_t stream) {
     if (n < 0 || 9 + 9 * n > 0xffffffffLL)
-        return set_err(ESOM_ERR_PARAM, "frame of %lld points does not fit the u32 length field%s", "", n);
+        return set_err(ESOM_ERR_PARAM, "frame of %lld points does not fit the u32 length field", (long long)n);
     if ((((uintptr_t)out) & 15) || (((uintptr_t)xy) & 3))
         return set_err(ESOM_ERR_PARAM, "frame buffer must be 16-byte aligned%s", "");
     const int64_t chunks = (13 + 9 * n + 15) / 16;
@@ -628,7 +628,7 @@ int esom_apply_transform(const float* X, int64_t n, int32_t d, const int32_t* ki
     if (n < 0 || d < 1) return set_err(ESOM_ERR_PARAM, "bad shape%s", "");
     if (n == 0) return ESOM_OK;
     const size_t smem = (size_t)d * sizeof(ColXf);
-    if (smem > 48 * 1024) return set_err(ESOM_ERR_UNSUPPORTED, "d=%lld too large for the transform kernel%s", "", d);
+    if (smem > 48 * 1024) return set_err(ESOM_ERR_UNSUPPORTED, "d=%lld too large for the transform kernel", (long long)d);
     if ((d & 3) == 0 && !(((uintptr_t)X) & 15) && !(((uintptr_t)out) & 15)) {
         const int64_t n4 = n * d / 4;
         transform4_kernel<<<stream_grid(n4, 256), 256, smem, stream>>>(reinterpret_cast<const float4*>(X), n4, d, kind,
@@ -661,7 +661,7 @@ int esom_fit_hi(const float* hi, const float* lo, int32_t g, int32_t d, double p
                 cudaStream_t stream) {
     if (g < 1) return set_err(ESOM_ERR_INPUT, "empty model%s", "");
     const size_t smem = (size_t)g * 8;
-    if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g=%lld too large for fit_hi%s", "", g);
+    if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g=%lld too large for fit_hi", (long long)g);
     cudaFuncSetAttribute(fit_hi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     fit_hi_kernel<<<1, 1024, smem, stream>>>(hi, lo, g, d, px, py, eps, out);
     return cuda_check("fit_hi_kernel");

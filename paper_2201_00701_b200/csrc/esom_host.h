@@ -5,7 +5,8 @@
 #include <stdint.h>
 
 namespace esom_host {
-int set_err(int code, const char* fmt, const char* a = "", long long b = 0, long long c = 0);
+// printf-style message into the thread-local error string; returns code
+int set_err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int cuda_check(const char* where, int launches = 1);  // also counts our kernel launches
 int num_sms();
 int max_smem_optin();

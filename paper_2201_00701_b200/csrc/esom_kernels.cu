@@ -13,6 +13,7 @@
 //   som_tick_kernel         sequential online SOM (one CTA)               ref: som.py:44-68
 //   kmeans_tick_kernel      sequential online k-means (one CTA)           ref: graphmodel.py:87-102
 //   batch_update_kernel     batch-SOM landmark update (NEW)
+#include <cstdarg>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -37,8 +38,11 @@ namespace esom_host {
 
 thread_local char g_err[512] = "";
 
-int set_err(int code, const char* fmt, const char* a, long long b, long long c) {
-    snprintf(g_err, sizeof(g_err), fmt, a, b, c);
+int set_err(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
     return code;
 }
 
@@ -410,16 +414,16 @@ int bmu_sort(const int32_t* idx, int64_t n, int k, int g, int32_t* cntb, int32_t
 
 // Batch-SOM statistics from a BMU-sorted order (after bmu_scatter, ends[b] is
 // the end of landmark b's segment of perm): one warp per (kSegPart sorted
-// positions, 32-dim slice) sums its points' coordinates in f64 and adds one
-// partial per segment it touches to S / C (~n/64 f64 atomics per address
-// row instead of one per point and dimension; the order of the partials is
-// scheduling dependent in the last f64 bits).
+// positions, 32-dim slice) sums its points' fixed-point coordinates (exact
+// int64) and adds one partial per segment it touches to S / C (~n/64 atomics
+// per address row instead of one per point and dimension; integer sums, so
+// the order of the partials does not matter).
 constexpr int kSegPart = 64;
 
 __global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict__ X, int d,
                                                          const int32_t* __restrict__ perm,
                                                          const int32_t* __restrict__ ends, int g, int64_t n,
-                                                         double* __restrict__ S, double* __restrict__ C) {
+                                                         acc_t* __restrict__ S, acc_t* __restrict__ C, double scale) {
     // warp w sums sorted positions [w*kSegPart, (w+1)*kSegPart) (times the 32-dim
     // slices): every launched warp has work; a range crossing a BMU boundary
     // flushes one partial per segment it touches (binary search for the first)
@@ -444,7 +448,7 @@ __global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict
         int64_t pos = p0;
         while (pos < p1) {
             const int64_t e = min((int64_t)__ldg(ends + b), p1);
-            double acc = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+            acc_t acc = 0, acc1 = 0, acc2 = 0, acc3 = 0;
             if (S)
                 for (int64_t base = pos; base < e; base += 32) {  // 32 perm entries per coalesced load
                     const int pe = base + lane < e ? __ldg(perm + base + lane) : 0;
@@ -457,16 +461,16 @@ __global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict
                     }
 #pragma unroll
                     for (int q = 0; q < 32; q += 4) {
-                        acc += (double)v[q];
-                        acc1 += (double)v[q + 1];
-                        acc2 += (double)v[q + 2];
-                        acc3 += (double)v[q + 3];
+                        acc += acc_fx(v[q], scale);
+                        acc1 += acc_fx(v[q + 1], scale);
+                        acc2 += acc_fx(v[q + 2], scale);
+                        acc3 += acc_fx(v[q + 3], scale);
                     }
                 }
             acc += (acc1 + acc2) + acc3;
             if (e > pos) {
                 if (S && c < d) atomicAdd(S + (int64_t)b * d + c, acc);
-                if (C && lane == 0 && sl == 0) atomicAdd(C + b, (double)(e - pos));
+                if (C && lane == 0 && sl == 0) atomicAdd(C + b, (acc_t)(e - pos));
             }
             pos = e;
             ++b;
@@ -475,20 +479,21 @@ __global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict
 }
 
 
-// Batch-SOM statistics straight from the natural point order when the f64
+// Batch-SOM statistics straight from the natural point order when the int64
 // table fits one SM (d <= 32, g (d + 1) 8 B <= 200 KB; C3): X streams
-// coalesced, each warp adds 8 points per step into a shared-memory f64 table
-// (lane = dimension, red.shared.add.f64), then one f64 atomic per table entry
-// into S / C.  No BMU sort and no row gather (the sorted-segment kernel above
+// coalesced, each warp adds 8 points per step into a shared-memory fixed-point
+// table (lane = dimension, 64-bit shared atomics), then one atomic per table
+// entry into S / C.  No BMU sort and no row gather (the sorted-segment kernel above
 // reads X in BMU order: random 128-byte rows, ncu 1.3 TB/s at C3).
 constexpr int kAccThreads = 1024;
 
 __global__ void __launch_bounds__(kAccThreads) bmu_accum_smem_kernel(const float* __restrict__ X, int64_t n, int d,
                                                                     const int32_t* __restrict__ idx, int k, int g,
-                                                                    double* __restrict__ S, double* __restrict__ C) {
-    extern __shared__ double sS[];  // g x d, then g counts
-    double* sC = sS + (size_t)g * d;
-    for (int e = threadIdx.x; e < g * d + g; e += kAccThreads) sS[e] = 0.0;
+                                                                    acc_t* __restrict__ S, acc_t* __restrict__ C,
+                                                                    double scale) {
+    extern __shared__ acc_t sS[];  // g x d, then g counts
+    acc_t* sC = sS + (size_t)g * d;
+    for (int e = threadIdx.x; e < g * d + g; e += kAccThreads) sS[e] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * (kAccThreads / 32) + warp;
@@ -505,15 +510,15 @@ __global__ void __launch_bounds__(kAccThreads) bmu_accum_smem_kernel(const float
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             if (b[u] < 0) continue;
-            if (lane < d) atomicAdd(sS + (size_t)b[u] * d + lane, (double)v[u]);
-            if (lane == 0) atomicAdd(sC + b[u], 1.0);
+            if (lane < d) atomicAdd(sS + (size_t)b[u] * d + lane, acc_fx(v[u], scale));
+            if (lane == 0) atomicAdd(sC + b[u], 1ull);
         }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < g * d; e += kAccThreads)
-        if (S && sS[e] != 0.0) atomicAdd(S + e, sS[e]);
+        if (S && sS[e] != 0) atomicAdd(S + e, sS[e]);
     for (int j = threadIdx.x; j < g; j += kAccThreads)
-        if (C && sC[j] != 0.0) atomicAdd(C + j, sC[j]);
+        if (C && sC[j] != 0) atomicAdd(C + j, sC[j]);
 }
 
 bool accum_smem_ok(int g, int d) { return d <= 32 && ((size_t)g * d + g) * 8 <= 200 * 1024; }
@@ -698,7 +703,7 @@ __global__ void __launch_bounds__(1024) online_tick_kernel(const float* __restri
 //   den_j = sum_b H_jb C_b;  mode 0: hi_j += (alpha/B)(num_j - den_j hi_j)
 //   mode 1: hi_j = num_j / den_j (den_j > 0).
 // ---------------------------------------------------------------------------
-__global__ void batch_update_kernel(const double* __restrict__ S, const double* __restrict__ C,
+__global__ void batch_update_kernel(const acc_t* __restrict__ S, const acc_t* __restrict__ C, double inv_scale,
                                     const float* __restrict__ lo, int g, int d, double sigma, double alpha, int mode,
                                     float* __restrict__ hi) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -711,7 +716,7 @@ __global__ void batch_update_kernel(const double* __restrict__ S, const double* 
         double den_p = 0.0, b_p = 0.0;
         for (int b = threadIdx.x; b < g; b += blockDim.x) {
             const double dx = ljx - (double)lo[2 * b], dy = ljy - (double)lo[2 * b + 1];
-            const double cb = C[b];
+            const double cb = (double)(long long)C[b];
             const double hv = cb > 0.0 ? exp(-(dx * dx + dy * dy) / denom) : 0.0;
             h[b] = hv;
             den_p += hv * cb;
@@ -739,7 +744,8 @@ __global__ void batch_update_kernel(const double* __restrict__ S, const double* 
             const int c = c0 + lane;
             double num = 0.0;
             if (c < d)
-                for (int b = w; b < g; b += nw) num = fma(h[b], S[(int64_t)b * d + c], num);
+                for (int b = w; b < g; b += nw)
+                    num = fma(h[b], (double)(long long)S[(int64_t)b * d + c] * inv_scale, num);
             red2[w][lane] = num;
             __syncthreads();
             if (w == 0 && c < d) {
@@ -971,6 +977,7 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
     a.bmu = s.bmu;
     a.accS = s.accS;
     a.accC = s.accC;
+    a.acc_scale = s.acc_scale;
     a.qe_sum = s.qe_sum;
     a.flag = s.flag;
     a.stats = tc_stats_ptr();
@@ -1049,6 +1056,7 @@ int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const ch
     a.bmu = s.bmu;
     a.accS = s.accS;
     a.accC = s.accC;
+    a.acc_scale = s.acc_scale;
     a.qe_sum = s.qe_sum;
     a.flag = s.flag;
     a.stats = tc_stats_ptr();
@@ -1141,6 +1149,7 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         x.qe_sum = a.qe_sum;
         x.accS = a.accS;
         x.accC = a.accC;
+        x.acc_scale = a.acc_scale;
         x.stats = tc_stats_ptr();
         {
             KTimer tm("knn_exact_group_kernel", st);
@@ -1252,8 +1261,8 @@ static ScanArgs scan_args(const Plan& p, const float* X, int64_t n, int32_t d, c
 
 int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, int32_t k, int32_t* idx,
              float* sqd, int32_t* nonfinite_flag, void* workspace, size_t ws_bytes, cudaStream_t stream) {
-    if (n < 0 || d < 1 || g < 1) return set_err(ESOM_ERR_PARAM, "bad shape%s n=%lld d=%lld", "", n, d);
-    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
+    if (n < 0 || d < 1 || g < 1) return set_err(ESOM_ERR_PARAM, "bad shape n=%lld d=%lld", (long long)n, (long long)d);
+    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld", (long long)k, (long long)g);
     if (n == 0) return ESOM_OK;
     if (k > 64 || d > 2048) {
         int gpow = 1;
@@ -1303,7 +1312,7 @@ int esom_project(const float* X, int64_t n, int32_t d, const float* hi, const fl
 
 int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* workspace, size_t ws_bytes,
                        int32_t* nonfinite_flag, cudaStream_t stream) {
-    if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64 (got %lld)%s", "", k);
+    if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64 (got %lld)", (long long)k);
     const Plan p = make_plan(d, g, k);
     const ModelLayout m = model_layout(g, d, k, true);
     if (ws_bytes < m.total) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
@@ -1331,17 +1340,23 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
 
 int esom_embed_prepared(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
                         const void* model_ws, void* point_ws, size_t point_ws_bytes, float* xy, int32_t* bmu,
-                        double* acc_S, double* acc_C, double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
+                        int64_t* acc_S, int64_t* acc_C, int32_t acc_fx_bits, double* qe_sum, int32_t* nonfinite_flag,
+                        cudaStream_t stream) {
     return esom_embed_prepared_ex(X, n, d, hi, lo, g, k, model_ws, point_ws, point_ws_bytes, xy, bmu, acc_S, acc_C,
-                                  qe_sum, nonfinite_flag, 0, nullptr, stream);
+                                  acc_fx_bits, qe_sum, nonfinite_flag, 0, nullptr, stream);
 }
 
 int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g,
                            int32_t k, const void* model_ws, void* point_ws, size_t point_ws_bytes, float* xy,
-                           int32_t* bmu, double* acc_S, double* acc_C, double* qe_sum, int32_t* nonfinite_flag,
-                           int32_t flags, int32_t* far_count, cudaStream_t stream) {
+                           int32_t* bmu, int64_t* acc_S_, int64_t* acc_C_, int32_t acc_fx_bits, double* qe_sum,
+                           int32_t* nonfinite_flag, int32_t flags, int32_t* far_count, cudaStream_t stream) {
     const bool bmu_order = (flags & ESOM_EMBED_BMU_ORDER) != 0;
-    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
+    acc_t* acc_S = reinterpret_cast<acc_t*>(acc_S_);
+    acc_t* acc_C = reinterpret_cast<acc_t*>(acc_C_);
+    if ((acc_S || acc_C) && (acc_fx_bits < 0 || acc_fx_bits > 60))
+        return set_err(ESOM_ERR_PARAM, "acc_fx_bits=%d outside [0, 60]", (int)acc_fx_bits);
+    const double acc_scale = ldexp(1.0, acc_fx_bits);
+    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld", (long long)k, (long long)g);
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64%s", "");
     if (n == 0) return ESOM_OK;
     if (point_ws_bytes < esom_point_workspace_bytes(n, d, k))
@@ -1376,7 +1391,8 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         if (acc_smem) {
             const size_t smem = ((size_t)g * d + g) * 8;
             cudaFuncSetAttribute(bmu_accum_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            bmu_accum_smem_kernel<<<num_sms(), kAccThreads, smem, stream>>>(X + s * d, m, d, idx, k, g, acc_S, acc_C);
+            bmu_accum_smem_kernel<<<num_sms(), kAccThreads, smem, stream>>>(X + s * d, m, d, idx, k, g, acc_S, acc_C,
+                                                                             acc_scale);
             if (int e = cuda_check("bmu_accum_smem_kernel")) return e;
         }
         if (need_perm || ((acc_S || acc_C) && !acc_smem)) {
@@ -1390,7 +1406,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
             if ((acc_S || acc_C) && !acc_smem) {
                 const int64_t warps = (m + kSegPart - 1) / kSegPart * ((d + 31) / 32);
                 bmu_segsum_kernel<<<grid_for(warps * 32, 256), 256, 0, stream>>>(X + s * d, d, perm, cntb, g, m,
-                                                                                  acc_S, acc_C);
+                                                                                  acc_S, acc_C, acc_scale);
                 if (int e = cuda_check("bmu_segsum_kernel")) return e;
             }
             if (l2_table || use_rec || bmu_order) q.perm = perm;
@@ -1442,20 +1458,22 @@ size_t esom_embed_workspace_bytes(int64_t n, int32_t g, int32_t d, int32_t k) {
 }
 
 int esom_embed(const float* X, int64_t n, int32_t d, const float* hi, const float* lo, int32_t g, int32_t k,
-               void* workspace, size_t ws_bytes, float* xy, int32_t* bmu, double* acc_S, double* acc_C,
-               double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
-    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld%s", "", k, g);
+               void* workspace, size_t ws_bytes, float* xy, int32_t* bmu, int64_t* acc_S, int64_t* acc_C,
+               int32_t acc_fx_bits, double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
+    if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld", (long long)k, (long long)g);
     const size_t mb = esom_workspace_bytes(g, d, k, 1);
     if (ws_bytes < esom_embed_workspace_bytes(n, g, d, k)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
     if (int e = esom_prepare_model(hi, g, d, k, workspace, mb, nonfinite_flag, stream)) return e;
     return esom_embed_prepared(X, n, d, hi, lo, g, k, workspace, reinterpret_cast<char*>(workspace) + mb,
-                               ws_bytes - mb, xy, bmu, acc_S, acc_C, qe_sum, nonfinite_flag, stream);
+                               ws_bytes - mb, xy, bmu, acc_S, acc_C, acc_fx_bits, qe_sum, nonfinite_flag, stream);
 }
 
 int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, int32_t g, void* workspace,
-                        size_t ws_bytes, int32_t* bmu, double* acc_S, double* acc_C, double* qe_sum,
-                        int32_t* nonfinite_flag, cudaStream_t stream) {
+                        size_t ws_bytes, int32_t* bmu, int64_t* acc_S, int64_t* acc_C, int32_t acc_fx_bits,
+                        double* qe_sum, int32_t* nonfinite_flag, cudaStream_t stream) {
     if (n < 0 || d < 1 || g < 1) return set_err(ESOM_ERR_PARAM, "bad shape%s", "");
+    if ((acc_S || acc_C) && (acc_fx_bits < 0 || acc_fx_bits > 60))
+        return set_err(ESOM_ERR_PARAM, "acc_fx_bits=%d outside [0, 60]", (int)acc_fx_bits);
     if (n == 0) return ESOM_OK;
     const Plan p = make_plan(d, g, 1);
     const ModelLayout m = model_layout(g, d, 1, false);
@@ -1471,8 +1489,9 @@ int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, i
         if (int e = prepare_tc3(hi, g, d, m, ws, nonfinite_flag, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, hi, g, 1, Lt, nonfinite_flag);
     a.bmu = bmu;
-    a.accS = acc_S;
-    a.accC = acc_C;
+    a.accS = reinterpret_cast<acc_t*>(acc_S);
+    a.accC = reinterpret_cast<acc_t*>(acc_C);
+    a.acc_scale = ldexp(1.0, acc_fx_bits);
     a.qe_sum = qe_sum;
     return run_knn(p, m, a, ws, stream);
 }
@@ -1508,15 +1527,17 @@ int esom_kmeans_tick(const float* X, int32_t d, const int64_t* sample_idx, int32
     return online_tick(false, X, d, sample_idx, B, hi_inout, nullptr, g, 1.0, alpha_km, ws, ws_bytes, stream);
 }
 
-int esom_batch_som_update(const double* acc_S, const double* acc_C, const float* lo, int32_t g, int32_t d,
-                          double sigma, double alpha, int32_t mode, float* hi_inout, cudaStream_t stream) {
+int esom_batch_som_update(const int64_t* acc_S, const int64_t* acc_C, int32_t acc_fx_bits, const float* lo, int32_t g,
+                          int32_t d, double sigma, double alpha, int32_t mode, float* hi_inout, cudaStream_t stream) {
     if (!(sigma > 0)) return set_err(ESOM_ERR_PARAM, "sigma must be > 0%s", "");
+    if (acc_fx_bits < 0 || acc_fx_bits > 60) return set_err(ESOM_ERR_PARAM, "acc_fx_bits=%d outside [0, 60]", (int)acc_fx_bits);
     const size_t smem = (size_t)g * 8;
     if (smem > (size_t)max_smem_optin()) return set_err(ESOM_ERR_UNSUPPORTED, "g too large%s", "");
     cudaFuncSetAttribute(batch_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = 256;
-    batch_update_kernel<<<g < num_sms() * 4 ? g : num_sms() * 4, threads, smem, stream>>>(acc_S, acc_C, lo, g, d, sigma,
-                                                                                          alpha, mode, hi_inout);
+    batch_update_kernel<<<g < num_sms() * 4 ? g : num_sms() * 4, threads, smem, stream>>>(
+        reinterpret_cast<const acc_t*>(acc_S), reinterpret_cast<const acc_t*>(acc_C), ldexp(1.0, -acc_fx_bits), lo, g, d,
+        sigma, alpha, mode, hi_inout);
     return cuda_check("batch_update_kernel");
 }
 

@@ -247,13 +247,13 @@ __global__ void __launch_bounds__(kThreads) knn_scan_kernel(ScanArgs a) {
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         if (a.accS) {
-            atomicAdd(a.accC + b0, 1.0);
+            atomicAdd(a.accC + b0, 1ull);
             if (a.nch == 1) {
 #pragma unroll
                 for (int c = 0; c < DC; ++c)
-                    if (c < a.d) atomicAdd(a.accS + (int64_t)b0 * a.d + c, (double)x[c]);
+                    if (c < a.d) atomicAdd(a.accS + (int64_t)b0 * a.d + c, acc_fx(x[c], a.acc_scale));
             } else {
-                for (int c = 0; c < a.d; ++c) atomicAdd(a.accS + (int64_t)b0 * a.d + c, (double)a.X[i * a.d + c]);
+                for (int c = 0; c < a.d; ++c) atomicAdd(a.accS + (int64_t)b0 * a.d + c, acc_fx(a.X[i * a.d + c], a.acc_scale));
             }
         }
     }

@@ -16,8 +16,9 @@ struct ScanArgs {
     int32_t* out_idx;        // n×k (nullable: statistics only)
     float* out_sqd;          // n×k
     int32_t* bmu;            // n   (nullable)
-    double* accS;            // g×d batch-SOM sums (nullable)
-    double* accC;            // g   counts as f64 (nullable)
+    unsigned long long* accS;  // g×d batch-SOM sums, int64 fixed point x 2^fx (nullable)
+    unsigned long long* accC;  // g   counts (int64, nullable)
+    double acc_scale;          // 2^fx
     double* qe_sum;          // sum of nearest squared distances (nullable)
     int32_t* flag;           // non-finite input flag
     float nz;                // -0.0f, opaque to ptxas
@@ -57,8 +58,9 @@ struct TcArgs {
     int32_t* out_idx;
     float* out_sqd;
     int32_t* bmu;
-    double* accS;
-    double* accC;
+    unsigned long long* accS;
+    unsigned long long* accC;
+    double acc_scale;
     double* qe_sum;
     int32_t* flag;
     int32_t* stats;          // [0] += candidates examined exactly (diagnostic, nullable)
@@ -80,8 +82,9 @@ struct Tc2Args {
     int32_t* out_idx;
     float* out_sqd;
     int32_t* bmu;
-    double* accS;
-    double* accC;
+    unsigned long long* accS;
+    unsigned long long* accC;
+    double acc_scale;
     double* qe_sum;
     int32_t* flag;
     int32_t* stats;          // [0] += logged candidates, [1] += slow-path points (diagnostic, nullable)
@@ -124,8 +127,9 @@ struct T3ExactArgs {
     float* out_sqd;
     int32_t* bmu;
     double* qe_sum;
-    double* accS;
-    double* accC;
+    unsigned long long* accS;
+    unsigned long long* accC;
+    double acc_scale;
     int32_t* stats;          // diagnostic: [2] += union sizes, [3] += groups evaluated, [4] += splits
 };
 

@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) knn_tc_kernel(TcArgs a) {
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         if (a.accS) {
-            atomicAdd(a.accC + b0, 1.0);
-            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)myx[c]);
+            atomicAdd(a.accC + b0, 1ull);
+            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(myx[c], a.acc_scale));
         }
     }
     flag_nonfinite(a.flag, bad);

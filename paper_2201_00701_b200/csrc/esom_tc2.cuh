@@ -566,8 +566,8 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         if (a.accS) {
-            atomicAdd(a.accC + b0, 1.0);
-            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(a.X + i * d + c));
+            atomicAdd(a.accC + b0, 1ull);
+            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(__ldg(a.X + i * d + c), a.acc_scale));
         }
     }
     flag_nonfinite(a.flag, bad);
@@ -847,8 +847,8 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         if (a.accS) {
-            atomicAdd(a.accC + b0, 1.0);
-            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(a.X + i * d + c));
+            atomicAdd(a.accC + b0, 1ull);
+            for (int c = 0; c < d; ++c) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(__ldg(a.X + i * d + c), a.acc_scale));
         }
     }
     if (a.stats && slow_local) atomicAdd(a.stats + 1, slow_local);

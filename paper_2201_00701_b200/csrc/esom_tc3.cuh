@@ -528,10 +528,10 @@ __global__ void __launch_bounds__(kT3ExactWarps * 32) knn_exact_warp_kernel(T3Ex
         if (lane == 0) {
             if (a.bmu) a.bmu[i] = b0;
             if (a.qe_sum) qe_local += (double)d0;
-            if (a.accC) atomicAdd(a.accC + b0, 1.0);
+            if (a.accC) atomicAdd(a.accC + b0, 1ull);
         }
         if (a.accS)
-            for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(xr + c));
+            for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(__ldg(xr + c), a.acc_scale));
         __syncwarp();
     }
     if (a.qe_sum && lane == 0 && qe_local != 0.0) atomicAdd(a.qe_sum, qe_local);
@@ -753,10 +753,10 @@ __global__ void __launch_bounds__(kT3GWarps * 32, 2) knn_exact_group_kernel(T3Ex
                 if (lane == 0) {
                     if (a.bmu) a.bmu[i] = b0;
                     if (a.qe_sum) qe_local += (double)d0;
-                    if (a.accC) atomicAdd(a.accC + b0, 1.0);
+                    if (a.accC) atomicAdd(a.accC + b0, 1ull);
                 }
                 if (a.accS)
-                    for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)xs[p * dpad + c]);
+                    for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(xs[p * dpad + c], a.acc_scale));
             }
         }
         // ---- points the screen could not bound (log overflow / too few candidates): reference scan ----
@@ -773,11 +773,11 @@ __global__ void __launch_bounds__(kT3GWarps * 32, 2) knn_exact_group_kernel(T3Ex
                 b0 = sn.b0;
                 if (a.bmu) a.bmu[i] = b0;
                 if (a.qe_sum) qe_local += (double)sn.d0;
-                if (a.accC) atomicAdd(a.accC + b0, 1.0);
+                if (a.accC) atomicAdd(a.accC + b0, 1ull);
             }
             b0 = __shfl_sync(0xffffffffu, b0, 0);
             if (a.accS)
-                for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, (double)__ldg(xr + c));
+                for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(__ldg(xr + c), a.acc_scale));
         }
         __syncwarp();
     }

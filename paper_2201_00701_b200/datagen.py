@@ -75,3 +75,36 @@ def gaussians_f32(c: int, n: int, d: int, seed: int, chunk: int = 1 << 18) -> np
     for s, blk in gaussians_chunks(c, n, d, seed, chunk):
         out[s:s + blk.shape[0]] = blk
     return out
+
+
+def gaussians_slice(c: int, n: int, d: int, seed: int, start: int, stop: int, pick=None,
+                    chunk: int = 1 << 18, sd: float = 0.5, center_span: float = 10.0):
+    """Rows [start, stop) of ``gaussians(c, n, d, seed)[0]`` plus the rows at
+    indices ``pick`` (any positions in [0, n)), without materialising the
+    other rows: the Philox stream is consumed block by block up to
+    max(stop, max(pick)) and only the wanted rows are kept.  One rank's
+    contiguous shard of the SURVEY §8d dataset, and the landmark rows every
+    rank must agree on."""
+    pick = np.asarray([] if pick is None else pick, np.int64)
+    out = np.empty((stop - start, d), np.float32)
+    picked = np.empty((pick.shape[0], d), np.float32)
+    end = max(stop, int(pick.max()) + 1 if pick.size else 0)
+    rng = Rng(seed)
+    centers = rng.uniform(0.0, center_span, size=(c, d))
+    labels = rng.integers(0, c, size=n)
+    for s in range(0, end, chunk):
+        m = min(chunk, n - s)
+        noise = rng.normal(0.0, 1.0, size=(m, d)) * sd
+        blk = (centers[labels[s:s + m]] + noise).astype(np.float32)
+        lo_, hi_ = max(s, start), min(s + m, stop)
+        if lo_ < hi_:
+            out[lo_ - start:hi_ - start] = blk[lo_ - s:hi_ - s]
+        sel = np.nonzero((pick >= s) & (pick < s + m))[0]
+        if sel.size:
+            picked[sel] = blk[pick[sel] - s]
+    return out, picked
+
+
+def som_model_rows(n: int, rows: int, cols: int, seed: int) -> np.ndarray:
+    """The dataset row indices ``som_model`` draws for hi (Rng(seed).choice_distinct)."""
+    return Rng(seed).choice_distinct(n, rows * cols)

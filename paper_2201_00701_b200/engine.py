@@ -31,6 +31,7 @@ import torch
 from . import _dev, _lib
 from .core import BITONIC_K_CHOICES, EmbedParams, InputError, LandmarkModel, ParameterError, Rng, points_of
 from .graphmodel import KmeansConfig, kmeans_tick
+from .knn import _run_knn
 from .projection import PreparedModel
 from .protocol import FrameBuffer, frame_points_bytes, pack_frame_points
 from .som import SomConfig, som_tick
@@ -170,13 +171,28 @@ class DeviceSession:
         self._pm_key = (hi, lo)  # the objects themselves: identity, never a recycled id()
         return self._pm
 
-    def embed(self, hi, lo, params: EmbedParams, backend: str = "bitonic", start: int = 0, stop=None) -> torch.Tensor:
-        """Re-project rows [start, stop) of the resident points (all by default)."""
+    def embed(self, hi, lo, params: EmbedParams, backend: str = "bitonic", start: int = 0, stop=None,
+              mode: str = "fast") -> torch.Tensor:
+        """Re-project rows [start, stop) of the resident points (all by default).
+        ``mode="faithful"``: k-NN -> scores -> the reference's projection
+        arithmetic op for op (what ``embed(mode="faithful")`` computes)."""
         g = int(np.shape(hi)[0])
         params.validate(g, backend)
         if backend not in ("base", "bitonic"):
             raise ParameterError(f"unknown knn backend {backend!r}")
         stop = self.n if stop is None else stop
+        if mode == "faithful":
+            from .projection import _project_dev, _scores_dev
+
+            with torch.cuda.device(self.device):
+                if stop > start:
+                    H, Lo = _dev.to_f32(hi, self.device), _dev.to_f32(lo, self.device)
+                    Xs = self.X[start:stop]
+                    nb = _run_knn(Xs, H, params.k)
+                    self.positions[start:stop] = _project_dev(Xs, H, Lo, nb.indices, _scores_dev(nb.sqdists))
+            return self.positions
+        if mode != "fast":
+            raise ParameterError(f"unknown projection mode {mode!r}")
         with torch.cuda.device(self.device):
             self._update_order()
             pm = self.prepared(hi, lo, params.k)
@@ -438,14 +454,15 @@ def gpu_tick(self):
 
     n = st.dataset.n
     if getattr(self, "full_reprojection", True) or n <= self.chunk_size:
-        sess.embed(st.model.hi, st.model.lo, st.embed_params, self.backend)
+        sess.embed(st.model.hi, st.model.lo, st.embed_params, self.backend, mode=getattr(self, "embed_mode", "fast"))
         st.chunk_cursor = 0
     else:
         if getattr(self, "_b200_positions", None) is not self._positions:
             sess.positions.zero_()  # the reference re-initialised its position buffer (ref: engine.py:229-230)
         start = st.chunk_cursor
         stop = min(start + self.chunk_size, n)
-        sess.embed(st.model.hi, st.model.lo, st.embed_params, self.backend, start, stop)
+        sess.embed(st.model.hi, st.model.lo, st.embed_params, self.backend, start, stop,
+                   mode=getattr(self, "embed_mode", "fast"))
         st.chunk_cursor = 0 if stop >= n else stop
     self._positions = self._b200_positions = sess.positions_host()
 

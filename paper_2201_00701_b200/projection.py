@@ -71,7 +71,7 @@ def projection_system(x_i, model, nbr_indices, s):
     lo = np.asarray(model.lo, np.float64)
     x = np.asarray(x_i, np.float64).ravel()
     idx = np.asarray(nbr_indices, np.int64).ravel()
-    sc = np.asarray(s.scores if isinstance(s, ScoreVector) else s, np.float64).ravel()
+    sc = np.asarray(getattr(s, "scores", s), np.float64).ravel()
     a = np.zeros((2, 2))
     c = np.zeros(2)
     k = idx.shape[0]
@@ -117,7 +117,7 @@ def project_point(x_i, model, nbr_indices, s) -> np.ndarray:
     if x.shape[1] != model.hi.shape[1]:
         raise InputError(f"point has {x.shape[1]} dims, model expects {model.hi.shape[1]}")
     idx = np.ascontiguousarray(nbr_indices, dtype=np.int32).reshape(1, -1)
-    sc = np.ascontiguousarray(np.asarray(s.scores if isinstance(s, ScoreVector) else s, np.float64)).reshape(1, -1)
+    sc = np.ascontiguousarray(np.asarray(getattr(s, "scores", s), np.float64)).reshape(1, -1)
     if idx.shape[1] != sc.shape[1]:
         raise InputError("neighbor row and score vector lengths differ")
     if idx.shape[1] < 3:
@@ -176,18 +176,20 @@ class PreparedModel:
             self.pws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         return self.pws
 
-    def embed_into(self, X: torch.Tensor, xy: torch.Tensor, *, bmu=None, acc_S=None, acc_C=None, qe_sum=None,
-                   flag=None, stream=None, bmu_order: bool = False, far_count=None) -> None:
+    def embed_into(self, X: torch.Tensor, xy: torch.Tensor, *, bmu=None, acc_S=None, acc_C=None, acc_fx: int = 0,
+                   qe_sum=None, flag=None, stream=None, bmu_order: bool = False, far_count=None) -> None:
         """Asynchronous embed of device points X (n×d f32) into xy (n×2 f32):
-        k-NN scan + projection kernels per L2-resident chunk.  ``bmu_order``
-        visits the projection in nearest-landmark order; ``far_count`` (device
-        int32) accumulates the points that took the f64 far-point path."""
+        k-NN + projection kernels per L2-resident chunk.  ``acc_S`` / ``acc_C``
+        (int64, nullable) receive the batch-SOM statistics in fixed point with
+        ``acc_fx`` fractional bits.  ``bmu_order`` visits the projection in
+        nearest-landmark order; ``far_count`` (device int32) accumulates the
+        points that took the f64 far-point path."""
         n, d = X.shape
         st = stream if stream is not None else _dev.stream_handle(self.device)
         pws = self.point_workspace(n)
         _lib.call("esom_embed_prepared_ex", _dev.ptr(X), n, d, _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.k,
                   _dev.ptr(self.ws), _dev.ptr(pws), pws.numel(), _dev.ptr(xy), _dev.ptr(bmu), _dev.ptr(acc_S),
-                  _dev.ptr(acc_C), _dev.ptr(qe_sum), _dev.ptr(flag if flag is not None else self.flag),
+                  _dev.ptr(acc_C), int(acc_fx), _dev.ptr(qe_sum), _dev.ptr(flag if flag is not None else self.flag),
                   1 if bmu_order else 0, _dev.ptr(far_count), st)
 
 
@@ -211,12 +213,11 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
     k = params.k
     want_numpy = not _dev.is_device_tensor(points)
     dev = _dev.cuda_device(points)
-    if (isinstance(points, torch.Tensor) and not points.is_cuda and points.is_pinned() and mode == "fast"
-            and k <= 64 and points.dtype == torch.float32 and points.is_contiguous()
-            and ps[0] >= 2 * _pipe_chunk(model.hi.shape[0])
-            and not chunk_size):
-        with torch.cuda.device(dev):
-            return _embed_host_pipelined(points, model, k, dev)
+    if mode == "fast" and k <= 64 and not chunk_size and ps[0] >= 2 * _pipe_chunk(g):
+        host = _pipelinable_host(points)
+        if host is not None:
+            with torch.cuda.device(dev):
+                return _embed_host_pipelined(host, model, k, dev)
     with torch.cuda.device(dev):
         X = _dev.to_f32(points, dev)
         n = X.shape[0]
@@ -252,13 +253,30 @@ def _pipe_chunk(g: int) -> int:
     return PIPE_CHUNK or (1 << 17 if g <= 256 else 1 << 18)
 
 
-def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
-    """embed() for pinned host points: chunked H2D on one copy stream, the
-    kernels on the compute stream and the D2H of finished chunks on a second
-    copy stream (PCIe is full duplex), with PIPE_DEPTH rotating device
-    buffers, so the end-to-end time approaches max(H2D, compute) instead of
-    their sum.  (A ramp of smaller first stages measured slower: the fixed
-    per-stage cost outweighs the shorter pipeline fill.)"""
+def _pipelinable_host(points):
+    """Host inputs the chunked pipeline takes: a pinned f32 torch tensor (DMA
+    straight from it) or a C-contiguous f32 numpy array -- the reference's own
+    calling convention -- staged through pinned chunks.  Anything else (other
+    dtypes, strided arrays) takes the one-shot conversion path."""
+    if isinstance(points, torch.Tensor):
+        if (not points.is_cuda and points.dtype == torch.float32 and points.is_contiguous()
+                and points.is_pinned()):
+            return points
+        return None
+    if isinstance(points, np.ndarray) and points.dtype == np.float32 and points.flags.c_contiguous:
+        return points
+    return None
+
+
+def _embed_host_pipelined(host, model, k: int, dev) -> np.ndarray:
+    """embed() for host points: chunked H2D on one copy stream, the kernels on
+    the compute stream and the D2H of finished chunks on a second copy stream
+    (PCIe is full duplex), with PIPE_DEPTH rotating device buffers, so the end
+    -to-end time approaches max(H2D, compute) instead of their sum.  A numpy
+    input (pageable) is first copied by host threads into a ring of pinned
+    staging chunks (a chunk is rewritten only after its previous H2D ran).
+    (A ramp of smaller first stages measured slower: the fixed per-stage
+    cost outweighs the shorter pipeline fill.)"""
     n, d = host.shape
     pm = PreparedModel(model.hi, model.lo, k, device=dev)
     flag = _dev.new_flag(dev)
@@ -268,23 +286,32 @@ def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
     c = min(_pipe_chunk(model.hi.shape[0]), n)
     nb = PIPE_DEPTH
     Xd, Yd, fresh = _pipe_buffers(dev, nb, c, d)
+    staged = isinstance(host, np.ndarray)
+    if staged:
+        stage = _pinned_stage(nb, c, d)
+        stage_free = [None] * nb  # H2D that last read stage slot b
     if fresh:
         h2d.wait_stream(comp)  # new allocations: order after prior work on the compute stream
     loaded = [torch.cuda.Event() for _ in range(nb)]
     computed = [None] * nb  # compute of the chunk that last used buffer b (Xd[b] free, Yd[b] ready)
     drained = [None] * nb   # D2H of the chunk that last used buffer b (Yd[b] free)
-    stages, s, m = [], 0, c
-    while s < n:
-        stages.append((s, min(m, n - s)))
-        s += m
-        m = min(2 * m, c)
-    for it, (s, m) in enumerate(stages):
+    for it, s in enumerate(range(0, n, c)):
+        m = min(c, n - s)
         b = it % nb
         if computed[b] is not None:
             h2d.wait_event(computed[b])
+        if staged:
+            if stage_free[b] is not None:
+                stage_free[b].synchronize()
+            _host_copy(stage[b][:m].numpy(), host[s:s + m])
+            src = stage[b][:m]
+        else:
+            src = host[s:s + m]
         with torch.cuda.stream(h2d):
-            Xd[b][:m].copy_(host[s:s + m], non_blocking=True)
+            Xd[b][:m].copy_(src, non_blocking=True)
         loaded[b].record(h2d)
+        if staged:
+            stage_free[b] = loaded[b]
         comp.wait_event(loaded[b])
         if drained[b] is not None:
             comp.wait_event(drained[b])
@@ -305,27 +332,59 @@ def _embed_host_pipelined(host: torch.Tensor, model, k: int, dev) -> np.ndarray:
     return out.numpy()
 
 
-_PIPE_BUFS: dict = {}
+_COPY_POOL = None
+
+
+def _host_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """Pageable -> pinned copy of one stage, split over host threads (numpy
+    releases the GIL inside the copy loop)."""
+    global _COPY_POOL
+    parts = 4
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _COPY_POOL = ThreadPoolExecutor(parts, thread_name_prefix="esom-stage")
+    m = src.shape[0]
+    step = (m + parts - 1) // parts
+    futs = [_COPY_POOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, m, step)]
+    for f in futs:
+        f.result()
+
+
+def _pinned_stage(nb: int, c: int, d: int):
+    """Pinned host staging ring of the numpy-input pipeline, per thread."""
+    cache = getattr(_dev._tls, "pinned_stage", None)
+    key = (nb, c, d)
+    if cache is None or cache[0] != key:
+        cache = _dev._tls.pinned_stage = (key, [torch.empty((c, d), dtype=torch.float32, pin_memory=True)
+                                                for _ in range(nb)])
+    return cache[1]
 
 
 def _pipe_buffers(dev, nb: int, c: int, d: int):
-    """Device staging buffers of the host pipeline, kept across calls (the
-    synchronous return of the pipeline guarantees they are idle)."""
+    """Device staging buffers of the host pipeline, kept across calls per
+    (thread, device) -- two threads embedding pinned inputs on one device
+    never share them; the synchronous return of the pipeline guarantees the
+    calling thread's buffers are idle."""
+    cache = getattr(_dev._tls, "pipe_bufs", None)
+    if cache is None:
+        cache = _dev._tls.pipe_bufs = {}
     key = (str(dev), nb, c, d)
-    fresh = key not in _PIPE_BUFS
+    fresh = key not in cache
     if fresh:
-        _PIPE_BUFS.clear()
-        _PIPE_BUFS[key] = ([torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(nb)],
-                           [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(nb)])
-    Xd, Yd = _PIPE_BUFS[key]
+        cache.clear()
+        cache[key] = ([torch.empty((c, d), dtype=torch.float32, device=dev) for _ in range(nb)],
+                      [torch.empty((c, 2), dtype=torch.float32, device=dev) for _ in range(nb)])
+    Xd, Yd = cache[key]
     return Xd, Yd, fresh
 
 
-_COPY_STREAMS: dict = {}
-
-
 def _copy_streams(dev):
+    """H2D and D2H copy streams of the host pipeline, per (thread, device)."""
+    cache = getattr(_dev._tls, "copy_streams", None)
+    if cache is None:
+        cache = _dev._tls.copy_streams = {}
     key = (dev.index if isinstance(dev, torch.device) else int(dev))
-    if key not in _COPY_STREAMS:
-        _COPY_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    return _COPY_STREAMS[key]
+    if key not in cache:
+        cache[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return cache[key]

@@ -55,13 +55,21 @@ def _online_tick(kind: str, dataset, model, sample_idx, a: float, sigma: float =
     want_numpy = not _dev.is_device_tensor(pts)
     dev = _dev.cuda_device(pts)
     with torch.cuda.device(dev):
-        X = _dev.to_f32(pts, dev)
         hi = _dev.to_f32(model.hi, dev).clone()
         g, d = hi.shape
-        if X.shape[1] != d:
-            raise InputError(f"points have d={X.shape[1]}, model has d={d}")
-        sidx = _dev.to_dev_async(np.asarray(sample_idx, np.int64), dev) if not isinstance(
-            sample_idx, torch.Tensor) else sample_idx.to(device=dev, dtype=torch.int64).contiguous()
+        if pts.shape[1] != d:
+            raise InputError(f"points have d={pts.shape[1]}, model has d={d}")
+        if want_numpy and not isinstance(sample_idx, torch.Tensor):
+            # host dataset: the tick reads only the sampled rows, so gather them on the
+            # host and upload B×d (not the whole n×d matrix every tick); same sample
+            # order, so the sequential update is unchanged
+            rows = np.asarray(pts, dtype=np.float32)[np.asarray(sample_idx, np.int64)]
+            X = _dev.to_dev_async(np.ascontiguousarray(rows), dev)
+            sidx = _dev.to_dev_async(np.arange(rows.shape[0], dtype=np.int64), dev)
+        else:
+            X = _dev.to_f32(pts, dev)
+            sidx = _dev.to_dev_async(np.asarray(sample_idx, np.int64), dev) if not isinstance(
+                sample_idx, torch.Tensor) else sample_idx.to(device=dev, dtype=torch.int64).contiguous()
         nb = _lib.load().esom_tick_workspace_bytes(g, d)
         ws = _dev.workspace(dev, nb, slot="tick")
         st = _dev.stream_handle(dev)
@@ -95,7 +103,7 @@ def quantization_error(dataset, hi) -> float:
         qe = torch.zeros(1, dtype=torch.float64, device=dev)
         flag = _dev.new_flag(dev)
         ws = _dev.workspace(dev, _lib.load().esom_workspace_bytes(g, d, 1, 0))
-        _lib.call("esom_bmu_accumulate", _dev.ptr(X), n, d, _dev.ptr(H), g, _dev.ptr(ws), ws.numel(), 0, 0, 0,
+        _lib.call("esom_bmu_accumulate", _dev.ptr(X), n, d, _dev.ptr(H), g, _dev.ptr(ws), ws.numel(), 0, 0, 0, 0,
                   _dev.ptr(qe), _dev.ptr(flag), _dev.stream_handle(dev))
         _dev.raise_if_nonfinite(flag)
         return float(qe.item()) / max(n, 1)

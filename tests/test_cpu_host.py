@@ -81,6 +81,9 @@ def test_rng_matches_reference_stream(golden):
     assert np.array_equal(Rng(7).integers(0, 1 << 20, size=256), golden["c3_som_sample"])
 
 
+_FX = 36  # fractional bits of the fixed-point statistics in the world-2 test
+
+
 def _gloo_worker(rank, world, port, result_path):
     import torch
     import torch.distributed as dist
@@ -94,12 +97,12 @@ def _gloo_worker(rank, world, port, result_path):
     g = np.load(ROOT / "tests" / "golden" / "golden.npz")
     pts, hi, lo = g["small_points"], g["small_hi0"], g["small_lo"]
     shard = np.array_split(np.arange(pts.shape[0]), world)[rank]
-    S, C = oracle.batch_som_accumulate(pts[shard], hi)
-    acc = torch.from_numpy(np.concatenate([S.ravel(), C.astype(np.float64)]))
+    fx = _FX
+    S, C = oracle.batch_som_accumulate_fx(pts[shard], hi, fx)
+    acc = torch.from_numpy(np.concatenate([S.ravel(), C]))  # int64 [S | C], as FrameLoop packs it
     _allreduce_(acc)  # the same call the device FrameLoop issues (NCCL there)
     gd = hi.size
-    new_hi = oracle.batch_som_update(acc[:gd].numpy().reshape(hi.shape), acc[gd:].numpy().astype(np.int64),
-                                     lo, hi, 0.9, 0.3)
+    new_hi = oracle.batch_som_update_fx(acc[:gd].numpy().reshape(hi.shape), acc[gd:].numpy(), fx, lo, hi, 0.9, 0.3)
     if rank == 0:
         np.save(result_path, new_hi)
     dist.barrier()
@@ -114,8 +117,26 @@ def test_sharded_batch_som_gloo_world2(tmp_path, golden):
     out = tmp_path / "hi.npy"
     mp.spawn(_gloo_worker, args=(2, port, str(out)), nprocs=2, join=True)
     sharded = np.load(out)
-    full = oracle.batch_som_step(golden["small_points"], golden["small_hi0"], golden["small_lo"], 0.9, 0.3)
+    pts, hi, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+    S, C = oracle.batch_som_accumulate_fx(pts, hi, _FX)
+    whole = oracle.batch_som_update_fx(S, C, _FX, lo, hi, 0.9, 0.3)
+    # exact integer statistics: the sharded step is bit-identical to the single-rank one
+    assert np.array_equal(sharded, whole)
+    # and the fixed-point rounding (2^-_FX) stays far inside f32 against the f64 restatement
+    full = oracle.batch_som_step(pts, hi, lo, 0.9, 0.3)
     np.testing.assert_allclose(sharded, full, rtol=1e-6, atol=1e-7)
+
+
+def test_acc_fx_bits_bounds():
+    from paper_2201_00701_b200.batch_som import acc_fx_bits
+    from paper_2201_00701_b200.core import ParameterError
+
+    assert acc_fx_bits(0.0, 10) == 40 and acc_fx_bits(15.0, 10_000_000) == 33
+    for mx, n in ((15.0, 10_000_000), (262144.0, 10_000_000), (1e-3, 1000)):
+        fx = acc_fx_bits(mx, n)
+        assert n * mx * 2.0 ** fx < 2.0 ** 62  # the int64 sum cannot overflow
+    with pytest.raises(ParameterError):
+        acc_fx_bits(1e30, 10)
 
 
 def _gloo_gather_worker(rank, world, port, result_path):
@@ -169,4 +190,4 @@ def test_bench_reference_arm_runs_on_cpu():
     assert res.returncode == 0, res.stderr
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["e2e"]["h2d_bytes_per_step"] == 0
