@@ -158,6 +158,12 @@ class FrameLoop:
             self.qe = torch.zeros(1, dtype=torch.float64, device=self.dev)
             self.xy = torch.empty((X.shape[0], 2), dtype=torch.float32, device=self.dev)
             self.flag = _dev.new_flag(self.dev)
+            self.far = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # projection visiting order: nearest-landmark order pays off when most points
+        # take the far-point path (trained SOMs; see DeviceSession._update_order);
+        # decided from the first eager frames' census, then fixed (graph replays)
+        self.bmu_order = False
+        self._census_frames = 2
 
     @property
     def launches_per_frame(self) -> int:
@@ -179,6 +185,8 @@ class FrameLoop:
 
         self._eager_frame()
         torch.cuda.synchronize(self.dev)
+        self._census()
+        self._census_frames = 0
         n0 = L.load().esom_launch_count()
         g = torch.cuda.CUDAGraph()
         # thread_local: the NCCL watchdog thread (multi-rank runs) may touch the
@@ -194,18 +202,30 @@ class FrameLoop:
         if g is not None:
             g.replay()
             return self.xy
-        return self._eager_frame()
+        xy = self._eager_frame()
+        if self._census_frames > 0:
+            self._census_frames -= 1
+            self._census()
+        return xy
+
+    def _far_arg(self):
+        return self.far if self._census_frames > 0 else None
+
+    def _census(self) -> None:
+        """Far-point census of the last frame (one 4-byte read) -> visiting order."""
+        self.bmu_order = 2 * int(self.far.item()) > self.X.shape[0]
+        self.far.zero_()
 
     def _eager_frame(self) -> torch.Tensor:
         m = self.model
         g, d = m.hi.shape
         if not self.train:
-            m.embed_into(self.X, self.xy, flag=self.flag)
+            m.embed_into(self.X, self.xy, flag=self.flag, bmu_order=self.bmu_order, far_count=self._far_arg())
             return self.xy
         self.acc.zero_()
         self.qe.zero_()
         m.embed_into(self.X, self.xy, acc_S=self.acc, acc_C=self.acc[g * d:], acc_fx=self.fx, qe_sum=self.qe,
-                     flag=self.flag)
+                     flag=self.flag, bmu_order=self.bmu_order, far_count=self._far_arg())
         _allreduce_(self.acc, self.group)
         update_landmarks_(m.hi, m.lo, self.acc, self.fx, self.cfg)
         m.update()  # re-pack tiles + pair table for the new landmarks

@@ -829,8 +829,14 @@ int grid_for(int64_t work, int threads) {
     return (int)b;
 }
 
+// hi -> f64 (exact widening), once per model
+__global__ void widen_kernel(const float* __restrict__ src, int64_t n, double* __restrict__ dst) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        dst[e] = (double)src[e];
+}
+
 struct ModelLayout {
-    size_t lt, tri, bhi, blo, ln, lstats, lrow, rec, total;
+    size_t lt, tri, bhi, blo, ln, lstats, lrow, rec, hi64, total;
     bool has_rec;  // g x g pair records for project_reg3_kernel (k <= 16, g <= 1024)
     int d16, gpad, ls;
     // tensor-core GEMM screen for d > 32 (esom_tc3.cuh): per-model operands + per-chunk scratch
@@ -872,6 +878,8 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
         m.ls = (((m.d16 + 3) / 4) | 1) * 4;
         o += a256((size_t)m.gpad * m.ls * 4);
     }
+    m.hi64 = o;  // f64 copy of hi: the far-point distances of the projection (precise_sqd)
+    if (with_pairs) o += a256((size_t)g * d * 8);
     m.t2chunk = 0;
     if (d <= 32 && m.gpad <= 1024) {
         m.t2chunk = 1 << 20;
@@ -1331,6 +1339,9 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
         pair_table_kernel<<<grid_for((int64_t)g * g, 256), 256, 0, stream>>>(hi, g, d, T, tmax);
     }
     if (int e = cuda_check("pair_table")) return e;
+    widen_kernel<<<grid_for((int64_t)g * d, 256), 256, 0, stream>>>(hi, (int64_t)g * d,
+                                                                    reinterpret_cast<double*>(ws + m.hi64));
+    if (int e = cuda_check("widen_hi")) return e;
     if (tc_eligible(1 << 20, d, g, k))
         if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
     if (m.t3 && t3_enabled())
@@ -1423,6 +1434,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         q.xy = xy + 2 * s;
         q.X = X + s * d;
         q.hi = hi;
+        q.hi64 = reinterpret_cast<const double*>(mws + ml.hi64);
         q.d = d;
         q.rec = use_rec ? rec : nullptr;
         {

@@ -124,8 +124,11 @@ __device__ __forceinline__ void count_prec(int32_t* cnt, bool prec) {
 
 
 template <int KP>
-__device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, const float* __restrict__ hi,
+__device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, const double* __restrict__ hi64,
                                             const int (&jj)[KP], int k, float (&qe)[KP]) {
+    // landmark rows come pre-widened (model workspace), so the only f32 -> f64
+    // conversions are x's: 2 per dimension pair per chunk of neighbours (the
+    // per-element F2F of both operands used to dominate trained-model frames)
     constexpr int QC = KP < 8 ? KP : 8;  // neighbours per pass (bounds the live f64 accumulators)
     double s0 = 0.0;
 #pragma unroll
@@ -133,20 +136,17 @@ __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, 
         double acc[QC];
 #pragma unroll
         for (int q = 0; q < QC; ++q) acc[q] = 0.0;
-        if ((d & 3) == 0) {
-            for (int c = 0; c < d; c += 4) {
-                const float4 xv = __ldg(reinterpret_cast<const float4*>(x + c));
+        if ((d & 1) == 0) {
+            for (int c = 0; c < d; c += 2) {
+                const float2 xv = __ldg(reinterpret_cast<const float2*>(x + c));
+                const double x0 = (double)xv.x, x1 = (double)xv.y;
 #pragma unroll
                 for (int q = 0; q < QC; ++q) {
                     if (q0 + q < k) {
-                        const float4 hv = __ldg(reinterpret_cast<const float4*>(hi + (int64_t)jj[q0 + q] * d + c));
-                        double t = (double)xv.x - (double)hv.x;
+                        const double2 hv = __ldg(reinterpret_cast<const double2*>(hi64 + (int64_t)jj[q0 + q] * d + c));
+                        double t = x0 - hv.x;
                         acc[q] = fma(t, t, acc[q]);
-                        t = (double)xv.y - (double)hv.y;
-                        acc[q] = fma(t, t, acc[q]);
-                        t = (double)xv.z - (double)hv.z;
-                        acc[q] = fma(t, t, acc[q]);
-                        t = (double)xv.w - (double)hv.w;
+                        t = x1 - hv.y;
                         acc[q] = fma(t, t, acc[q]);
                     }
                 }
@@ -157,7 +157,7 @@ __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, 
 #pragma unroll
                 for (int q = 0; q < QC; ++q) {
                     if (q0 + q < k) {
-                        const double t = xc - (double)__ldg(hi + (int64_t)jj[q0 + q] * d + c);
+                        const double t = xc - __ldg(hi64 + (int64_t)jj[q0 + q] * d + c);
                         acc[q] = fma(t, t, acc[q]);
                     }
                 }
@@ -592,52 +592,23 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         // far from the landmarks: f64 squared distances as double-float pairs (precise_sqd)
         float qe[KP];
         if (prec) {
-            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi, jj, k, qe);
+            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, jj, k, qe);
         } else {
 #pragma unroll
             for (int q = 0; q < KP; ++q) qe[q] = sq[q];
         }
         float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
-        int pj[KP], prb[KP];
-        float pqe[KP], psc[KP], plx[KP], ply[KP];
+        // all pairs u < v, fully unrolled (static register indices, no ring rotation).
+        // Slot KP-1 never pairs: its score is exactly 0 (the reference's tail
+        // s_{k-1} = 0 when k == KP, the uniform fallback's trailing 0, or padding).
 #pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            pj[q] = jj[q];
-            prb[q] = rb[q];
-            pqe[q] = qe[q];
-            psc[q] = sc[q];
-            plx[q] = lx[q];
-            ply[q] = ly[q];
-        }
-        // ring schedule (see project_reg_kernel): round r pairs slot u with u + r mod KP
-        #pragma unroll 2  // rotate-by-2 per trip: half the ring register moves (C2: 0.287 -> 0.257 ms; slower in reg3)
-        for (int r = 1; r <= KP / 2; ++r) {
-            {
-                const int j0 = pj[0], b0 = prb[0];
-                const float s0 = pqe[0], c0 = psc[0], x0 = plx[0], y0 = ply[0];
+        for (int u = 0; u < KP - 2; ++u) {
 #pragma unroll
-                for (int q = 0; q < KP - 1; ++q) {
-                    pj[q] = pj[q + 1];
-                    prb[q] = prb[q + 1];
-                    pqe[q] = pqe[q + 1];
-                    psc[q] = psc[q + 1];
-                    plx[q] = plx[q + 1];
-                    ply[q] = ply[q + 1];
-                }
-                pj[KP - 1] = j0;
-                prb[KP - 1] = b0;
-                pqe[KP - 1] = s0;
-                psc[KP - 1] = c0;
-                plx[KP - 1] = x0;
-                ply[KP - 1] = y0;
-            }
-            const bool half = r == KP / 2;
-#pragma unroll
-            for (int u = 0; u < KP; ++u) {
-                const float w = (half && u >= KP / 2) ? 0.0f : sc[u] * psc[u];
-                const int ti = max(jj[u] < pj[u] ? rb[u] + pj[u] : prb[u] + jj[u], 0);
+            for (int v = u + 1; v < KP - 1; ++v) {
+                const float w = sc[u] * sc[v];
+                const int ti = max(jj[u] < jj[v] ? rb[u] + jj[v] : rb[v] + jj[u], 0);
                 const float tv = T[ti];
-                const float ex = __fsub_rn(plx[u], lx[u]), ey = __fsub_rn(ply[u], ly[u]);
+                const float ex = __fsub_rn(lx[v], lx[u]), ey = __fsub_rn(ly[v], ly[u]);
                 const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
                 const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
                 tmax = keep ? fmaxf(tmax, tv) : tmax;
@@ -645,7 +616,7 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
                 const float wr = w * rr;
                 const float g1 = ex * rr, g2 = ey * rr;
                 // dnum/hd2 by the law of cosines + g . (lo_u - o)
-                const float h = fmaf(qe[u] - pqe[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
+                const float h = fmaf(qe[u] - qe[v], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
                 const float wg1 = wr * ex, wg2 = wr * ey;  // w g
                 a11 = fmaf(wg1, g1, a11);
                 a12 = fmaf(wg1, g2, a12);
@@ -784,43 +755,23 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
 
         float qe[KP];
         if (prec) {
-            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi, jj, k, qe);
+            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, jj, k, qe);
         } else {
 #pragma unroll
             for (int q = 0; q < KP; ++q) qe[q] = sq[q];
         }
         float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
-        int pj[KP];
-        float pqe[KP], psc[KP];
+        // all pairs u < v fully unrolled; slot KP-1 has score 0 (see project_reg2_kernel)
 #pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            pj[q] = jj[q];
-            pqe[q] = qe[q];
-            psc[q] = sc[q];
-        }
-                for (int r = 1; r <= KP / 2; ++r) {  // ring schedule: round r pairs slot u with u + r mod KP
-            {
-                const int j0 = pj[0];
-                const float s0 = pqe[0], c0 = psc[0];
+        for (int u = 0; u < KP - 2; ++u) {
 #pragma unroll
-                for (int q = 0; q < KP - 1; ++q) {
-                    pj[q] = pj[q + 1];
-                    pqe[q] = pqe[q + 1];
-                    psc[q] = psc[q + 1];
-                }
-                pj[KP - 1] = j0;
-                pqe[KP - 1] = s0;
-                psc[KP - 1] = c0;
-            }
-            const bool half = r == KP / 2;
-#pragma unroll
-            for (int u = 0; u < KP; ++u) {
-                const float w = (half && u >= KP / 2) ? 0.0f : sc[u] * psc[u];
-                const float4 rc = __ldg(rec + rowb[u] + pj[u]);
+            for (int v = u + 1; v < KP - 1; ++v) {
+                const float w = sc[u] * sc[v];
+                const float4 rc = __ldg(rec + rowb[u] + jj[v]);
                 const bool keep = (w > 0.0f) & (rc.x >= 0.0f);
                 tmax = keep ? fmaxf(tmax, rc.x) : tmax;
                 const float wk = keep ? w : 0.0f;
-                const float h = fmaf(qe[u] - pqe[u], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
+                const float h = fmaf(qe[u] - qe[v], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
                 const float wg1 = wk * rc.y, wg2 = wk * rc.z;
                 a11 = fmaf(wg1, rc.y, a11);
                 a12 = fmaf(wg1, rc.z, a12);

@@ -35,6 +35,7 @@ struct ProjArgs {
     float* xy;               // n×2 out
     const float* X;          // outlier exact path
     const float* hi;
+    const double* hi64;      // hi widened to f64 (model workspace): far-point distances
     int d;
     const int32_t* perm;     // optional visiting order (nullable)
     const float4* rec;       // g x g pair records {T, g1, g2, g.lo_u} (project_reg3_kernel; nullable)

@@ -17,7 +17,7 @@ from bench import make_inputs  # noqa: E402
 
 def main():
     dev = torch.device("cuda", 0)
-    pts, hi, lo, k, _ = make_inputs("c2", 0)
+    pts, hi, lo, k, _, _ = make_inputs("c2", 0, 1)
     host = torch.from_numpy(pts).pin_memory()
     d_buf = torch.empty(host.shape, dtype=torch.float32, device=dev)
     for _ in range(3):

@@ -15,7 +15,7 @@ from bench import make_inputs  # noqa: E402
 
 def main(w):
     import importlib
-    pts, hi, lo, k, _ = make_inputs(w, 0)
+    pts, hi, lo, k, _, _ = make_inputs(w, 0, 1)
     host = torch.from_numpy(pts).pin_memory()
     for chunk, depth in [(1 << 16, 4), (1 << 17, 3), (1 << 18, 3), (1 << 19, 2)]:
         os.environ["ESOM_PIPE_CHUNK"] = str(chunk)

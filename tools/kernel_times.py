@@ -38,7 +38,7 @@ def main(names):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     L = _lib.load()
     for name in names:
-        pts, hi, lo, k, _ = make_inputs(name, 0)
+        pts, hi, lo, k, _, _ = make_inputs(name, 0, 1)
         n, d = pts.shape
         X = torch.from_numpy(pts).to(dev)
         pm = PreparedModel(hi, lo, k, device=dev)

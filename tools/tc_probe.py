@@ -26,7 +26,7 @@ def main(names):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     cnt = torch.zeros(8, dtype=torch.int32, device=dev)
     for name in names:
-        pts, hi, lo, k, _ = make_inputs(name, 0)
+        pts, hi, lo, k, _, _ = make_inputs(name, 0, 1)
         n, d = pts.shape
         X = torch.from_numpy(pts).to(dev)
         H = torch.from_numpy(hi).to(dev)
