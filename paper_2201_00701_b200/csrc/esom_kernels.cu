@@ -835,8 +835,20 @@ __global__ void widen_kernel(const float* __restrict__ src, int64_t n, double* _
         dst[e] = (double)src[e];
 }
 
+// |h_j|^2 in f64 per landmark row (the far-point distances' dot-product form)
+__global__ void row_norm64_kernel(const float* __restrict__ hi, int g, int d, double* __restrict__ hn) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < g; j += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < d; ++c) {
+            const double v = (double)hi[(int64_t)j * d + c];
+            s = fma(v, v, s);
+        }
+        hn[j] = s;
+    }
+}
+
 struct ModelLayout {
-    size_t lt, tri, bhi, blo, ln, lstats, lrow, rec, hi64, total;
+    size_t lt, tri, bhi, blo, ln, lstats, lrow, rec, hi64, hn64, total;
     bool has_rec;  // g x g pair records for project_reg3_kernel (k <= 16, g <= 1024)
     int d16, gpad, ls;
     // tensor-core GEMM screen for d > 32 (esom_tc3.cuh): per-model operands + per-chunk scratch
@@ -880,6 +892,8 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
     }
     m.hi64 = o;  // f64 copy of hi: the far-point distances of the projection (precise_sqd)
     if (with_pairs) o += a256((size_t)g * d * 8);
+    m.hn64 = o;  // |h_j|^2 in f64 (same use)
+    if (with_pairs) o += a256((size_t)g * 8);
     m.t2chunk = 0;
     if (d <= 32 && m.gpad <= 1024) {
         m.t2chunk = 1 << 20;
@@ -1342,6 +1356,8 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     widen_kernel<<<grid_for((int64_t)g * d, 256), 256, 0, stream>>>(hi, (int64_t)g * d,
                                                                     reinterpret_cast<double*>(ws + m.hi64));
     if (int e = cuda_check("widen_hi")) return e;
+    row_norm64_kernel<<<grid_for(g, 128), 128, 0, stream>>>(hi, g, d, reinterpret_cast<double*>(ws + m.hn64));
+    if (int e = cuda_check("row_norm64")) return e;
     if (tc_eligible(1 << 20, d, g, k))
         if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
     if (m.t3 && t3_enabled())
@@ -1380,7 +1396,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
     const int64_t chunk = n < embed_chunk(d, k) ? n : embed_chunk(d, k);
     // pair records {T, g, g.lo_u} for this call's layout (project_reg3_kernel)
     // (g <= 256: the triangle table sits in shared memory and v2 is as fast without the record build)
-    const bool use_rec = ml.has_rec && g > 256 && !getenv("ESOM_PROJ_V2") && !getenv("ESOM_PROJ_V1");
+    const bool use_rec = ml.has_rec && g > 256;
     float4* rec = reinterpret_cast<float4*>(const_cast<char*>(mws) + ml.rec);
     if (use_rec)
         if (int e = launch_pair_records(T, lo, g, rec, stream)) return e;
@@ -1431,10 +1447,13 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         q.T = T;
         q.tmax = reinterpret_cast<const float*>(mws + ml.lstats) + 2;
         q.prec_count = far_count;
+        q.far_heavy = bmu_order ? 1 : 0;
         q.xy = xy + 2 * s;
         q.X = X + s * d;
         q.hi = hi;
         q.hi64 = reinterpret_cast<const double*>(mws + ml.hi64);
+
+        q.hn64 = reinterpret_cast<const double*>(mws + ml.hn64);
         q.d = d;
         q.rec = use_rec ? rec : nullptr;
         {

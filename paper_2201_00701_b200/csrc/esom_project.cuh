@@ -123,9 +123,18 @@ __device__ __forceinline__ void count_prec(int32_t* cnt, bool prec) {
 
 
 
-template <int KP>
+template <int KP, bool SMEM = false>
 __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, const double* __restrict__ hi64,
-                                            const int (&jj)[KP], int k, float (&qe)[KP]) {
+                                            int hs, const int (&jj)[KP], int k, float (&qe)[KP]) {
+    // rows (stride hs doubles) in shared memory (plain loads) or the model workspace (read-only path)
+    auto row2 = [&](int j, int c) {
+        const double2* p = reinterpret_cast<const double2*>(hi64 + (int64_t)j * hs + c);
+        return SMEM ? *p : __ldg(p);
+    };
+    auto row1 = [&](int j, int c) {
+        const double* p = hi64 + (int64_t)j * hs + c;
+        return SMEM ? *p : __ldg(p);
+    };
     // landmark rows come pre-widened (model workspace), so the only f32 -> f64
     // conversions are x's: 2 per dimension pair per chunk of neighbours (the
     // per-element F2F of both operands used to dominate trained-model frames)
@@ -143,7 +152,7 @@ __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, 
 #pragma unroll
                 for (int q = 0; q < QC; ++q) {
                     if (q0 + q < k) {
-                        const double2 hv = __ldg(reinterpret_cast<const double2*>(hi64 + (int64_t)jj[q0 + q] * d + c));
+                        const double2 hv = row2(jj[q0 + q], c);
                         double t = x0 - hv.x;
                         acc[q] = fma(t, t, acc[q]);
                         t = x1 - hv.y;
@@ -157,11 +166,75 @@ __device__ __forceinline__ void precise_sqd(const float* __restrict__ x, int d, 
 #pragma unroll
                 for (int q = 0; q < QC; ++q) {
                     if (q0 + q < k) {
-                        const double t = xc - __ldg(hi64 + (int64_t)jj[q0 + q] * d + c);
+                        const double t = xc - row1(jj[q0 + q], c);
                         acc[q] = fma(t, t, acc[q]);
                     }
                 }
             }
+        }
+        if (q0 == 0) s0 = acc[0];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) qe[q0 + q] = q0 + q < k ? (float)(acc[q] - s0) : 0.0f;
+    }
+}
+
+// precise_sqd for a compile-time d (d = 32: C2-C4), in the dot-product form
+//   s_j - s_0 = (|h_j|^2 - |h_0|^2) - 2 x.(h_j - h_0),  x.h_j = sum_c x_c h_jc
+// (one f64 FMA per element, |h_j|^2 precomputed per model; f64 keeps the
+// cancellation harmless: ~1e-13 absolute at these magnitudes), with x held in
+// registers (its loads all in flight at once) and the dimension loop unrolled
+// so the row loads of the next step issue early.
+// FULL (frames where most points are far, i.e. trained models): x held in
+// registers and every step unrolled -- the most loads in flight, at the price of
+// registers the common case needs elsewhere; otherwise x streams one step ahead.
+template <int KP, int D, bool SMEM, bool FULL>
+__device__ __forceinline__ void precise_sqd_fixed(const float* __restrict__ xg, const double* __restrict__ hi64,
+                                                  int hs, const double* __restrict__ hn, const int (&jj)[KP], int k,
+                                                  float (&qe)[KP]) {
+    constexpr int QC = KP < 4 ? KP : 4;
+    float xr[FULL ? D : 4];
+    if (FULL) {
+#pragma unroll
+        for (int c = 0; c < D; c += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(xg + c));
+            xr[c] = v.x; xr[c + 1] = v.y; xr[c + 2] = v.z; xr[c + 3] = v.w;
+        }
+    }
+    double s0 = 0.0;
+#pragma unroll
+    for (int q0 = 0; q0 < KP; q0 += QC) {
+        double acc[QC];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) acc[q] = 0.0;
+        float4 xn = FULL ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(reinterpret_cast<const float4*>(xg));
+#pragma unroll (FULL ? D / 4 : 2)
+        for (int c = 0; c < D; c += 4) {
+            float4 xc;
+            if (FULL) {
+                xc = make_float4(xr[c % (FULL ? D : 4)], xr[(c + 1) % (FULL ? D : 4)], xr[(c + 2) % (FULL ? D : 4)],
+                                 xr[(c + 3) % (FULL ? D : 4)]);
+            } else {
+                xc = xn;
+                if (c + 4 < D) xn = __ldg(reinterpret_cast<const float4*>(xg + c + 4));  // one step ahead
+            }
+            const double x0 = (double)xc.x, x1 = (double)xc.y, x2 = (double)xc.z, x3 = (double)xc.w;
+#pragma unroll
+            for (int q = 0; q < QC; ++q) {
+                if (q0 + q < k) {
+                    const double2* pr = reinterpret_cast<const double2*>(hi64 + (int64_t)jj[q0 + q] * hs + c);
+                    const double2 h01 = SMEM ? pr[0] : __ldg(pr);
+                    const double2 h23 = SMEM ? pr[1] : __ldg(pr + 1);
+                    acc[q] = fma(x0, h01.x, acc[q]);
+                    acc[q] = fma(x1, h01.y, acc[q]);
+                    acc[q] = fma(x2, h23.x, acc[q]);
+                    acc[q] = fma(x3, h23.y, acc[q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+            const double hq = q0 + q < k ? (SMEM ? hn[jj[q0 + q]] : __ldg(hn + jj[q0 + q])) : 0.0;
+            acc[q] = fma(-2.0, acc[q], hq);  // s_j - |x|^2
         }
         if (q0 == 0) s0 = acc[0];
 #pragma unroll
@@ -319,173 +392,12 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
     }
 }
 
-// ---------------------------------------------------------------------------
-// k <= 16: the whole per-point state lives in registers and the k(k-1)/2 pair
-// loop is fully unrolled (static register indexing; no per-pair shared
-// loads except the pair-table entry).  Same arithmetic as above.
-// ---------------------------------------------------------------------------
-constexpr int kRegThreads = 256;
-
-template <int KP, bool TSMEM>
-__global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
-    constexpr int PT = kRegThreads;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int tid = threadIdx.x;
-    const int g = a.g, k = a.k;
-    float2* LO = reinterpret_cast<float2*>(smem_raw);
-    int* RB = reinterpret_cast<int*>(LO + g);
-    float* tsm = reinterpret_cast<float*>(RB + g + ((g & 1) ? 1 : 0));
-    if (TSMEM) {
-        const int ntri = g * (g - 1) / 2;
-        for (int e = tid; e < ntri; e += PT) tsm[e] = __ldg(a.T + e);
-    }
-    for (int j = tid; j < g; j += PT) {
-        LO[j] = make_float2(a.lo[2 * j], a.lo[2 * j + 1]);
-        RB[j] = j * (2 * g - j - 1) / 2 - j - 1;
-    }
-    __syncthreads();
-    const float* T = TSMEM ? tsm : a.T;
-
-    for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
-        // optional BMU-sorted visiting order: lanes of a warp then share
-        // neighbour sets, so their pair-table reads hit the same L1 lines
-        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
-        int jj[KP];
-        float sq[KP], sc[KP], lx[KP], ly[KP];
-        const int32_t* irow = a.idx + i * k;
-        const float* drow = a.sqd + i * k;
-        double sigma = 0.0;
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            if (q < k) {
-                jj[q] = __ldg(irow + q);
-                sq[q] = __ldg(drow + q);
-            } else {
-                jj[q] = 0;
-                sq[q] = 0.0f;
-            }
-            const float2 l = LO[jj[q]];
-            lx[q] = l.x;
-            ly[q] = l.y;
-            if (q < k) sigma += (double)__fsqrt_rn(sq[q]);
-        }
-        // scores (f64 like the reference; ref: projection.py:38-59)
-        sigma /= (double)k;
-        bool uniform = sigma < kScoreEps;
-        double dk = 0.0;
-#pragma unroll
-        for (int q = 0; q < KP; ++q)
-            if (q == k - 1) dk = (double)__fsqrt_rn(sq[q]);
-        if (!uniform) {
-            const double inv = -1.0 / (2.0 * sigma * sigma);
-            const double tail = exp(dk * dk * inv);
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                const double dq = (double)__fsqrt_rn(sq[q]);
-                const double v = q < k ? exp(dq * dq * inv) - tail : 0.0;
-                sc[q] = v > 0.0 ? (float)v : 0.0f;
-                if (q == 0) uniform = v < kScoreEps;
-            }
-        }
-        if (uniform) {
-#pragma unroll
-            for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
-        }
-
-        double a11 = 0.0, a12 = 0.0, a22 = 0.0, c1 = 0.0, c2 = 0.0;
-        float tmax = 0.0f;
-        // Ring schedule over the KP slots: round r pairs slot u with slot
-        // (u + r) mod KP, r = 1..KP/2 (the last round only u < KP/2), which
-        // visits every unordered pair exactly once.  The partner arrays are
-        // rotated by one slot per round, so the round body is static code
-        // (KP pair bodies) inside a short dynamic loop: small I-cache
-        // footprint, registers only.  A pair's contribution is symmetric in
-        // (u, v) (g flips sign together with h), so visiting (v, u) is exact
-        // up to rounding.  Slots >= k carry zero weight.
-        int pj[KP];
-        float psq[KP], psc[KP], plx[KP], ply[KP];
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            pj[q] = jj[q];
-            psq[q] = sq[q];
-            psc[q] = sc[q];
-            plx[q] = lx[q];
-            ply[q] = ly[q];
-        }
-        for (int r = 1; r <= KP / 2; ++r) {
-            // rotate partners by one: p[q] <- p[q + 1]
-            {
-                const int j0 = pj[0];
-                const float s0 = psq[0], c0 = psc[0], x0 = plx[0], y0 = ply[0];
-#pragma unroll
-                for (int q = 0; q < KP - 1; ++q) {
-                    pj[q] = pj[q + 1];
-                    psq[q] = psq[q + 1];
-                    psc[q] = psc[q + 1];
-                    plx[q] = plx[q + 1];
-                    ply[q] = ply[q + 1];
-                }
-                pj[KP - 1] = j0;
-                psq[KP - 1] = s0;
-                psc[KP - 1] = c0;
-                plx[KP - 1] = x0;
-                ply[KP - 1] = y0;
-            }
-            const bool half = r == KP / 2;
-#pragma unroll
-            for (int u = 0; u < KP; ++u) {
-                const float w = (half && u >= KP / 2) ? 0.0f : sc[u] * psc[u];
-                const int lo_j = min(jj[u], pj[u]), hi_j = max(jj[u], pj[u]);
-                const int ti = ((lo_j * (2 * g - 1 - lo_j)) >> 1) + hi_j - lo_j - 1;  // packed upper triangle
-                const float tv = w > 0.0f ? T[ti] : -1.0f;
-                const float ex = __fsub_rn(plx[u], lx[u]), ey = __fsub_rn(ply[u], ly[u]);
-                const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-                const bool keep = (tv >= 0.0f) & (ld2 >= kLd2Min);
-                tmax = keep ? fmaxf(tmax, tv) : tmax;
-                const float rr = keep ? rcp_approx(ld2) : 0.0f;  // MUFU.RCP (<= 1 ulp); ld2 >= 1e-12
-                const float g1 = ex * rr, g2 = ey * rr;
-                // dnum/hd2 by the law of cosines + g . lo_u
-                const float h = fmaf(sq[u] - psq[u], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
-                const double W = keep ? (double)w : 0.0;
-                const double G1 = (double)g1, G2 = (double)g2;
-                const double wg1 = W * G1, wg2 = W * G2, wh = W * (double)h;
-                a11 = fma(wg1, G1, a11);
-                a12 = fma(wg1, G2, a12);
-                a22 = fma(wg2, G2, a22);
-                c1 = fma(wh, G1, c1);
-                c2 = fma(wh, G2, c2);
-            }
-        }
-        // kappa <= 2 max(sqd) max(T): exact pair-wise check only when that bound trips
-        float sqmax = 0.0f;
-#pragma unroll
-        for (int q = 0; q < KP; ++q) sqmax = fmaxf(sqmax, sq[q]);
-        float kappa = 2.0f * sqmax * tmax;
-        float2 out;
-        if (kappa > (float)kKappaMax) {
-            // far outlier: exact x-based f64 pair loop (rare; rows spilled to local memory)
-            double o5[5];
-            pairs_exact_f64(a.X + i * a.d, a.d, a.hi, a.lo, k, jj, sc, 1, o5);
-            a11 = o5[0];
-            a12 = o5[1];
-            a22 = o5[2];
-            c1 = o5[3];
-            c2 = o5[4];
-        }
-        const double det = a11 * a22 - a12 * a12;
-        const double tr = a11 + a22;
-        if (det < kDetRel * tr * tr + kDetAbs) {
-            out = make_float2(lx[0], ly[0]);
-        } else {
-            out.x = (float)((c1 * a22 - c2 * a12) / det);
-            out.y = (float)((a11 * c2 - a12 * c1) / det);
-        }
-        reinterpret_cast<float2*>(a.xy)[i] = out;
-    }
-}
+constexpr int kRegThreads = 256;  // project_reg3_kernel (255 registers: one CTA per SM)
 
 // ---------------------------------------------------------------------------
-// v2 (default for k <= 16): same law-of-cosines projection, cheaper per pair.
+// k <= 16 (default; the pair triangle in shared memory up to g ~ 330): the
+// law-of-cosines projection with the whole per-point state in registers and
+// the pair loop fully unrolled (static register indices).
 //  * scores in f32 (MUFU sqrt/ex2; ~1e-7 relative, far inside the embedding
 //    tolerance), normal equations accumulated in f32 about the nearest
 //    landmark's layout position o = lo[idx0] (small magnitudes), solved in f64;
@@ -494,18 +406,41 @@ __global__ void __launch_bounds__(kRegThreads) project_reg_kernel(ProjArgs a) {
 //  * pair-table index from per-slot row bases (no triangle arithmetic per pair),
 //    unconditional table reads, vector loads of the neighbour rows.
 // ---------------------------------------------------------------------------
-template <int KP, bool TSMEM>
-__global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
-    constexpr int PT = kRegThreads;
+constexpr int kReg2Threads = 512;  // 16 warps/SM at <= 128 registers (one CTA: the pair table fills smem)
+
+// shared-memory bytes of project_reg2_kernel: LO, RB | pair triangle | f64 rows
+__host__ __device__ inline size_t reg2_tri_offset(int g) { return ((size_t)g * 12 + 4 + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t reg2_hi64_offset(int g) {
+    return (reg2_tri_offset(g) + (size_t)g * (g - 1) / 2 * 4 + 15) & ~(size_t)15;
+}
+// row stride (doubles) of the f64 rows in shared memory: an odd number of 16-byte
+// units, so the rows of different neighbours start in different bank groups
+// (a 256-byte stride put every lane's 128-bit load on the same banks)
+__host__ __device__ inline int reg2_hi64_stride(int d) {
+    const int u = (d + 1) / 2;  // 16-byte units
+    return 2 * (u | 1);
+}
+
+template <int KP, bool TSMEM, bool HSMEM, bool FARHEAVY>
+__global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs a) {
+    constexpr int PT = kReg2Threads;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
     float2* LO = reinterpret_cast<float2*>(smem_raw);
     int* RB = reinterpret_cast<int*>(LO + g);
-    float* tsm = reinterpret_cast<float*>(RB + g + ((g & 1) ? 1 : 0));
+    float* tsm = reinterpret_cast<float*>(smem_raw + reg2_tri_offset(g));
+    double* h64 = reinterpret_cast<double*>(smem_raw + reg2_hi64_offset(g));
+    double* hn_s = h64 + (size_t)g * reg2_hi64_stride(a.d);  // g row norms after the rows
     if (TSMEM) {
         const int ntri = g * (g - 1) / 2;
         for (int e = tid; e < ntri; e += PT) tsm[e] = __ldg(a.T + e);
+    }
+    const int hs = reg2_hi64_stride(a.d);
+    if (HSMEM) {  // f64 landmark rows for the far-point distances (precise_sqd)
+        const int nh = g * a.d;
+        for (int e = tid; e < nh; e += PT) h64[(e / a.d) * hs + e % a.d] = __ldg(a.hi64 + e);
+        for (int j = tid; j < g; j += PT) hn_s[j] = __ldg(a.hn64 + j);
     }
     for (int j = tid; j < g; j += PT) {
         LO[j] = make_float2(a.lo[2 * j], a.lo[2 * j + 1]);
@@ -537,8 +472,26 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
                 sq[q] = q < k ? __ldg(drow + q) : 0.0f;
             }
         }
+        float sqmax = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) sqmax = fmaxf(sqmax, sq[q]);
+        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
+        count_prec(a.prec_count, prec);
+        // far from the landmarks: the k squared distances again in f64, kept as f32
+        // offsets from the nearest (precise_sqd); first, while little else is live
+        float qe[KP];
+        if (prec) {
+            if (a.d == 32)
+                precise_sqd_fixed<KP, 32, HSMEM, FARHEAVY>(a.X + i * 32, HSMEM ? h64 : a.hi64, HSMEM ? hs : 32,
+                                                 HSMEM ? hn_s : a.hn64, jj, k, qe);
+            else
+                precise_sqd<KP, HSMEM>(a.X + i * a.d, a.d, HSMEM ? h64 : a.hi64, HSMEM ? hs : a.d, jj, k, qe);
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) qe[q] = sq[q];
+        }
         const float2 o = LO[jj[0]];
-        float sig = 0.0f, sqk = 0.0f, sqmax = 0.0f;
+        float sig = 0.0f, sqk = 0.0f;
 #pragma unroll
         for (int q = 0; q < KP; ++q) {
             const float2 l = LO[jj[q]];
@@ -548,7 +501,6 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
             const float dq = q < k ? sqrt_approx(sq[q]) : 0.0f;
             sig += dq;
             if (q == k - 1) sqk = sq[q];
-            sqmax = fmaxf(sqmax, sq[q]);
         }
         // scores (ref: projection.py:38-59) in f32, as the scale-free weights
         // s_q / tail = expm1((d_k^2 - d_q^2) / 2 sigma^2): the normal equations
@@ -556,8 +508,6 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
         // precision where the reference's e_q - tail cancels (far outliers).
         sig = sig / (float)k;
         bool uniform = sig < (float)kScoreEps;
-        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
-        count_prec(a.prec_count, prec);
         if (!uniform) {
             const float inv = 1.0f / (2.0f * sig * sig);
             const float tail = ex2_approx(-1.44269504f * sqk * inv);
@@ -589,14 +539,6 @@ __global__ void __launch_bounds__(kRegThreads) project_reg2_kernel(ProjArgs a) {
             for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
         }
 
-        // far from the landmarks: f64 squared distances as double-float pairs (precise_sqd)
-        float qe[KP];
-        if (prec) {
-            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, jj, k, qe);
-        } else {
-#pragma unroll
-            for (int q = 0; q < KP; ++q) qe[q] = sq[q];
-        }
         float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
         // all pairs u < v, fully unrolled (static register indices, no ring rotation).
         // Slot KP-1 never pairs: its score is exactly 0 (the reference's tail
@@ -755,7 +697,7 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
 
         float qe[KP];
         if (prec) {
-            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, jj, k, qe);
+            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, a.d, jj, k, qe);
         } else {
 #pragma unroll
             for (int q = 0; q < KP; ++q) qe[q] = sq[q];
@@ -807,19 +749,18 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
     }
 }
 
-template <int KP, bool TSMEM>
+template <int KP, bool TSMEM, bool HSMEM>
 int launch_project_reg(ProjArgs a, size_t smem, cudaStream_t st) {
-    static const bool v1 = getenv("ESOM_PROJ_V1") != nullptr;  // A/B switch (measurement only)
-    auto kern = v1 ? project_reg_kernel<KP, TSMEM> : project_reg2_kernel<KP, TSMEM>;
+    auto kern = a.far_heavy ? project_reg2_kernel<KP, TSMEM, HSMEM, true> : project_reg2_kernel<KP, TSMEM, HSMEM, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRegThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kReg2Threads, smem);
     if (per_sm < 1) per_sm = 1;
-    const int64_t nblk = (a.n + kRegThreads - 1) / kRegThreads;
+    const int64_t nblk = (a.n + kReg2Threads - 1) / kReg2Threads;
     int64_t grid = (int64_t)esom_host::num_sms() * per_sm;
     if (grid > nblk) grid = nblk;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kRegThreads, smem, st>>>(a);
+    kern<<<(unsigned)grid, kReg2Threads, smem, st>>>(a);
     return esom_host::cuda_check("project_reg_kernel");
 }
 
@@ -838,11 +779,12 @@ int launch_project_t(ProjArgs a, cudaStream_t st) {
             kern<<<(unsigned)grid, kRegThreads, 0, st>>>(a);
             return esom_host::cuda_check("project_reg3_kernel");
         }
-        const size_t base = (size_t)a.g * 12 + 256;
-        const size_t tbytes = (size_t)a.g * (a.g - 1) / 2 * 4;
         const size_t cap = (size_t)esom_host::max_smem_optin() - 1024;
-        if (base + tbytes <= cap) return launch_project_reg<KP, true>(a, base + tbytes, st);
-        return launch_project_reg<KP, false>(a, base, st);
+        const size_t with_t = reg2_hi64_offset(a.g);
+        const size_t with_h = with_t + (size_t)a.g * (reg2_hi64_stride(a.d) + 1) * 8;
+        if (with_h <= cap) return launch_project_reg<KP, true, true>(a, with_h, st);
+        if (with_t <= cap) return launch_project_reg<KP, true, false>(a, with_t, st);
+        return launch_project_reg<KP, false, false>(a, reg2_tri_offset(a.g), st);
     }
     constexpr int kProjThreads = proj_threads<KP>();
     const size_t base = (size_t)a.g * 12 + (size_t)KP * kProjThreads * 12 + 64;

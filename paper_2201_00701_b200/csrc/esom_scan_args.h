@@ -36,11 +36,13 @@ struct ProjArgs {
     const float* X;          // outlier exact path
     const float* hi;
     const double* hi64;      // hi widened to f64 (model workspace): far-point distances
+    const double* hn64;      // |h_j|^2 in f64 (model workspace)
     int d;
     const int32_t* perm;     // optional visiting order (nullable)
     const float4* rec;       // g x g pair records {T, g1, g2, g.lo_u} (project_reg3_kernel; nullable)
     const float* tmax;       // device scalar: max kept T of the model (f64-distance decision)
     int32_t* prec_count;     // += points that took the f64 far-point path (nullable)
+    int far_heavy;           // the caller expects most points far (nearest-landmark order): far-path codegen
 };
 
 // tensor-core screened k-NN (esom_tc.cuh)
