@@ -96,7 +96,6 @@ struct Tc2Args {
     int32_t* ckey;           // split mode: n x lowest candidate (locality sort key)
     const int32_t* perm;     // split mode, exact kernel: visiting order (nullable)
     int key_by_count;        // experiment: sort the exact phase by candidate count instead of locality
-    int exact_v1;            // A/B: exact kernel without the d16 == 32 row prefetch (ESOM_EXACT_V1)
 };
 
 // tensor-core GEMM screen for d > 32 (esom_tc3.cuh)

@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
     mbar_wait(&bar_load, 0);
     const f2 nz2 = f2_pack(-0.0f, -0.0f);
     const int d4 = (d16 + 3) >> 2;
-    const bool full = d4 == 8 && !a.exact_v1;  // A/B switch (ESOM_EXACT_V1)
+    const bool full = d4 == 8;
     double qe_local = 0.0;
     int slow_local = 0;
     for (int64_t pos = blockIdx.x * (int64_t)kExactBitsThreads + tid; pos < a.n;
@@ -865,8 +865,6 @@ int launch_exact_bits_t(Tc2Args a, cudaStream_t st) {
     if (smem > (size_t)esom_host::max_smem_optin())
         return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact rows exceed shared memory%s", "");
     auto kern = knn_exact_bits_kernel<KP>;
-    static const int v1 = getenv("ESOM_EXACT_V1") ? 1 : 0;
-    a.exact_v1 = v1;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t grid = (a.n + kExactBitsThreads - 1) / kExactBitsThreads;
     if (grid > esom_host::num_sms()) grid = esom_host::num_sms();

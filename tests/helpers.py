@@ -28,12 +28,6 @@ def c2_inputs():
     return pts, hi, lo
 
 
-def c4_inputs_head():
-    # full 10M generation is needed to reproduce the stream; tests use the
-    # fixture's stored 1024-row head + model instead (make_golden.py)
-    raise NotImplementedError
-
-
 def small_inputs(golden):
     return golden["small_points"], golden["small_hi0"], golden["small_lo"]
 
