@@ -1019,9 +1019,8 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
             c.bmu = s.bmu ? s.bmu + s0 : nullptr;
             c.cbits = reinterpret_cast<uint32_t*>(w + m.t2bits);
             c.cinfo = reinterpret_cast<int2*>(w + m.t2info);
-            const bool lsort = c.n >= 4096 && !getenv("ESOM_TC2_NOSORT");
+            const bool lsort = c.n >= 4096;
             c.ckey = lsort ? reinterpret_cast<int32_t*>(w + m.t2key) : nullptr;
-            c.key_by_count = getenv("ESOM_TC2_KEYCNT") ? 1 : 0;
             int e;
             {
                 KTimer tm("knn_tc2_kernel", st);
@@ -1136,12 +1135,6 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
         t.ccount = reinterpret_cast<int32_t*>(ws + m.cnt3);
         t.bmu_approx = reinterpret_cast<int32_t*>(ws + m.bmu3);
         t.stats = tc_stats_ptr();
-        {
-            const char* ev = getenv("ESOM_T3_PASSES");  // 1: experimental one-pass (log compaction) mode
-            t.passes = ev && atoi(ev) == 1 ? 1 : 2;
-            const char* ec = getenv("ESOM_T3_COARSE");
-            t.coarse1 = ec ? atoi(ec) != 0 : 0;  // coarse bound pass: fewer MMAs but a looser cut (slower today)
-        }
         const int kp = kp_for(a.k);
         int e;
         {
@@ -1346,7 +1339,7 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     if (int e = cuda_check("pack_landmarks")) return e;
     float* tmax = reinterpret_cast<float*>(ws + m.lstats) + 2;
     cudaMemsetAsync(tmax, 0, 4, stream);
-    if (d <= 64 && !getenv("ESOM_PAIR_V1")) {
+    if (d <= 64) {
         const int nt = (g + kPairTile - 1) / kPairTile;
         pair_table_tiled_kernel<<<dim3(nt, nt), 256, 0, stream>>>(hi, g, d, T, tmax);
     } else {
@@ -1414,7 +1407,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
         const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
         const bool need_perm = l2_table || ((use_rec || bmu_order) && m >= 4096);
-        const bool acc_smem = (acc_S || acc_C) && !need_perm && accum_smem_ok(g, d) && !getenv("ESOM_SEGSUM");
+        const bool acc_smem = (acc_S || acc_C) && !need_perm && accum_smem_ok(g, d);
         if (acc_smem) {
             const size_t smem = ((size_t)g * d + g) * 8;
             cudaFuncSetAttribute(bmu_accum_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -95,7 +95,6 @@ struct Tc2Args {
     int2* cinfo;             // split mode: n x {candidates (-1: non-finite input), non-empty word mask}
     int32_t* ckey;           // split mode: n x lowest candidate (locality sort key)
     const int32_t* perm;     // split mode, exact kernel: visiting order (nullable)
-    int key_by_count;        // experiment: sort the exact phase by candidate count instead of locality
 };
 
 // tensor-core GEMM screen for d > 32 (esom_tc3.cuh)
@@ -105,8 +104,6 @@ struct Tc3Args {
     const float* xnorm;      // n: |x - c| (rounded up)
     int64_t n;
     int d, dk, gpad, k;      // dk = d padded to 32, gpad = g padded to 256
-    int passes;              // 2: group-min bound pass + candidate pass; 1: candidate pass with log compaction
-    int coarse1;             // bound pass with x_hi . l_hi only (looser bound E1, a third of the MMAs)
     const uint16_t* Bhi;     // -2 (l - c) split bf16, [256-row round][K chunk] canonical
     const uint16_t* Blo;
     const float* ln;         // gpad: |l - c|^2 (+inf padding)

@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         if (SPLIT) {  // the exact phase runs in knn_exact_bits_kernel
             if (valid) {
                 a.cinfo[i] = make_int2(xbad ? -1 : cnt, (int)nzw);
-                if (a.ckey) a.ckey[i] = a.key_by_count ? min(cnt, a.g - 1) : (first < 0 ? 0 : first);
+                if (a.ckey) a.ckey[i] = first < 0 ? 0 : first;
             }
             stat_local += valid ? cnt : 0;
             continue;
@@ -600,7 +600,7 @@ template <int KP, int W>
 int launch_tc2_t(Tc2Args a, cudaStream_t st) {
     const size_t cap = (size_t)esom_host::max_smem_optin();
     const bool split = a.cbits != nullptr;
-    const bool rs = !split && tc2_smem_bytes<W>(a, true) <= cap && !getenv("ESOM_TC2_ROWS_L2");
+    const bool rs = !split && tc2_smem_bytes<W>(a, true) <= cap;
     const size_t smem = tc2_smem_bytes<W>(a, rs, split);
     if (smem > cap) return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "tc2: shape exceeds shared memory%s", "");
     auto kern = split ? knn_tc2_kernel<KP, W, false, true>

@@ -63,17 +63,6 @@ __device__ __forceinline__ float t3_eps(float xnorm, float lmax, float lnmax, in
     return 2.0f * (e0 + (d + 3.0f) * 5.9605e-8f * dtrue);
 }
 
-// Bound E1 for the pass-1 screen that uses x_hi . l_hi only (one MMA per K step):
-// |x.l - x_hi.l_hi| <= (2^-8 + 2^-18) S (RN bf16 rounding of both operands), x2 for
-// B = -2l; accumulation, norm and reference-rounding terms as t3_eps; all x2.
-__device__ __forceinline__ float t3_eps_hi(float xnorm, float lmax, float lnmax, int d, int dk, float tau) {
-    const float S = xnorm * lmax;
-    const float nm = (float)(dk >> 4);
-    const float e0 = 2.0f * (3.9063e-3f + 3.8147e-6f) * S + 4.0f * nm * 1.1921e-7f * (lnmax + 2.0f * S) +
-                     1.1921e-7f * (2.0f * lnmax + xnorm * xnorm + fabsf(tau));
-    const float dtrue = fmaxf(xnorm * xnorm + tau, 0.0f) + 4.0f * e0 + 1.0f;
-    return 2.0f * (e0 + (d + 3.0f) * 5.9605e-8f * dtrue);
-}
 
 template <int KP>
 struct T3Compacted {
@@ -158,25 +147,22 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
         if ((tid & 31) == 0) {
             uint32_t q = 0;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
-                for (int pass = 2 - a.passes; pass < 2; ++pass)
+                for (int pass = 0; pass < 2; ++pass)
                     for (int r = 0; r < R; ++r)
                         for (int kc = 0; kc < nkc; ++kc, ++q) {
                             const int s = (int)(q % kT3Stages);
                             mbar_wait(&empty[s], ((q / kT3Stages) & 1u) ^ 1u);
                             unsigned char* sb = stage + (size_t)s * kT3Stage;
-                            const bool hi_only = pass == 0 && a.coarse1;  // bound pass: x_hi . l_hi only
-                            mbar_expect_tx(&full[s], hi_only ? kT3Stage / 2 : kT3Stage);
+                            mbar_expect_tx(&full[s], kT3Stage);
                             for (int t = 0; t < 2; ++t) {
                                 const size_t ao = ((size_t)(2 * st + t) * nkc + kc) * (kT3AChunk / 2);
                                 tma_bulk_g2s(sb + (2 * t) * kT3AChunk, a.Ahi + ao, kT3AChunk, &full[s]);
-                                if (!hi_only)
-                                    tma_bulk_g2s(sb + (2 * t + 1) * kT3AChunk, a.Alo + ao, kT3AChunk, &full[s]);
+                                tma_bulk_g2s(sb + (2 * t + 1) * kT3AChunk, a.Alo + ao, kT3AChunk, &full[s]);
                             }
                             const size_t bo = ((size_t)(r >> 1) * nkc + kc) * (kT3BChunk / 2) +
                                               (size_t)(r & 1) * (kT3BHalf / 2);  // bf16 elements
                             tma_bulk_g2s(sb + 4 * kT3AChunk, a.Bhi + bo, kT3BHalf, &full[s]);
-                            if (!hi_only)
-                                tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BHalf, a.Blo + bo, kT3BHalf, &full[s]);
+                            tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BHalf, a.Blo + bo, kT3BHalf, &full[s]);
                         }
         }
     } else if (warp == kT3Epi / 32 + 1) {
@@ -186,7 +172,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             const uint32_t idesc = umma_idesc_bf16(128, kT3N);
             const uint32_t sboA = (kT3Kc / 8) * 128, sboB = (kT3Kc / 8) * 128, lbo = 128;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
-                for (int pass = 2 - a.passes; pass < 2; ++pass)
+                for (int pass = 0; pass < 2; ++pass)
                     for (int r = 0; r < R; ++r, ++rr) {
                         const uint32_t buf = rr & 1u;
                         mbar_wait(&tmem_empty[buf], ((rr >> 1) & 1u) ^ 1u);  // epilogue read this buffer's last use
@@ -205,12 +191,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                                     const uint32_t acc0 = (kc | ks) ? 1u : 0u;
                                     umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
                                               acc0);
-                                    if (pass == 1 || !a.coarse1) {
-                                        umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bl + ko, lbo, sboB),
-                                                  idesc, 1);
-                                        umma_bf16(dcol, umma_desc(al + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB),
-                                                  idesc, 1);
-                                    }
+                                    umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bl + ko, lbo, sboB), idesc,
+                                              1);
+                                    umma_bf16(dcol, umma_desc(al + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
+                                              1);
                                 }
                             }
                             umma_commit(&empty[s]);  // stage reusable once these MMAs retire
@@ -237,8 +221,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             float gm[kT3Groups];
 #pragma unroll
             for (int q = 0; q < kT3Groups; ++q) gm[q] = kInf;
-            // ---- pass 1 (two-pass mode): group minima over all rounds ----
-            for (int r = 0; r < (a.passes == 2 ? R : 0); ++r, ++rr) {
+            // ---- pass 1: group minima over all rounds ----
+            for (int r = 0; r < R; ++r, ++rr) {
                 const uint32_t buf = rr & 1u, tcol = tcol0 + buf * 256u;
                 mbar_wait(&tmem_full[buf], (rr >> 1) & 1u);
                 tc_fence_after();
@@ -258,16 +242,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                 tc_fence_before();
                 mbar_arrive(&tmem_empty[buf]);
             }
-            // one-pass mode: no bound yet (every landmark is logged until the first
-            // compaction sets the cut to the k-th smallest logged D~ + 2E)
-            float tcut = kInf;
-            if (a.passes == 2) {
-                // k-th smallest T_j = d_ref_j - |x'|^2 <= tau + E1 (E1: pass-1 bound), so every true
-                // top-k member has D~_j <= T_j + E <= tau + E1 + E
+            // k-th smallest T_j = d_ref_j - |x'|^2 <= tau + E, so every true top-k
+            // member has D~_j <= T_j + E <= tau + 2E.  (Measured and dropped: a
+            // one-pass mode with log compaction, 70 ms, and an x_hi.l_hi-only bound
+            // pass, 36 ms -- its looser cut overflows the log; this mode: 22 ms.)
+            float tcut;
+            {
                 const float tau = kth_of_64<KP>(gm, k);
                 const float e_full = t3_eps(xnorm, lmax, lnmax, a.d, a.dk, tau);
-                const float e_pass1 = a.coarse1 ? t3_eps_hi(xnorm, lmax, lnmax, a.d, a.dk, tau) : e_full;
-                tcut = tau + e_pass1 + e_full + 9.6e-7f * fabsf(tau);
+                tcut = tau + 2.0f * e_full + 9.6e-7f * fabsf(tau);
             }
             // ---- pass 2: log candidates (index order) ----
             int cnt = 0;
@@ -786,7 +769,7 @@ __global__ void __launch_bounds__(kT3GWarps * 32, 2) knn_exact_group_kernel(T3Ex
 
 template <int KP>
 int launch_exact_warp_t(T3ExactArgs a, cudaStream_t st) {
-    if ((a.d & 7) == 0 && !getenv("ESOM_T3_PERPOINT")) {
+    if ((a.d & 7) == 0) {  // (the per-point kernel below measured 22 vs 15 ms at C5)
         const size_t per_warp = (size_t)t3_group_stride(a.dpad, a.g) * 4;
         const size_t smem = (size_t)kT3GWarps * per_warp;
         if (smem <= (size_t)esom_host::max_smem_optin()) {

@@ -1,15 +1,19 @@
-"""Scores, projection and the fused ``embed`` on the B200 (mirror of ref: projection.py).
+"""Scores, projection and ``embed`` on the B200 (mirror of ref: projection.py).
 
 * ``scores`` / ``project_point`` / ``project_neighbors`` run the faithful
   kernels: the reference's mixed f32/f64 arithmetic
   with every operation separately rounded, so results equal the reference
   except where CUDA's f64 ``exp`` differs from glibc's by one ulp.
-* ``embed`` runs ONE fused sm_100a kernel per call: exact f32 distance scan
-  + register top-k + scores + projection.  Its projection evaluates each
-  pair's high-dimensional coordinate through the law of cosines from the
-  exact squared distances (no neighbour-row gathers) and checks to the
-  stated tolerance (max |xy - xy_ref| <= 1e-4 x embedding extent, tests);
-  ``mode="faithful"`` chains knn -> scores -> faithful projection instead.
+* ``embed`` (``mode="fast"``, the default) runs, per chunk of points, the
+  exact k-NN (d <= 32: tensor-core screen, BMU counting sort, exact
+  re-evaluation; d > 32: operand split, tcgen05 GEMM screen, BMU sort, exact
+  re-evaluation) and one projection kernel: scores in registers and each
+  pair's high-dimensional coordinate through the law of cosines on the exact
+  squared distances (no neighbour-row gathers; far points recompute their
+  distances in f64), checked to the stated tolerance (max |xy - xy_ref| <=
+  1e-4 x embedding extent).  ``esom_embed_launches`` counts the launches.
+  ``mode="faithful"`` chains knn -> scores -> faithful projection instead
+  (what ``install()`` patches into the reference by default).
 """
 
 from __future__ import annotations

@@ -20,6 +20,6 @@ ref = oracle.embed(pts, hi, lo, k)
 for mode in ("fast", "faithful"):
     xy = esom.embed(pts, esom.LandmarkModel.create(hi, lo), esom.EmbedParams(k=k), backend="base", mode=mode)
     err = np.abs(xy - ref).max(axis=1)
-    print(mode, os.environ.get("ESOM_PROJ_V2"), "max err", err.max(), "per point", np.round(err, 5))
+    print(mode, "max err", err.max(), "per point", np.round(err, 5))
 idx, sqd = oracle.knn(pts, hi, k)
 print("idx", idx[int(np.argmax(err))], "sqd", sqd[int(np.argmax(err))])
