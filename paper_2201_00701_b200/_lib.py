@@ -98,7 +98,14 @@ def check(code: int) -> None:
         raise ParameterError(msg)
     if code == ESOM_ERR_INPUT:
         raise InputError(msg)
+    if code == ESOM_ERR_UNSUPPORTED:
+        raise UnsupportedShape(msg)
     raise RuntimeError(f"libesom error {code}: {msg}")
+
+
+class UnsupportedShape(RuntimeError):
+    """A kernel's shared-memory / register plan does not cover this shape
+    (ESOM_ERR_UNSUPPORTED); callers with a general fallback catch it."""
 
 
 def call(name: str, *args) -> None:

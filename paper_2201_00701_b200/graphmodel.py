@@ -160,6 +160,11 @@ def _edge_device(edges, g: int, dev):
     if hit is not None and hit[0] is edges.pairs and hit[1] is edges.rest:
         return hit[2]
     pairs = np.ascontiguousarray(edges.pairs, dtype=np.int32).reshape(-1, 2)
+    if pairs.size and (int(pairs.min()) < 0 or int(pairs.max()) >= g):
+        # the reference's np.add.at raises here (ref: graphmodel.py:160-163); the
+        # kernel would read out of bounds
+        bad = int(pairs.max()) if int(pairs.max()) >= g else int(pairs.min())
+        raise IndexError(f"index {bad} is out of bounds for axis 0 with size {g}")
     ptr, sid = _edge_csr(pairs, g)
     out = (torch.from_numpy(pairs.copy()).to(dev),
            torch.from_numpy(np.ascontiguousarray(edges.rest, dtype=np.float32)).to(dev),

@@ -238,10 +238,15 @@ def embed(points, model, params: EmbedParams, backend: str = "bitonic", chunk_si
             return _dev.out_like(xy, want_numpy)
         if mode != "fast":
             raise ParameterError(f"unknown projection mode {mode!r}")
-        pm = PreparedModel(model.hi, model.lo, k, device=dev)
-        flag = _dev.new_flag(dev)
-        for s in range(0, n, step):
-            pm.embed_into(X[s:s + step], xy[s:s + step], flag=flag)
+        try:
+            pm = PreparedModel(model.hi, model.lo, k, device=dev)
+            flag = _dev.new_flag(dev)
+            for s in range(0, n, step):
+                pm.embed_into(X[s:s + step], xy[s:s + step], flag=flag)
+        except _lib.UnsupportedShape:
+            # beyond the fast kernels' shared-memory plans (very large g): the
+            # faithful chain covers any shape, like the reference
+            return embed(X if not want_numpy else points, model, params, backend, chunk_size, mode="faithful")
         _dev.raise_if_nonfinite(flag)
         _dev.raise_if_nonfinite(pm.flag)
         return _dev.out_like(xy, want_numpy)
@@ -281,6 +286,15 @@ def _embed_host_pipelined(host, model, k: int, dev) -> np.ndarray:
     staging chunks (a chunk is rewritten only after its previous H2D ran).
     (A ramp of smaller first stages measured slower: the fixed per-stage
     cost outweighs the shorter pipeline fill.)"""
+    try:
+        return _embed_host_pipeline_run(host, model, k, dev)
+    except _lib.UnsupportedShape:
+        # beyond the fast kernels' shared-memory plans: the faithful chain (any shape)
+        torch.cuda.synchronize(dev)
+        return embed(host if isinstance(host, np.ndarray) else host.numpy(), model, EmbedParams(k=k), mode="faithful")
+
+
+def _embed_host_pipeline_run(host, model, k: int, dev) -> np.ndarray:
     n, d = host.shape
     pm = PreparedModel(model.hi, model.lo, k, device=dev)
     flag = _dev.new_flag(dev)

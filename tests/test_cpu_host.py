@@ -191,3 +191,33 @@ def test_bench_reference_arm_runs_on_cpu():
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_projection_system_equals_reference(golden):
+    """projection_system is host-side f64 introspection (ref: projection.py:151-186,
+    SURVEY §8a P4): identical to the reference's on the same inputs."""
+    import importlib
+
+    src = ROOT / "baseline" / "_ref"
+    if not (src / "embedview").exists():
+        pytest.skip("reference not staged")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, str(src))
+    try:
+        refp = importlib.import_module("embedview.projection")
+        refc = importlib.import_module("embedview.core")
+        from oracle import oracle
+        from paper_2201_00701_b200.projection import projection_system
+
+        pts, hi, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+        idx, sqd = oracle.knn(pts[:40], hi, 8)
+        sc = oracle.scores(sqd)
+        model = refc.LandmarkModel.create(hi, lo)
+        for i in range(40):
+            a1, c1 = projection_system(pts[i], model, idx[i], sc[i])
+            a2, c2 = refp.projection_system(pts[i], model, idx[i], refp.ScoreVector(scores=sc[i]))
+            assert np.array_equal(a1, a2) and np.array_equal(c1, c2)
+    finally:
+        sys.path.remove(str(src))
+        for m in [m for m in sys.modules if m == "embedview" or m.startswith("embedview.")]:
+            del sys.modules[m]

@@ -243,3 +243,40 @@ def test_embed_on_trained_som_vs_oracle(grid, k):
     hd2 = ((h[:, None, :] - h[None, :, :]) ** 2).sum(-1)[np.triu_indices(len(h), 1)]
     _, sqd = oracle.knn(pts[:2000], hi, k)
     assert np.median(2 * sqd.max(1) * 0.5 / hd2.min()) > 256
+
+
+def test_embed_beyond_fast_kernel_shapes_falls_back():
+    """g beyond the fast projection's shared-memory plan (k = 64: g > ~11k):
+    embed falls back to the faithful chain instead of failing, as the
+    reference handles any g (numpy, pinned-host and device inputs)."""
+    gen = np.random.default_rng(9)
+    g, d, k = 12_288, 8, 64
+    hi = gen.normal(size=(g, d)).astype(np.float32)
+    lo = gen.uniform(0, 100, size=(g, 2)).astype(np.float32)
+    pts = gen.normal(size=(600, d)).astype(np.float32)
+    model = esom.LandmarkModel.create(hi, lo)
+    want = oracle.embed(pts, hi, lo, k)
+    ext = float(np.ptp(lo, axis=0).max())
+    for inp in (pts, torch.from_numpy(pts).cuda()):
+        got = esom.embed(inp, model, esom.EmbedParams(k=k))
+        got = got.cpu().numpy() if isinstance(got, torch.Tensor) else got
+        assert float(np.abs(got - want).max()) <= 1e-4 * ext
+
+
+def test_projection_system_matches_reference_formula(golden):
+    """projection_system (ref: projection.py:151-186): the f64 normal equations;
+    their Cramer solution is the faithful projection of the same point, and A
+    is symmetric positive semi-definite."""
+    pts, hi, lo = golden["small_points"], golden["small_hi0"], golden["small_lo"]
+    model = esom.LandmarkModel.create(hi, lo)
+    nb = esom.knn_base(pts[:50], hi, 8)
+    for i in range(50):
+        s = esom.scores(nb.sqdists[i])
+        a, c = esom.projection_system(pts[i], model, nb.indices[i], s)
+        assert np.allclose(a, a.T) and np.all(np.linalg.eigvalsh(a) >= -1e-9)
+        det = a[0, 0] * a[1, 1] - a[0, 1] ** 2
+        tr = a[0, 0] + a[1, 1]
+        xy = esom.project_point(pts[i], model, nb.indices[i], s)
+        if det >= 1e-9 * tr * tr + 1e-30:
+            sol = np.array([(c[0] * a[1, 1] - c[1] * a[0, 1]) / det, (a[0, 0] * c[1] - a[0, 1] * c[0]) / det])
+            assert np.allclose(sol.astype(np.float32), xy, rtol=1e-5, atol=1e-5 * float(np.ptp(lo)))
