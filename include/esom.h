@@ -81,9 +81,12 @@ int esom_project(const float *X, int64_t n, int32_t d, const float *hi, const fl
                  int32_t g, const int32_t *idx, const double *scores, int32_t k, float *xy,
                  cudaStream_t stream);
 
-/* Per-model preparation for the fused path: pack landmarks into TMA tiles
- * and build the g×g pair table (0.5/hd2).  Re-run whenever hi changes. */
-int esom_prepare_model(const float *hi, int32_t g, int32_t d, int32_t k, void *workspace,
+/* Per-model preparation of esom_embed_prepared: landmark tiles, tensor-core
+ * operands (rows ordered along the Morton curve of the layout lo, which
+ * keeps the screen's k-th-distance bound tight for trained SOMs; lo may be
+ * NULL = index order), the g×g pair table (0.5/hd2) and f64 rows.  Re-run
+ * whenever hi or lo changes. */
+int esom_prepare_model(const float *hi, const float *lo, int32_t g, int32_t d, int32_t k, void *workspace,
                        size_t ws_bytes, int32_t *nonfinite_flag, cudaStream_t stream);
 
 /* Per-call scratch of esom_embed_prepared for n points: the neighbour rows

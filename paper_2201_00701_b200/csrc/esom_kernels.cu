@@ -262,13 +262,16 @@ __global__ void center_kernel(const float* __restrict__ hi, int g, int d, int dp
 // bf16 hi/lo in the canonical K-major layout (gpad rows x d16, zero padded),
 // |l'_j|^2 (nearest f32 of the f64 sum; +inf on padding rows) and max |l'_j|,
 // max |l'_j|^2 (rounded up) for the error bounds.
-__global__ void tc_prepare_kernel(const float* __restrict__ hi, int g, int d, int d16, int gpad,
-                                  const float* __restrict__ cen, uint16_t* __restrict__ Bhi,
-                                  uint16_t* __restrict__ Blo, float* __restrict__ ln, float* __restrict__ lstats) {
+__global__ void tc_prepare_kernel(const float* __restrict__ hi0, int g, int d, int d16, int gpad,
+                                  const int32_t* __restrict__ rowmap, const float* __restrict__ cen,
+                                  uint16_t* __restrict__ Bhi, uint16_t* __restrict__ Blo, float* __restrict__ ln,
+                                  float* __restrict__ lstats) {
     const int chunks = d16 / 8;
     const int64_t total = (int64_t)gpad * chunks;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int row = (int)(e / chunks), c0 = (int)(e % chunks) * 8;
+        // screen row `row` holds landmark rowmap[row] (rows >= g: padding)
+        const float* hi = hi0 + (row < g ? (int64_t)(__ldg(rowmap + row) - row) * d : 0);
         uint32_t hw[4], lw[4];
         for (int q = 0; q < 8; q += 2) {
             const float v0 = (row < g && c0 + q < d) ? -2.0f * (hi[(int64_t)row * d + c0 + q] - cen[c0 + q]) : 0.0f;
@@ -304,12 +307,94 @@ __global__ void tc_prepare_kernel(const float* __restrict__ hi, int g, int d, in
 // Exact-phase landmark rows for esom_tc2.cuh: gpad x ls f32, dims >= d and
 // rows >= g zero (a +0 term leaves the reference's sequential sum unchanged;
 // padding rows are never logged: their |l|^2 is +inf).
-__global__ void lrow_kernel(const float* __restrict__ hi, int g, int d, int gpad, int ls, float* __restrict__ Lr) {
+__global__ void lrow_kernel(const float* __restrict__ hi, int g, int d, int gpad, int ls,
+                            const int32_t* __restrict__ rowmap, float* __restrict__ Lr) {
     const int64_t total = (int64_t)gpad * ls;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int j = (int)(e / ls), c = (int)(e % ls);
-        Lr[e] = (j < g && c < d) ? hi[(int64_t)j * d + c] : 0.0f;
+        Lr[e] = (j < g && c < d) ? hi[(int64_t)__ldg(rowmap + j) * d + c] : 0.0f;
     }
+}
+
+// Screen-row order of the landmarks (tensor-core screens, g <= 1024).  The
+// screens bound the k-th distance by the k-th smallest minimum over 32
+// landmark groups (screen row mod 32), which is tight only when a point's k
+// nearest landmarks fall in different groups.  A trained SOM keeps
+// lattice-adjacent landmarks adjacent in hi, and with index order a 4 x 4
+// lattice patch of a 32-wide map fell into 4 groups (C4 trained: 58 exact
+// candidates per point).  Ordering the rows along the Morton curve of the
+// LAYOUT (lo) makes any compact patch span consecutive rows, i.e. distinct
+// groups (C4 trained: 19 candidates; untrained models are unaffected).  One
+// CTA: min/max of lo, 2 x 10-bit Morton keys, bitonic sort of (key, index)
+// (ties by index); lo == NULL or g > 1024: identity.
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v &= 1023u;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+__global__ void __launch_bounds__(1024) screen_order_kernel(const float* __restrict__ lo, int g, int gpad,
+                                                           int32_t* __restrict__ rowmap) {
+    __shared__ uint64_t key[1024];
+    __shared__ float red[4][32];
+    const int t = threadIdx.x;
+    if (lo == nullptr || gpad > 1024) {
+        for (int j = t; j < gpad; j += blockDim.x) rowmap[j] = j;
+        return;
+    }
+    float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    for (int j = t; j < g; j += blockDim.x) {
+        const float x = lo[2 * j], y = lo[2 * j + 1];
+        mnx = fminf(mnx, x); mny = fminf(mny, y); mxx = fmaxf(mxx, x); mxy = fmaxf(mxy, y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+    }
+    if ((t & 31) == 0) {
+        red[0][t >> 5] = mnx; red[1][t >> 5] = mny; red[2][t >> 5] = mxx; red[3][t >> 5] = mxy;
+    }
+    __syncthreads();
+    mnx = red[0][0]; mny = red[1][0]; mxx = red[2][0]; mxy = red[3][0];
+    for (int w = 1; w < 32; ++w) {
+        mnx = fminf(mnx, red[0][w]); mny = fminf(mny, red[1][w]);
+        mxx = fmaxf(mxx, red[2][w]); mxy = fmaxf(mxy, red[3][w]);
+    }
+    const float span = fmaxf(fmaxf(mxx - mnx, mxy - mny), 1e-30f);
+    for (int j = t; j < 1024; j += blockDim.x) {
+        uint64_t kv = ~0ull;  // padding rows sort last, in index order
+        if (j < g) {
+            const float fx = (lo[2 * j] - mnx) / span, fy = (lo[2 * j + 1] - mny) / span;
+            // non-finite layouts (rejected elsewhere) fall back to index order
+            const uint32_t qx = (fx >= 0.0f && fx <= 1.0f) ? (uint32_t)(fx * 1023.0f) : 0u;
+            const uint32_t qy = (fy >= 0.0f && fy <= 1.0f) ? (uint32_t)(fy * 1023.0f) : 0u;
+            kv = ((uint64_t)(spread10(qx) | (spread10(qy) << 1)) << 32) | (uint32_t)j;
+        } else {
+            kv = (~0ull << 32) | (uint32_t)j;
+        }
+        key[j] = kv;
+    }
+    __syncthreads();
+    for (int size = 2; size <= 1024; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int j = t; j < 1024; j += blockDim.x) {
+                const int p = j ^ stride;
+                if (p > j) {
+                    const uint64_t a = key[j], b = key[p];
+                    if ((a > b) == ((j & size) == 0)) {
+                        key[j] = b;
+                        key[p] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int j = t; j < gpad; j += blockDim.x) rowmap[j] = (int32_t)(uint32_t)key[j];
 }
 
 // BMU bucket sort of a chunk's neighbour rows (counting sort on idx[:,0]):
@@ -848,7 +933,7 @@ __global__ void row_norm64_kernel(const float* __restrict__ hi, int g, int d, do
 }
 
 struct ModelLayout {
-    size_t lt, tri, bhi, blo, ln, lstats, lrow, rec, hi64, hn64, total;
+    size_t lt, tri, bhi, blo, ln, lstats, lrow, rowmap, rec, hi64, hn64, total;
     bool has_rec;  // g x g pair records for project_reg3_kernel (k <= 16, g <= 1024)
     int d16, gpad, ls;
     // tensor-core GEMM screen for d > 32 (esom_tc3.cuh): per-model operands + per-chunk scratch
@@ -884,6 +969,8 @@ ModelLayout model_layout(int g, int d, int k, bool with_pairs) {
     o += a256((size_t)m.gpad * 4);
     m.lstats = o;
     o += 256;
+    m.rowmap = o;  // screen row -> landmark index of the tensor-core operands below
+    o += a256((size_t)m.gpad * 4);
     m.ls = 0;
     m.lrow = o;
     if (d <= 32) {  // padded f32 rows of the pipelined tensor-core screen (esom_tc2.cuh)
@@ -939,16 +1026,25 @@ bool tc_enabled() {  // ESOM_TC=0 forces the CUDA-core scan (read per call: test
 // shapes the split-bf16 tensor-core screen handles (smem budget of esom_tc.cuh)
 bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1024 && d <= 32 && g <= 4096 && k <= 16; }
 
-int prepare_tc(const float* hi, int g, int d, const ModelLayout& m, char* ws, cudaStream_t st) {
+// lo (nullable): the layout that orders the screen rows (screen_order_kernel);
+// only the split tc2 screen + exact kernel read the row map, so any other
+// screen that will run gets the identity order
+int tc2_warpgroups();
+int prepare_tc(const float* hi, const float* lo, int g, int d, int k, const ModelLayout& m, char* ws,
+               cudaStream_t st) {
     cudaMemsetAsync(ws + m.lstats, 0, 8, st);
     float* cen = reinterpret_cast<float*>(ws + m.lstats + 128);
+    int32_t* rowmap = reinterpret_cast<int32_t*>(ws + m.rowmap);
+    const bool ordered = lo && tc2_warpgroups() > 0 && m.ls && kp_for(k) <= 16 && m.gpad <= 1024 && m.t2chunk;
+    screen_order_kernel<<<1, 1024, 0, st>>>(ordered ? lo : nullptr, g, m.gpad, rowmap);
     center_kernel<<<(m.d16 + 31) / 32, 1024, 0, st>>>(hi, g, d, m.d16, cen);
     tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
-        hi, g, d, m.d16, m.gpad, cen, reinterpret_cast<uint16_t*>(ws + m.bhi), reinterpret_cast<uint16_t*>(ws + m.blo),
-        reinterpret_cast<float*>(ws + m.ln), reinterpret_cast<float*>(ws + m.lstats));
-    if (int e = cuda_check("tc_prepare_kernel", 2)) return e;  // center + operands
+        hi, g, d, m.d16, m.gpad, rowmap, cen, reinterpret_cast<uint16_t*>(ws + m.bhi),
+        reinterpret_cast<uint16_t*>(ws + m.blo), reinterpret_cast<float*>(ws + m.ln),
+        reinterpret_cast<float*>(ws + m.lstats));
+    if (int e = cuda_check("tc_prepare_kernel", 3)) return e;  // order + center + operands
     if (m.ls) {
-        lrow_kernel<<<grid_for((int64_t)m.gpad * m.ls, 256), 256, 0, st>>>(hi, g, d, m.gpad, m.ls,
+        lrow_kernel<<<grid_for((int64_t)m.gpad * m.ls, 256), 256, 0, st>>>(hi, g, d, m.gpad, m.ls, rowmap,
                                                                           reinterpret_cast<float*>(ws + m.lrow));
         return cuda_check("lrow_kernel");
     }
@@ -990,6 +1086,7 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
     a.Blo = reinterpret_cast<const uint16_t*>(ws + m.blo);
     a.ln = reinterpret_cast<const float*>(ws + m.ln);
     a.Lrow = reinterpret_cast<const float*>(ws + m.lrow);
+    a.rowmap = reinterpret_cast<const int32_t*>(ws + m.rowmap);
     a.ls = m.ls;
     a.L = s.L;
     a.lstats = reinterpret_cast<const float*>(ws + m.lstats);
@@ -1300,7 +1397,7 @@ int esom_knn(const float* X, int64_t n, int32_t d, const float* L, int32_t g, in
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
     if (tc_eligible(n, d, g, k))
-        if (int e = prepare_tc(L, g, d, m, ws, stream)) return e;
+        if (int e = prepare_tc(L, nullptr, g, d, k, m, ws, stream)) return e;
     if (m.t3 && t3_enabled())
         if (int e = prepare_tc3(L, g, d, m, ws, nonfinite_flag, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, L, g, k, Lt, nonfinite_flag);
@@ -1325,7 +1422,7 @@ int esom_project(const float* X, int64_t n, int32_t d, const float* hi, const fl
     return cuda_check("project_kernel");
 }
 
-int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* workspace, size_t ws_bytes,
+int esom_prepare_model(const float* hi, const float* lo, int32_t g, int32_t d, int32_t k, void* workspace, size_t ws_bytes,
                        int32_t* nonfinite_flag, cudaStream_t stream) {
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64 (got %lld)", (long long)k);
     const Plan p = make_plan(d, g, k);
@@ -1352,7 +1449,7 @@ int esom_prepare_model(const float* hi, int32_t g, int32_t d, int32_t k, void* w
     row_norm64_kernel<<<grid_for(g, 128), 128, 0, stream>>>(hi, g, d, reinterpret_cast<double*>(ws + m.hn64));
     if (int e = cuda_check("row_norm64")) return e;
     if (tc_eligible(1 << 20, d, g, k))
-        if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
+        if (int e = prepare_tc(hi, lo, g, d, k, m, ws, stream)) return e;
     if (m.t3 && t3_enabled())
         if (int e = prepare_tc3(hi, g, d, m, ws, nonfinite_flag, stream)) return e;
     return ESOM_OK;
@@ -1487,7 +1584,7 @@ int esom_embed(const float* X, int64_t n, int32_t d, const float* hi, const floa
     if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld", (long long)k, (long long)g);
     const size_t mb = esom_workspace_bytes(g, d, k, 1);
     if (ws_bytes < esom_embed_workspace_bytes(n, g, d, k)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
-    if (int e = esom_prepare_model(hi, g, d, k, workspace, mb, nonfinite_flag, stream)) return e;
+    if (int e = esom_prepare_model(hi, lo, g, d, k, workspace, mb, nonfinite_flag, stream)) return e;
     return esom_embed_prepared(X, n, d, hi, lo, g, k, workspace, reinterpret_cast<char*>(workspace) + mb,
                                ws_bytes - mb, xy, bmu, acc_S, acc_C, acc_fx_bits, qe_sum, nonfinite_flag, stream);
 }
@@ -1508,7 +1605,7 @@ int esom_bmu_accumulate(const float* X, int64_t n, int32_t d, const float* hi, i
                                                                                                    Lt, nonfinite_flag);
     if (int e = cuda_check("pack_landmarks")) return e;
     if (tc_eligible(n, d, g, 1))
-        if (int e = prepare_tc(hi, g, d, m, ws, stream)) return e;
+        if (int e = prepare_tc(hi, nullptr, g, d, 1, m, ws, stream)) return e;
     if (m.t3 && t3_enabled())
         if (int e = prepare_tc3(hi, g, d, m, ws, nonfinite_flag, stream)) return e;
     ScanArgs a = scan_args(p, X, n, d, hi, g, 1, Lt, nonfinite_flag);

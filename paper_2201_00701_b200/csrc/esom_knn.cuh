@@ -86,6 +86,27 @@ __device__ __forceinline__ void topk_insert(float (&td)[KP], int (&ti)[KP], floa
     }
 }
 
+// (distance, index) lexicographic insertion: the (d, j) order of knn_base
+// whatever order the candidates are visited in (the tensor-core screens visit
+// them in screen-row order, a permutation of the landmark indices)
+__device__ __forceinline__ bool key_lt(float va, int ja, float vb, int jb) {
+    return va < vb || (va == vb && ja < jb);
+}
+template <int KP>
+__device__ __forceinline__ void topk_insert_lex(float (&td)[KP], int (&ti)[KP], float v, int j) {
+#pragma unroll
+    for (int q = KP - 1; q > 0; --q) {
+        const bool gp = key_lt(v, j, td[q - 1], ti[q - 1]);
+        const bool gc = key_lt(v, j, td[q], ti[q]);
+        td[q] = gp ? td[q - 1] : (gc ? v : td[q]);
+        ti[q] = gp ? ti[q - 1] : (gc ? j : ti[q]);
+    }
+    if (key_lt(v, j, td[0], ti[0])) {
+        td[0] = v;
+        ti[0] = j;
+    }
+}
+
 // number of values (live or -inf padding) strictly below v
 template <int KP>
 __device__ __forceinline__ int vlist_count_lt(const float (&vd)[KP], float v) {

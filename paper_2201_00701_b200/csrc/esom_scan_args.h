@@ -77,7 +77,8 @@ struct Tc2Args {
     const uint16_t* Bhi;     // gpad×d16 bf16 of -2 l (hi part), canonical K-major
     const uint16_t* Blo;     // lo part
     const float* ln;         // gpad |l_j|^2 (f32, +inf on padding rows)
-    const float* Lrow;       // gpad×ls f32 rows, zero-padded dims (global)
+    const float* Lrow;       // gpad×ls f32 rows, zero-padded dims (global), in screen-row order
+    const int32_t* rowmap;   // screen row -> landmark index (gpad; nullable = identity)
     int ls;                  // Lrow stride (floats, multiple of 4, ls/4 odd)
     const float* L;          // row-major g×d (slow path)
     const float* lstats;     // [0] max|l'_j|, [1] max|l'_j|^2 (centred)

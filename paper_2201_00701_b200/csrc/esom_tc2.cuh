@@ -538,8 +538,10 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (e + u < cnt && s4[u] < td[KP - 1]) topk_insert<KP>(td, ti, s4[u], jq[u]);
+                for (int u = 0; u < 4; ++u) {
+                    const int jo = a.rowmap ? __ldg(a.rowmap + jq[u]) : jq[u];  // screen row -> landmark
+                    if (e + u < cnt && key_lt(s4[u], jo, td[KP - 1], ti[KP - 1])) topk_insert_lex<KP>(td, ti, s4[u], jo);
+                }
             }
 #pragma unroll
             for (int q = 0; q < KP; ++q) {
@@ -637,6 +639,9 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
     // per-thread copy of the point's candidate bitmap ([word][thread]): the extraction
     // then waits on shared, not global, memory
     uint32_t* bsm = reinterpret_cast<uint32_t*>(smem_raw + ((r_bytes + 127) / 128) * 128) + tid;
+    // screen row -> landmark index (after the bitmaps)
+    int32_t* rmap = reinterpret_cast<int32_t*>(bsm - tid + (size_t)nwords * kExactBitsThreads);
+    for (int j = tid; j < a.gpad; j += kExactBitsThreads) rmap[j] = a.rowmap ? __ldg(a.rowmap + j) : j;
     if (tid == 0) {
         mbar_init(&bar_load, 1);
         fence_mbar_init();
@@ -791,14 +796,14 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                 bool amb = !(L[15] < kInf) || dmin == L[15];
 #pragma unroll
                 for (int q = 0; q < 15; ++q) amb |= L[q] == L[q + 1];
-                if (!amb) {
+                if (!amb) {  // distinct distances: value order is the (d, j) order
 #pragma unroll
                     for (int q = 0; q < 16; ++q)
                         if (oi) {
-                            oi[q] = LJ[q];
+                            oi[q] = rmap[LJ[q]];
                             od[q] = L[q];
                         }
-                    b0 = LJ[0];
+                    b0 = rmap[LJ[0]];
                     d0 = L[0];
                     written = k;
                     done = true;
@@ -819,8 +824,11 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                     float s4[4];
                     next4(wi, m, nz, jq, s4);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (e + u < cnt && s4[u] < td[KP - 1]) topk_insert<KP>(td, ti, s4[u], jq[u]);
+                    for (int u = 0; u < 4; ++u) {
+                        const int jo = rmap[jq[u]];  // screen row -> landmark index
+                        if (e + u < cnt && key_lt(s4[u], jo, td[KP - 1], ti[KP - 1]))
+                            topk_insert_lex<KP>(td, ti, s4[u], jo);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < KP; ++q) {
@@ -861,7 +869,8 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
 
 template <int KP>
 int launch_exact_bits_t(Tc2Args a, cudaStream_t st) {
-    const size_t smem = ((size_t)a.gpad * a.ls * 4 + 127) / 128 * 128 + (size_t)(a.gpad / 32) * kExactBitsThreads * 4;
+    const size_t smem = ((size_t)a.gpad * a.ls * 4 + 127) / 128 * 128 + (size_t)(a.gpad / 32) * kExactBitsThreads * 4 +
+                        (size_t)a.gpad * 4;  // + the row map
     if (smem > (size_t)esom_host::max_smem_optin())
         return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact rows exceed shared memory%s", "");
     auto kern = knn_exact_bits_kernel<KP>;

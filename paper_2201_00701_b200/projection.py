@@ -169,7 +169,7 @@ class PreparedModel:
                 self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
             if getattr(self, "flag", None) is None:
                 self.flag = _dev.new_flag(dev)
-            _lib.call("esom_prepare_model", _dev.ptr(self.hi), self.g, self.d, self.k, _dev.ptr(self.ws),
+            _lib.call("esom_prepare_model", _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.d, self.k, _dev.ptr(self.ws),
                       self.ws.numel(), _dev.ptr(self.flag), _dev.stream_handle(dev))
         return self
 

@@ -41,4 +41,10 @@ for t in (0, ticks):
         if c.value:
             out[name] = round(ms, 4)
     L.esom_timing_begin(0)
-    print(json.dumps({"workload": wl, "ticks": t, "bmu_order": loop.bmu_order, "kernels_ms": out}), flush=True)
+    cnt = torch.zeros(8, dtype=torch.int32, device=dev)
+    L.esom_set_tc_stats(cnt.data_ptr())
+    loop._eager_frame()
+    torch.cuda.synchronize()
+    L.esom_set_tc_stats(None)
+    print(json.dumps({"workload": wl, "ticks": t, "bmu_order": loop.bmu_order, "kernels_ms": out,
+                      "cand_per_pt": int(cnt[0].item()) / X.shape[0], "slow_pts": int(cnt[1].item())}), flush=True)
