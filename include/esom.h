@@ -161,6 +161,12 @@ int esom_batch_som_update(const int64_t *acc_S, const int64_t *acc_C, int32_t ac
                           const float *lo, int32_t g, int32_t d, double sigma, double alpha,
                           int32_t mode, float *hi_inout, cudaStream_t stream);
 
+/* Page-lock / release a caller-owned host range in place (cudaHostRegister):
+ * repeated host inputs then DMA straight from the caller's buffer.  Errors
+ * are returned (and cleared), never left pending. */
+int esom_host_register(void *p, size_t bytes);
+int esom_host_unregister(void *p);
+
 /* ---- data formats either side of the path ---- */
 
 /* Frame colours: rint((X[:, color_dim] - lo) / span * 255) as u8, 128 when

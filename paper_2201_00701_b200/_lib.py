@@ -38,6 +38,8 @@ SIGNATURES = {
     "esom_som_tick": [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _f64, _f64, _vp, _sz, _vp],
     "esom_kmeans_tick": [_vp, _i32, _vp, _i32, _vp, _i32, _f64, _vp, _sz, _vp],
     "esom_batch_som_update": [_vp, _vp, _i32, _vp, _i32, _i32, _f64, _f64, _i32, _vp, _vp],
+    "esom_host_register": [_vp, _sz],
+    "esom_host_unregister": [_vp],
     "esom_color_channel": [_vp, _i64, _i32, _i32, _f64, _f64, _vp, _vp],
     "esom_frame_points_pack": [_vp, _vp, _i64, C.c_uint32, _vp, _vp],
     "esom_fcs_decode": [_vp, _i64, _i32, _vp, _vp, _vp],

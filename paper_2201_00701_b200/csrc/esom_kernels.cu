@@ -1662,4 +1662,23 @@ int esom_batch_som_update(const int64_t* acc_S, const int64_t* acc_C, int32_t ac
     return cuda_check("batch_update_kernel");
 }
 
+// Page-lock a caller-owned host range in place (the numpy-input pipeline of
+// embed pins arrays it sees repeatedly).  A failure is reported and cleared,
+// so it cannot surface later as a kernel launch error.
+int esom_host_register(void* p, size_t bytes) {
+    if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        return set_err(ESOM_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+    }
+    return ESOM_OK;
+}
+
+int esom_host_unregister(void* p) {
+    if (cudaHostUnregister(p) != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        return set_err(ESOM_ERR_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+    }
+    return ESOM_OK;
+}
+
 }  // extern "C"

@@ -273,8 +273,57 @@ def _pipelinable_host(points):
             return points
         return None
     if isinstance(points, np.ndarray) and points.dtype == np.float32 and points.flags.c_contiguous:
-        return points
+        pinned = _pinned_in_place(points)
+        return pinned if pinned is not None else points
     return None
+
+
+# numpy inputs embedded repeatedly (the interactive loop re-projects the same
+# dataset every frame) are pinned IN PLACE on their second use
+# (cudaHostRegister), so later calls DMA straight from the caller's array at
+# full PCIe speed; the range is unpinned when the array is garbage collected.
+# One-shot inputs keep the staged copy (registration costs about as much as
+# the copy).  Bounded by _HOST_REG_CAP bytes.
+_HOST_REG: dict = {}
+_HOST_SEEN: dict = {}
+_HOST_REG_CAP = 16 << 30
+_HOST_LOCK = None
+
+
+def _pinned_in_place(host: np.ndarray):
+    import threading
+    import weakref
+
+    global _HOST_LOCK
+    if _HOST_LOCK is None:
+        _HOST_LOCK = threading.Lock()
+    ptr = int(host.__array_interface__["data"][0])
+    key = (ptr, int(host.nbytes))
+    owner = host
+    while isinstance(owner.base, np.ndarray):
+        owner = owner.base
+    if owner.base is not None or host.nbytes < (8 << 20):
+        return None  # foreign buffer (mmap, bytes, ...) or too small to matter
+    with _HOST_LOCK:
+        if key in _HOST_REG:
+            return torch.from_numpy(host)
+        oid = id(owner)
+        if _HOST_SEEN.get(key) != oid:  # first use: remember, copy through staging
+            _HOST_SEEN.clear()
+            _HOST_SEEN[key] = oid
+            return None
+        if sum(k[1] for k in _HOST_REG) + key[1] > _HOST_REG_CAP:
+            return None
+        if _lib.load().esom_host_register(ptr, key[1]) != 0:
+            return None  # (already registered by someone else, or no memory to lock)
+
+        def _release(k=key):
+            with _HOST_LOCK:
+                if _HOST_REG.pop(k, None) is not None:
+                    _lib.load().esom_host_unregister(k[0])
+
+        _HOST_REG[key] = weakref.finalize(owner, _release)
+    return torch.from_numpy(host)
 
 
 def _embed_host_pipelined(host, model, k: int, dev) -> np.ndarray:

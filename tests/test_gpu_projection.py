@@ -280,3 +280,29 @@ def test_projection_system_matches_reference_formula(golden):
         if det >= 1e-9 * tr * tr + 1e-30:
             sol = np.array([(c[0] * a[1, 1] - c[1] * a[0, 1]) / det, (a[0, 0] * c[1] - a[0, 1] * c[0]) / det])
             assert np.allclose(sol.astype(np.float32), xy, rtol=1e-5, atol=1e-5 * float(np.ptp(lo)))
+
+
+def test_numpy_input_pinned_in_place_on_reuse():
+    """embed(numpy) through the chunked host pipeline: the first call stages the
+    rows through pinned chunks, a repeated call pins the caller's array in
+    place (cudaHostRegister) and DMAs from it; results identical, and the
+    range is released when the array is collected."""
+    import gc
+
+    from paper_2201_00701_b200 import projection as P
+
+    pts, hi, lo = c2_inputs()
+    x = np.array(pts[: 1 << 19])  # a fresh owning array (8 MiB+)
+    model = esom.LandmarkModel.create(hi, lo)
+    params = esom.EmbedParams(k=16)
+    a = esom.embed(x, model, params)
+    n0 = len(P._HOST_REG)
+    b = esom.embed(x, model, params)
+    c = esom.embed(x, model, params)
+    assert len(P._HOST_REG) == n0 + 1
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    want = esom.embed(torch.from_numpy(pts[: 1 << 19]).cuda(), model, params).cpu().numpy()
+    assert np.array_equal(a, want)
+    del x
+    gc.collect()
+    assert len(P._HOST_REG) == n0
