@@ -388,8 +388,9 @@ def run_ours(args):
     barrier()
     # one frame = one CUDA-graph launch; with training at N > 1 the graph holds the
     # NCCL all-reduce of the statistics too (eager frames if capture is refused)
-    use_graph = not args.no_graph
-    graph_note = None
+    # (gloo dry runs cannot capture collectives: training frames then run eagerly)
+    use_graph = not args.no_graph and (world == 1 or not train or args.dist_backend == "nccl")
+    graph_note = None if use_graph or args.no_graph else "eager frames: a gloo collective cannot be captured"
     if use_graph:
         try:
             loop.capture()
@@ -535,7 +536,7 @@ def run_ours(args):
             "frame": frame_view,
             "clocks": clocks,
             "gpu_launches": launches_timed,
-            "cuda_graph": use_graph if not graph_note else {"used": False, "note": graph_note},
+            "cuda_graph": use_graph if graph_note is None else {"used": False, "note": graph_note},
             "e2e": e2e,
             "e2e_numpy": e2e_numpy,
             "cpu_baseline": cpu,

@@ -86,8 +86,9 @@ int esom_project(const float *X, int64_t n, int32_t d, const float *hi, const fl
  * keeps the screen's k-th-distance bound tight for trained SOMs; lo may be
  * NULL = index order), the g×g pair table (0.5/hd2) and f64 rows.  Re-run
  * whenever hi or lo changes. */
-int esom_prepare_model(const float *hi, const float *lo, int32_t g, int32_t d, int32_t k, void *workspace,
-                       size_t ws_bytes, int32_t *nonfinite_flag, cudaStream_t stream);
+#define ESOM_PREPARE_KEEP_ORDER 1  /* lo unchanged since the last preparation of this workspace */
+int esom_prepare_model(const float *hi, const float *lo, int32_t g, int32_t d, int32_t k, int32_t flags,
+                       void *workspace, size_t ws_bytes, int32_t *nonfinite_flag, cudaStream_t stream);
 
 /* Per-call scratch of esom_embed_prepared for n points: the neighbour rows
  * of one L2-resident chunk of points (scan -> projection). */

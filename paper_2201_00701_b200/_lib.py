@@ -28,7 +28,7 @@ SIGNATURES = {
     "esom_knn": [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp],
     "esom_scores": [_vp, _i64, _i32, _vp, _vp],
     "esom_project": [_vp, _i64, _i32, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp],
-    "esom_prepare_model": [_vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp, _vp],
+    "esom_prepare_model": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp, _vp],
     "esom_embed_prepared": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _i32, _vp,
                             _vp, _vp],
     "esom_embed_prepared_ex": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _i32,

@@ -412,23 +412,34 @@ __global__ void bmu_hist_kernel(const int32_t* __restrict__ idx, int64_t n, int 
 }
 
 __global__ void bmu_scan_kernel(int32_t* __restrict__ cnt, int g) {  // one CTA: exclusive scan in place
-    __shared__ int32_t part[1024];
+    // each thread sums a contiguous chunk, then a warp-shuffle block scan of the
+    // chunk sums (a serial pass over 1024 partials by one thread cost ~9 us)
+    __shared__ int32_t wsum[32];
     const int per = (g + blockDim.x - 1) / blockDim.x;
     const int b0 = threadIdx.x * per;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int s = 0;
     for (int b = b0; b < b0 + per && b < g; ++b) s += cnt[b];
-    part[threadIdx.x] = s;
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int t = 0; t < (int)blockDim.x; ++t) {
-            const int v = part[t];
-            part[t] = acc;
-            acc += v;
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        int v = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
         }
+        if (lane < nw) wsum[lane] = v;  // inclusive scan of the warp sums
     }
     __syncthreads();
-    int acc = part[threadIdx.x];
+    int acc = incl - s + (w > 0 ? wsum[w - 1] : 0);
     for (int b = b0; b < b0 + per && b < g; ++b) {
         const int v = cnt[b];
         cnt[b] = acc;
@@ -1031,18 +1042,19 @@ bool tc_eligible(int64_t n, int d, int g, int k) { return tc_enabled() && n >= 1
 // screen that will run gets the identity order
 int tc2_warpgroups();
 int prepare_tc(const float* hi, const float* lo, int g, int d, int k, const ModelLayout& m, char* ws,
-               cudaStream_t st) {
+               cudaStream_t st, bool keep_order = false) {
     cudaMemsetAsync(ws + m.lstats, 0, 8, st);
     float* cen = reinterpret_cast<float*>(ws + m.lstats + 128);
     int32_t* rowmap = reinterpret_cast<int32_t*>(ws + m.rowmap);
     const bool ordered = lo && tc2_warpgroups() > 0 && m.ls && kp_for(k) <= 16 && m.gpad <= 1024 && m.t2chunk;
-    screen_order_kernel<<<1, 1024, 0, st>>>(ordered ? lo : nullptr, g, m.gpad, rowmap);
+    if (!keep_order)  // (the caller's layout is unchanged since the last preparation: keep its order)
+        screen_order_kernel<<<1, 1024, 0, st>>>(ordered ? lo : nullptr, g, m.gpad, rowmap);
     center_kernel<<<(m.d16 + 31) / 32, 1024, 0, st>>>(hi, g, d, m.d16, cen);
     tc_prepare_kernel<<<grid_for((int64_t)m.gpad * (m.d16 / 8), 256), 256, 0, st>>>(
         hi, g, d, m.d16, m.gpad, rowmap, cen, reinterpret_cast<uint16_t*>(ws + m.bhi),
         reinterpret_cast<uint16_t*>(ws + m.blo), reinterpret_cast<float*>(ws + m.ln),
         reinterpret_cast<float*>(ws + m.lstats));
-    if (int e = cuda_check("tc_prepare_kernel", 3)) return e;  // order + center + operands
+    if (int e = cuda_check("tc_prepare_kernel", keep_order ? 2 : 3)) return e;  // (order) + center + operands
     if (m.ls) {
         lrow_kernel<<<grid_for((int64_t)m.gpad * m.ls, 256), 256, 0, st>>>(hi, g, d, m.gpad, m.ls, rowmap,
                                                                           reinterpret_cast<float*>(ws + m.lrow));
@@ -1422,7 +1434,8 @@ int esom_project(const float* X, int64_t n, int32_t d, const float* hi, const fl
     return cuda_check("project_kernel");
 }
 
-int esom_prepare_model(const float* hi, const float* lo, int32_t g, int32_t d, int32_t k, void* workspace, size_t ws_bytes,
+int esom_prepare_model(const float* hi, const float* lo, int32_t g, int32_t d, int32_t k, int32_t flags, void* workspace,
+                       size_t ws_bytes,
                        int32_t* nonfinite_flag, cudaStream_t stream) {
     if (k > 64) return set_err(ESOM_ERR_UNSUPPORTED, "fused embed supports k <= 64 (got %lld)", (long long)k);
     const Plan p = make_plan(d, g, k);
@@ -1449,7 +1462,7 @@ int esom_prepare_model(const float* hi, const float* lo, int32_t g, int32_t d, i
     row_norm64_kernel<<<grid_for(g, 128), 128, 0, stream>>>(hi, g, d, reinterpret_cast<double*>(ws + m.hn64));
     if (int e = cuda_check("row_norm64")) return e;
     if (tc_eligible(1 << 20, d, g, k))
-        if (int e = prepare_tc(hi, lo, g, d, k, m, ws, stream)) return e;
+        if (int e = prepare_tc(hi, lo, g, d, k, m, ws, stream, (flags & ESOM_PREPARE_KEEP_ORDER) != 0)) return e;
     if (m.t3 && t3_enabled())
         if (int e = prepare_tc3(hi, g, d, m, ws, nonfinite_flag, stream)) return e;
     return ESOM_OK;
@@ -1584,7 +1597,7 @@ int esom_embed(const float* X, int64_t n, int32_t d, const float* hi, const floa
     if (k < 1 || k > g) return set_err(ESOM_ERR_PARAM, "k=%lld violates 1 <= k <= g=%lld", (long long)k, (long long)g);
     const size_t mb = esom_workspace_bytes(g, d, k, 1);
     if (ws_bytes < esom_embed_workspace_bytes(n, g, d, k)) return set_err(ESOM_ERR_PARAM, "workspace too small%s", "");
-    if (int e = esom_prepare_model(hi, lo, g, d, k, workspace, mb, nonfinite_flag, stream)) return e;
+    if (int e = esom_prepare_model(hi, lo, g, d, k, 0, workspace, mb, nonfinite_flag, stream)) return e;
     return esom_embed_prepared(X, n, d, hi, lo, g, k, workspace, reinterpret_cast<char*>(workspace) + mb,
                                ws_bytes - mb, xy, bmu, acc_S, acc_C, acc_fx_bits, qe_sum, nonfinite_flag, stream);
 }

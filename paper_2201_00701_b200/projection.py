@@ -157,8 +157,11 @@ class PreparedModel:
         self.update(hi, lo)
 
     def update(self, hi=None, lo=None):
+        """Re-prepare after hi (and/or lo) changed.  The screen-row order
+        derives from lo alone, so it is kept when no new lo is given."""
         dev = self.device
         with torch.cuda.device(dev):
+            keep = lo is None and getattr(self, "ws", None) is not None
             if hi is not None:
                 self.hi = _dev.to_f32(hi, dev)
             if lo is not None:
@@ -167,9 +170,11 @@ class PreparedModel:
             nbytes = _lib.load().esom_workspace_bytes(self.g, self.d, self.k, 1)
             if getattr(self, "ws", None) is None or self.ws.numel() < nbytes:
                 self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+                keep = False
             if getattr(self, "flag", None) is None:
                 self.flag = _dev.new_flag(dev)
-            _lib.call("esom_prepare_model", _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.d, self.k, _dev.ptr(self.ws),
+            _lib.call("esom_prepare_model", _dev.ptr(self.hi), _dev.ptr(self.lo), self.g, self.d, self.k,
+                      1 if keep else 0, _dev.ptr(self.ws),
                       self.ws.numel(), _dev.ptr(self.flag), _dev.stream_handle(dev))
         return self
 

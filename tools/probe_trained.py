@@ -2,7 +2,7 @@
 trained model (T online SOM ticks), through FrameLoop (census-chosen visiting
 order), for ncu captures of the trained projection.
 
-    python tools/probe_trained.py [ticks] [workload]
+    python tools/probe_trained.py [ticks] [workload] [only]
 """
 import ctypes
 import json
@@ -24,7 +24,8 @@ dev = torch.device("cuda", 0)
 pts, hi, lo, k, train, n_total = make_inputs(wl, 0, 1)
 X = torch.from_numpy(pts).to(dev)
 L = _lib.load()
-for t in (0, ticks):
+only = len(sys.argv) > 3 and sys.argv[3] == "only"  # the trained model alone (ncu captures)
+for t in ((ticks,) if only else (0, ticks)):
     h = train_model(X, hi, lo, t, 1) if t else hi
     loop = FrameLoop(X, h, lo, k, train=False)
     for _ in range(3):
