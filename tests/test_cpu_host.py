@@ -221,3 +221,23 @@ def test_projection_system_equals_reference(golden):
         sys.path.remove(str(src))
         for m in [m for m in sys.modules if m == "embedview" or m.startswith("embedview.")]:
             del sys.modules[m]
+
+
+def test_bench_rank_slices_tile_the_survey_dataset(monkeypatch):
+    """bench.py's per-rank inputs: contiguous row blocks of ONE §8d dataset
+    (same centres everywhere) and the same landmarks on every rank, drawn
+    from the whole dataset (weak: n per rank; strong: the n rows split)."""
+    import bench
+    from paper_2201_00701_b200 import datagen
+
+    monkeypatch.setitem(bench.WORKLOADS, "tw", (4, 3000, 5, 4, 4, 8, False, "weak", "test weak"))
+    monkeypatch.setitem(bench.WORKLOADS, "ts", (4, 7001, 5, 4, 4, 8, True, "strong", "test strong"))
+    for name, world, n_total in (("tw", 3, 9000), ("ts", 4, 7001)):
+        full = datagen.gaussians(4, n_total, 5, seed=1)[0]
+        hi_full, lo_full = datagen.som_model(full, 4, 4, seed=2)
+        parts = []
+        for r in range(world):
+            pts, hi, lo, k, train, nt = bench.make_inputs(name, r, world)
+            assert nt == n_total and np.array_equal(hi, hi_full) and np.array_equal(lo, lo_full)
+            parts.append(pts)
+        assert np.array_equal(np.concatenate(parts), full)
