@@ -436,8 +436,8 @@ def run_ours(args):
     loop._eager_frame()
     torch.cuda.synchronize(dev)
     ktimes = {}
-    for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "knn_gemm_kernel", "knn_exact_group_kernel",
-                 "project_kernel"):
+    for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "embed_fused_kernel", "knn_gemm_kernel",
+                 "knn_exact_group_kernel", "project_kernel"):
         cnt = ctypes.c_int32(0)
         ms_k = L.esom_timing_query(name.encode(), ctypes.byref(cnt))
         if cnt.value:
@@ -469,7 +469,9 @@ def run_ours(args):
                         "note": "achieved = algorithmic 2gd flops/point (one x.L^T); the kernel issues 6x that "
                                 "in bf16 MMAs (3 split products, group-min pass + candidate pass)"}
         else:
-            per_pt = (4 * d + 8 * k) if dom.startswith("knn") else (8 * k + 8)
+            # k-NN kernels: X + idx/sqd rows; projection: idx/sqd rows + xy; the fused exact +
+            # projection kernel: the embed's own bytes, X + xy
+            per_pt = {"embed_fused_kernel": 4 * d + 8}.get(dom, (4 * d + 8 * k) if dom.startswith("knn") else (8 * k + 8))
             achieved = n * per_pt / (kms * 1e-3) / 1e9
             roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                         "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -1080,7 +1080,8 @@ int launch_tc2_w(Tc2Args a, int W, cudaStream_t st) {
 }
 
 // pipelined screen (esom_tc2.cuh); ESOM_ERR_UNSUPPORTED when the shape does not fit
-int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st) {
+int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st,
+                 const ProjArgs* fuse = nullptr, bool* fused_done = nullptr) {
     const int W = tc2_warpgroups();
     // the non-empty-word mask of the candidate bitmaps is one 32-bit word:
     // gpad <= 1024 (larger g: the round-streaming esom_tc.cuh screen; the
@@ -1143,6 +1144,27 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
                                       const_cast<int32_t*>(c.perm), st))
                     return e2;
             }
+            if (fuse && p.kp == 16) {  // embed: exact phase + projection in one kernel
+                ProjArgs q = *fuse;
+                q.n = c.n;
+                q.X = fuse->X + s0 * s.d;
+                q.xy = fuse->xy + 2 * s0;
+                q.idx = fuse->idx + s0 * s.k;
+                q.sqd = fuse->sqd + s0 * s.k;
+                c.out_idx = nullptr;
+                c.out_sqd = nullptr;
+                KTimer tmf("embed_fused_kernel", st);
+                e = launch_embed_fused_c(c, q, st);
+                if (e == ESOM_OK) {
+                    if (fused_done) *fused_done = true;
+                    continue;
+                }
+                if (e != ESOM_ERR_UNSUPPORTED) return e;
+                g_err[0] = 0;
+                c.out_idx = s.out_idx ? s.out_idx + s0 * s.k : nullptr;
+                c.out_sqd = s.out_sqd ? s.out_sqd + s0 * s.k : nullptr;
+            }
+            if (fused_done) *fused_done = false;
             KTimer tm2("knn_exact_bits_kernel", st);
             e = p.kp == 4 ? launch_exact_bits_t<4>(c, st) : p.kp == 8 ? launch_exact_bits_t<8>(c, st)
                                                                       : launch_exact_bits_t<16>(c, st);
@@ -1159,9 +1181,10 @@ int dispatch_tc2(const Plan& p, const ModelLayout& m, const ScanArgs& s, const c
     return ESOM_ERR_UNSUPPORTED;
 }
 
-int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st) {
+int dispatch_tc(const Plan& p, const ModelLayout& m, const ScanArgs& s, const char* ws, cudaStream_t st,
+                const ProjArgs* fuse = nullptr, bool* fused_done = nullptr) {
     {
-        const int e = dispatch_tc2(p, m, s, ws, st);
+        const int e = dispatch_tc2(p, m, s, ws, st, fuse, fused_done);
         if (e != ESOM_ERR_UNSUPPORTED) return e;
         g_err[0] = 0;
     }
@@ -1284,9 +1307,13 @@ int run_t3(const ModelLayout& m, const ScanArgs& a, const char* wsc, cudaStream_
 }
 
 // k-NN over a prepared model workspace: tensor-core screen when eligible, else the CUDA-core scan
-int run_knn(const Plan& p, const ModelLayout& m, ScanArgs a, const char* ws, cudaStream_t st) {
+// fuse (embed only): when the split tc2 path runs, the projection is fused into the
+// exact phase (*fused_done = true: the caller skips its projection launch)
+int run_knn(const Plan& p, const ModelLayout& m, ScanArgs a, const char* ws, cudaStream_t st,
+            const ProjArgs* fuse = nullptr, bool* fused_done = nullptr) {
+    if (fused_done) *fused_done = false;
     if (tc_eligible(a.n, a.d, a.g, a.k)) {
-        const int e = dispatch_tc(p, m, a, ws, st);
+        const int e = dispatch_tc(p, m, a, ws, st, fuse, fused_done);
         if (e != ESOM_ERR_UNSUPPORTED) return e;
     }
     if (m.t3 && t3_enabled() && a.n >= 256 && a.d <= 1536) return run_t3(m, a, ws, st);
@@ -1512,11 +1539,32 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         a.out_sqd = sqd;
         a.bmu = bmu ? bmu + s : nullptr;
         a.qe_sum = qe_sum;  // batch-SOM sums come from the BMU-sorted order below (no atomics)
-        if (int e = run_knn(p, ml, a, mws, stream)) return e;
-        ProjArgs q{};
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
         const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
         const bool need_perm = l2_table || ((use_rec || bmu_order) && m >= 4096);
+        ProjArgs q{};
+        q.idx = idx;
+        q.sqd = sqd;
+        q.n = m;
+        q.k = k;
+        q.g = g;
+        q.lo = lo;
+        q.T = T;
+        q.tmax = reinterpret_cast<const float*>(mws + ml.lstats) + 2;
+        q.prec_count = far_count;
+        q.far_heavy = bmu_order ? 1 : 0;
+        q.xy = xy + 2 * s;
+        q.X = X + s * d;
+        q.hi = hi;
+        q.hi64 = reinterpret_cast<const double*>(mws + ml.hi64);
+        q.hn64 = reinterpret_cast<const double*>(mws + ml.hn64);
+        q.d = d;
+        q.rec = use_rec ? rec : nullptr;
+        // the exact phase and the projection in one kernel when the projection would
+        // run in natural order from the shared-memory pair triangle (not far-heavy)
+        const bool try_fuse = p.kp == 16 && k == 16 && !need_perm && !use_rec && !bmu_order;
+        bool fused = false;
+        if (int e = run_knn(p, ml, a, mws, stream, try_fuse ? &q : nullptr, &fused)) return e;
         const bool acc_smem = (acc_S || acc_C) && !need_perm && accum_smem_ok(g, d);
         if (acc_smem) {
             const size_t smem = ((size_t)g * d + g) * 8;
@@ -1541,25 +1589,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
             }
             if (l2_table || use_rec || bmu_order) q.perm = perm;
         }
-        q.idx = idx;
-        q.sqd = sqd;
-        q.n = m;
-        q.k = k;
-        q.g = g;
-        q.lo = lo;
-        q.T = T;
-        q.tmax = reinterpret_cast<const float*>(mws + ml.lstats) + 2;
-        q.prec_count = far_count;
-        q.far_heavy = bmu_order ? 1 : 0;
-        q.xy = xy + 2 * s;
-        q.X = X + s * d;
-        q.hi = hi;
-        q.hi64 = reinterpret_cast<const double*>(mws + ml.hi64);
-
-        q.hn64 = reinterpret_cast<const double*>(mws + ml.hn64);
-        q.d = d;
-        q.rec = use_rec ? rec : nullptr;
-        {
+        if (!fused) {
             KTimer tm("project_kernel", stream);
             if (int e = dispatch_project(p.kp, q, stream)) return e;
         }

@@ -421,6 +421,147 @@ __host__ __device__ inline int reg2_hi64_stride(int d) {
     return 2 * (u | 1);
 }
 
+// One point of project_reg2_kernel: scores + law-of-cosines projection from the
+// point's k neighbour indices jj and exact squared distances sq (slots >= k:
+// padding with zero weight).  Shared with the fused embed kernel
+// (esom_fused.cuh; STORE_ROW: the rows are in registers only, so the rare
+// faithful fallback first writes them to the point workspace).
+template <int KP, bool TSMEM, bool HSMEM, bool FARHEAVY, bool STORE_ROW>
+__device__ __forceinline__ void reg2_point(const ProjArgs& a, int64_t i, const int (&jj)[KP], const float (&sq)[KP],
+                                           const float2* LO, const int* RB, const float* T, const double* h64,
+                                           const double* hn_s, int hs, float tmax_model) {
+    const int k = a.k;
+    int rb[KP];
+    float sc[KP], lx[KP], ly[KP];
+    float sqmax = 0.0f;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) sqmax = fmaxf(sqmax, sq[q]);
+    const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
+    count_prec(a.prec_count, prec);
+    // far from the landmarks: the k squared distances again in f64, kept as f32
+    // offsets from the nearest (precise_sqd); first, while little else is live
+    float qe[KP];
+    if (prec) {
+        if (a.d == 32)
+            precise_sqd_fixed<KP, 32, HSMEM, FARHEAVY>(a.X + i * 32, HSMEM ? h64 : a.hi64, HSMEM ? hs : 32,
+                                             HSMEM ? hn_s : a.hn64, jj, k, qe);
+        else
+            precise_sqd<KP, HSMEM>(a.X + i * a.d, a.d, HSMEM ? h64 : a.hi64, HSMEM ? hs : a.d, jj, k, qe);
+    } else {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) qe[q] = sq[q];
+    }
+    const float2 o = LO[jj[0]];
+    float sig = 0.0f, sqk = 0.0f;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+        const float2 l = LO[jj[q]];
+        lx[q] = l.x - o.x;  // layout about the nearest landmark
+        ly[q] = l.y - o.y;
+        rb[q] = RB[jj[q]];
+        const float dq = q < k ? sqrt_approx(sq[q]) : 0.0f;
+        sig += dq;
+        if (q == k - 1) sqk = sq[q];
+    }
+    // scores (ref: projection.py:38-59) in f32, as the scale-free weights
+    // s_q / tail = expm1((d_k^2 - d_q^2) / 2 sigma^2): the normal equations
+    // are homogeneous in w, and the difference form keeps full relative
+    // precision where the reference's e_q - tail cancels (far outliers).
+    sig = sig / (float)k;
+    bool uniform = sig < (float)kScoreEps;
+    if (!uniform) {
+        const float inv = 1.0f / (2.0f * sig * sig);
+        const float tail = ex2_approx(-1.44269504f * sqk * inv);
+        float dls[KP];
+        if (prec) {  // far points: exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
+            const double dk = (double)__fsqrt_rn(sqk);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                const double dq = (double)__fsqrt_rn(sq[q]);
+                dls[q] = q < k ? (float)((dk * dk - dq * dq) * (double)inv) : 0.0f;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) dls[q] = q < k ? (sqk - sq[q]) * inv : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const float dl = dls[q];  // >= 0 (rows ascending); 0 at q = k-1
+            const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
+                                                                   1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+            const float e = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
+            sc[q] = e;
+            if (q == 0)  // the reference's s_0 = e_0 - tail < 1e-9 test (no underflow of tail * e)
+                uniform = ex2_approx(-1.44269504f * sq[0] * inv) - tail < (float)kScoreEps;
+        }
+    }
+    if (uniform) {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
+    }
+
+    float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
+    // all pairs u < v, fully unrolled (static register indices, no ring rotation).
+    // Slot KP-1 never pairs: its score is exactly 0 (the reference's tail
+    // s_{k-1} = 0 when k == KP, the uniform fallback's trailing 0, or padding).
+#pragma unroll
+    for (int u = 0; u < KP - 2; ++u) {
+#pragma unroll
+        for (int v = u + 1; v < KP - 1; ++v) {
+            const float w = sc[u] * sc[v];
+            const int ti = max(jj[u] < jj[v] ? rb[u] + jj[v] : rb[v] + jj[u], 0);
+            const float tv = T[ti];
+            const float ex = __fsub_rn(lx[v], lx[u]), ey = __fsub_rn(ly[v], ly[u]);
+            const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
+            const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
+            tmax = keep ? fmaxf(tmax, tv) : tmax;
+            const float rr = keep ? rcp_approx(ld2) : 0.0f;  // g = 0 for skipped pairs (ld2 may be 0)
+            const float wr = w * rr;
+            const float g1 = ex * rr, g2 = ey * rr;
+            // dnum/hd2 by the law of cosines + g . (lo_u - o)
+            const float h = fmaf(qe[u] - qe[v], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
+            const float wg1 = wr * ex, wg2 = wr * ey;  // w g
+            a11 = fmaf(wg1, g1, a11);
+            a12 = fmaf(wg1, g2, a12);
+            a22 = fmaf(wg2, g2, a22);
+            c1 = fmaf(wg1, h, c1);
+            c2 = fmaf(wg2, h, c2);
+        }
+    }
+    double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
+    float spread = sqmax;  // prec: the error of qe_u - qe_v scales with the offsets' spread
+    if (prec) {
+        spread = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
+    }
+    const float kappa = 2.0f * spread * tmax;
+    const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
+    const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
+    if (far || illc) {
+        if (STORE_ROW) {  // the fused kernel keeps the rows in registers: hand them over
+#pragma unroll
+            for (int q = 0; q < KP; ++q)
+                if (q < k) {
+                    const_cast<int32_t*>(a.idx)[i * k + q] = jj[q];
+                    const_cast<float*>(a.sqd)[i * k + q] = sq[q];
+                }
+        }
+        faithful_point(a, i);
+        return;
+    }
+    const double det = A11 * A22 - A12 * A12;
+    const double tr = A11 + A22;
+    float2 out;
+    if (det < kDetRel * tr * tr + kDetAbs) {
+        out = o;
+    } else {
+        out.x = (float)((C1 * A22 - C2 * A12) / det + (double)o.x);
+        out.y = (float)((A11 * C2 - A12 * C1) / det + (double)o.y);
+    }
+    reinterpret_cast<float2*>(a.xy)[i] = out;
+}
+
 template <int KP, bool TSMEM, bool HSMEM, bool FARHEAVY>
 __global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs a) {
     constexpr int PT = kReg2Threads;
@@ -453,8 +594,8 @@ __global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs 
 
     for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
         const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
-        int jj[KP], rb[KP];
-        float sq[KP], sc[KP], lx[KP], ly[KP];
+        int jj[KP];
+        float sq[KP];
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
         if (vec) {
@@ -472,125 +613,7 @@ __global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs 
                 sq[q] = q < k ? __ldg(drow + q) : 0.0f;
             }
         }
-        float sqmax = 0.0f;
-#pragma unroll
-        for (int q = 0; q < KP; ++q) sqmax = fmaxf(sqmax, sq[q]);
-        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
-        count_prec(a.prec_count, prec);
-        // far from the landmarks: the k squared distances again in f64, kept as f32
-        // offsets from the nearest (precise_sqd); first, while little else is live
-        float qe[KP];
-        if (prec) {
-            if (a.d == 32)
-                precise_sqd_fixed<KP, 32, HSMEM, FARHEAVY>(a.X + i * 32, HSMEM ? h64 : a.hi64, HSMEM ? hs : 32,
-                                                 HSMEM ? hn_s : a.hn64, jj, k, qe);
-            else
-                precise_sqd<KP, HSMEM>(a.X + i * a.d, a.d, HSMEM ? h64 : a.hi64, HSMEM ? hs : a.d, jj, k, qe);
-        } else {
-#pragma unroll
-            for (int q = 0; q < KP; ++q) qe[q] = sq[q];
-        }
-        const float2 o = LO[jj[0]];
-        float sig = 0.0f, sqk = 0.0f;
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const float2 l = LO[jj[q]];
-            lx[q] = l.x - o.x;  // layout about the nearest landmark
-            ly[q] = l.y - o.y;
-            rb[q] = RB[jj[q]];
-            const float dq = q < k ? sqrt_approx(sq[q]) : 0.0f;
-            sig += dq;
-            if (q == k - 1) sqk = sq[q];
-        }
-        // scores (ref: projection.py:38-59) in f32, as the scale-free weights
-        // s_q / tail = expm1((d_k^2 - d_q^2) / 2 sigma^2): the normal equations
-        // are homogeneous in w, and the difference form keeps full relative
-        // precision where the reference's e_q - tail cancels (far outliers).
-        sig = sig / (float)k;
-        bool uniform = sig < (float)kScoreEps;
-        if (!uniform) {
-            const float inv = 1.0f / (2.0f * sig * sig);
-            const float tail = ex2_approx(-1.44269504f * sqk * inv);
-            float dls[KP];
-            if (prec) {  // far points: exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
-                const double dk = (double)__fsqrt_rn(sqk);
-#pragma unroll
-                for (int q = 0; q < KP; ++q) {
-                    const double dq = (double)__fsqrt_rn(sq[q]);
-                    dls[q] = q < k ? (float)((dk * dk - dq * dq) * (double)inv) : 0.0f;
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < KP; ++q) dls[q] = q < k ? (sqk - sq[q]) * inv : 0.0f;
-            }
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                const float dl = dls[q];  // >= 0 (rows ascending); 0 at q = k-1
-                const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
-                                                                       1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
-                const float e = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
-                sc[q] = e;
-                if (q == 0)  // the reference's s_0 = e_0 - tail < 1e-9 test (no underflow of tail * e)
-                    uniform = ex2_approx(-1.44269504f * sq[0] * inv) - tail < (float)kScoreEps;
-            }
-        }
-        if (uniform) {
-#pragma unroll
-            for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
-        }
-
-        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
-        // all pairs u < v, fully unrolled (static register indices, no ring rotation).
-        // Slot KP-1 never pairs: its score is exactly 0 (the reference's tail
-        // s_{k-1} = 0 when k == KP, the uniform fallback's trailing 0, or padding).
-#pragma unroll
-        for (int u = 0; u < KP - 2; ++u) {
-#pragma unroll
-            for (int v = u + 1; v < KP - 1; ++v) {
-                const float w = sc[u] * sc[v];
-                const int ti = max(jj[u] < jj[v] ? rb[u] + jj[v] : rb[v] + jj[u], 0);
-                const float tv = T[ti];
-                const float ex = __fsub_rn(lx[v], lx[u]), ey = __fsub_rn(ly[v], ly[u]);
-                const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-                const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
-                tmax = keep ? fmaxf(tmax, tv) : tmax;
-                const float rr = keep ? rcp_approx(ld2) : 0.0f;  // g = 0 for skipped pairs (ld2 may be 0)
-                const float wr = w * rr;
-                const float g1 = ex * rr, g2 = ey * rr;
-                // dnum/hd2 by the law of cosines + g . (lo_u - o)
-                const float h = fmaf(qe[u] - qe[v], tv, 0.5f) + fmaf(g1, lx[u], g2 * ly[u]);
-                const float wg1 = wr * ex, wg2 = wr * ey;  // w g
-                a11 = fmaf(wg1, g1, a11);
-                a12 = fmaf(wg1, g2, a12);
-                a22 = fmaf(wg2, g2, a22);
-                c1 = fmaf(wg1, h, c1);
-                c2 = fmaf(wg2, h, c2);
-            }
-        }
-        double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
-        float spread = sqmax;  // prec: the error of qe_u - qe_v scales with the offsets' spread
-        if (prec) {
-            spread = 0.0f;
-#pragma unroll
-            for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
-        }
-        const float kappa = 2.0f * spread * tmax;
-        const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
-        const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
-        if (far || illc) {
-            faithful_point(a, i);
-            continue;
-        }
-        const double det = A11 * A22 - A12 * A12;
-        const double tr = A11 + A22;
-        float2 out;
-        if (det < kDetRel * tr * tr + kDetAbs) {
-            out = o;
-        } else {
-            out.x = (float)((C1 * A22 - C2 * A12) / det + (double)o.x);
-            out.y = (float)((A11 * C2 - A12 * C1) / det + (double)o.y);
-        }
-        reinterpret_cast<float2*>(a.xy)[i] = out;
+        reg2_point<KP, TSMEM, HSMEM, FARHEAVY, false>(a, i, jj, sq, LO, RB, T, h64, hn_s, hs, tmax_model);
     }
 }
 
@@ -602,7 +625,7 @@ __global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs 
 // so a warp's lanes share records).  Per pair: one 16-byte load, the weight,
 // h = 1/2 + g.lo_u + (sqd_u - sqd_v) T, five FMAs.  Same fallbacks as v2.
 // ---------------------------------------------------------------------------
-__global__ void pair_record_kernel(const float* __restrict__ T, const float* __restrict__ lo, int g,
+static __global__ void pair_record_kernel(const float* __restrict__ T, const float* __restrict__ lo, int g,
                                    float4* __restrict__ rec) {
     const int64_t total = (int64_t)g * g;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {

@@ -154,6 +154,9 @@ int launch_scan_t(ScanArgs a, cudaStream_t st);   // esom_scan.cuh, instantiated
 
 template <int KP>
 int launch_project_t(ProjArgs a, cudaStream_t st);
+// exact k-NN + projection in one kernel (esom_fused.cuh; k = 16, d <= 32, small g);
+// ESOM_ERR_UNSUPPORTED when the shape does not qualify
+int launch_embed_fused_c(Tc2Args a, ProjArgs q, cudaStream_t st);
 // g x g pair records of project_reg3_kernel from the pair triangle T and the layout lo
 int launch_pair_records(const float* T, const float* lo, int g, float4* rec, cudaStream_t st);  // esom_project.cuh, instantiated in inst/*.cu
 

@@ -626,60 +626,27 @@ int launch_tc2_t(Tc2Args a, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 constexpr int kExactBitsThreads = 512;
 
+// One point of the exact phase: the reference-exact top k of the point's
+// candidates (bitmap in bsm, screen rows in Ls, row map rmap), in (distance,
+// landmark index) order.  rj / rd hold the k results in slots [KP - k, KP);
+// written = k unless the point needs the reference scan (non-finite input or
+// overflowing distances).  Shared by knn_exact_bits_kernel and the fused
+// embed kernel (esom_fused.cuh).
+struct ExactPoint {
+    int b0;
+    float d0;
+    int written;
+};
+
 template <int KP>
-__global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc2Args a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bar_load;
-    const int tid = threadIdx.x;
+__device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t i, int cnt, uint32_t nzw,
+                                                       const float* __restrict__ Ls, const uint32_t* bsm,
+                                                       const int32_t* rmap, int (&rj)[KP], float (&rd)[KP]) {
     const int d = a.d, d16 = a.d16, k = a.k, ls = a.ls;
     const int off = KP - k;
-    const int nwords = a.gpad >> 5;
-    float* Ls = reinterpret_cast<float*>(smem_raw);
-    const uint32_t r_bytes = (uint32_t)a.gpad * ls * 4u;
-    // per-thread copy of the point's candidate bitmap ([word][thread]): the extraction
-    // then waits on shared, not global, memory
-    uint32_t* bsm = reinterpret_cast<uint32_t*>(smem_raw + ((r_bytes + 127) / 128) * 128) + tid;
-    // screen row -> landmark index (after the bitmaps)
-    int32_t* rmap = reinterpret_cast<int32_t*>(bsm - tid + (size_t)nwords * kExactBitsThreads);
-    for (int j = tid; j < a.gpad; j += kExactBitsThreads) rmap[j] = a.rowmap ? __ldg(a.rowmap + j) : j;
-    if (tid == 0) {
-        mbar_init(&bar_load, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        mbar_expect_tx(&bar_load, r_bytes);
-        tma_bulk_g2s(Ls, a.Lrow, r_bytes, &bar_load);
-    }
-    mbar_wait(&bar_load, 0);
     const f2 nz2 = f2_pack(-0.0f, -0.0f);
     const int d4 = (d16 + 3) >> 2;
     const bool full = d4 == 8;
-    double qe_local = 0.0;
-    int slow_local = 0;
-    for (int64_t pos = blockIdx.x * (int64_t)kExactBitsThreads + tid; pos < a.n;
-         pos += (int64_t)gridDim.x * kExactBitsThreads) {
-        // points grouped by lowest candidate: a warp's lanes share landmark rows (smem broadcasts)
-        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
-        const int2 info = a.cinfo[i];
-        const int cnt = info.x;
-        uint32_t nzw = (uint32_t)info.y;
-        {
-            const uint32_t* bg = a.cbits + (size_t)i * nwords;
-            if ((nwords & 3) == 0) {
-                for (int w4 = 0; w4 < nwords; w4 += 4) {
-                    const uint4 u = __ldg(reinterpret_cast<const uint4*>(bg + w4));
-                    bsm[(w4 + 0) * kExactBitsThreads] = u.x;
-                    bsm[(w4 + 1) * kExactBitsThreads] = u.y;
-                    bsm[(w4 + 2) * kExactBitsThreads] = u.z;
-                    bsm[(w4 + 3) * kExactBitsThreads] = u.w;
-                }
-            } else {
-                for (int w1 = 0; w1 < nwords; ++w1) bsm[w1 * kExactBitsThreads] = __ldg(bg + w1);
-            }
-        }
-        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
-        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
         int b0 = 0;
         float d0 = 0.0f;
         int written = 0;
@@ -798,11 +765,10 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                 for (int q = 0; q < 15; ++q) amb |= L[q] == L[q + 1];
                 if (!amb) {  // distinct distances: value order is the (d, j) order
 #pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        if (oi) {
-                            oi[q] = rmap[LJ[q]];
-                            od[q] = L[q];
-                        }
+                    for (int q = 0; q < 16; ++q) {
+                        rj[q] = rmap[LJ[q]];
+                        rd[q] = L[q];
+                    }
                     b0 = rmap[LJ[0]];
                     d0 = L[0];
                     written = k;
@@ -832,12 +798,10 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                 }
 #pragma unroll
                 for (int q = 0; q < KP; ++q) {
+                    rj[q] = ti[q];
+                    rd[q] = td[q];
                     if (q >= off) {
                         written += ti[q] < a.g ? 1 : 0;
-                        if (oi) {
-                            oi[q - off] = ti[q];
-                            od[q - off] = td[q];
-                        }
                         if (q == off) {
                             b0 = ti[q];
                             d0 = td[q];
@@ -845,6 +809,74 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
                     }
                 }
             }
+        }
+    return ExactPoint{b0, d0, written};
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc2Args a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bar_load;
+    const int tid = threadIdx.x;
+    const int d = a.d, k = a.k, ls = a.ls;
+    const int off = KP - k;
+    const int nwords = a.gpad >> 5;
+    float* Ls = reinterpret_cast<float*>(smem_raw);
+    const uint32_t r_bytes = (uint32_t)a.gpad * ls * 4u;
+    // per-thread copy of the point's candidate bitmap ([word][thread]): the extraction
+    // then waits on shared, not global, memory
+    uint32_t* bsm = reinterpret_cast<uint32_t*>(smem_raw + ((r_bytes + 127) / 128) * 128) + tid;
+    // screen row -> landmark index (after the bitmaps)
+    int32_t* rmap = reinterpret_cast<int32_t*>(bsm - tid + (size_t)nwords * kExactBitsThreads);
+    for (int j = tid; j < a.gpad; j += kExactBitsThreads) rmap[j] = a.rowmap ? __ldg(a.rowmap + j) : j;
+    if (tid == 0) {
+        mbar_init(&bar_load, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&bar_load, r_bytes);
+        tma_bulk_g2s(Ls, a.Lrow, r_bytes, &bar_load);
+    }
+    mbar_wait(&bar_load, 0);
+    double qe_local = 0.0;
+    int slow_local = 0;
+    for (int64_t pos = blockIdx.x * (int64_t)kExactBitsThreads + tid; pos < a.n;
+         pos += (int64_t)gridDim.x * kExactBitsThreads) {
+        // points grouped by lowest candidate: a warp's lanes share landmark rows (smem broadcasts)
+        const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
+        const int2 info = a.cinfo[i];
+        const int cnt = info.x;
+        uint32_t nzw = (uint32_t)info.y;
+        {
+            const uint32_t* bg = a.cbits + (size_t)i * nwords;
+            if ((nwords & 3) == 0) {
+                for (int w4 = 0; w4 < nwords; w4 += 4) {
+                    const uint4 u = __ldg(reinterpret_cast<const uint4*>(bg + w4));
+                    bsm[(w4 + 0) * kExactBitsThreads] = u.x;
+                    bsm[(w4 + 1) * kExactBitsThreads] = u.y;
+                    bsm[(w4 + 2) * kExactBitsThreads] = u.z;
+                    bsm[(w4 + 3) * kExactBitsThreads] = u.w;
+                }
+            } else {
+                for (int w1 = 0; w1 < nwords; ++w1) bsm[w1 * kExactBitsThreads] = __ldg(bg + w1);
+            }
+        }
+        int rj[KP];
+        float rd[KP];
+        ExactPoint ep = exact_bits_point<KP>(a, i, cnt, nzw, Ls, bsm, rmap, rj, rd);
+        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+        int b0 = ep.b0;
+        float d0 = ep.d0;
+        const int written = ep.written;
+        if (written == k && oi) {
+#pragma unroll
+            for (int q = 0; q < KP; ++q)
+                if (q >= off) {
+                    oi[q - off] = rj[q];
+                    od[q - off] = rd[q];
+                }
         }
         if (written != k) {
             const SlowNearest sn = knn_point_slow(a.X + i * d, d, a.L, a.g, k, oi, od);

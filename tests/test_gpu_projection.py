@@ -306,3 +306,25 @@ def test_numpy_input_pinned_in_place_on_reuse():
     del x
     gc.collect()
     assert len(P._HOST_REG) == n0
+
+
+@pytest.mark.parametrize("rows,cols,n", [(16, 16, 300_000), (12, 12, 70_001)])
+def test_fused_exact_projection_equals_two_kernel_path(rows, cols, n):
+    """embed's fused exact-k-NN + projection kernel (esom_fused.cuh, k = 16, the
+    pair triangle in shared memory) gives the SAME bits as the two-kernel path
+    (forced here by the nearest-landmark visiting order, which never fuses)."""
+    from paper_2201_00701_b200.projection import PreparedModel
+
+    pts = datagen.gaussians(16, n, 32, seed=3)[0].astype(np.float32)
+    hi, lo = datagen.som_model(pts, rows, cols, seed=4)
+    X = torch.from_numpy(pts).cuda()
+    pm = PreparedModel(hi, lo, 16)
+    a = torch.empty((n, 2), dtype=torch.float32, device="cuda")
+    b = torch.empty_like(a)
+    pm.embed_into(X, a)
+    pm.embed_into(X, b, bmu_order=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    want = oracle.embed(pts[::997], hi, lo, 16)
+    ext = float(np.ptp(lo, axis=0).max())
+    assert float(np.abs(a[::997].cpu().numpy() - want).max()) <= 1e-4 * ext

@@ -35,7 +35,7 @@ for t in ((ticks,) if only else (0, ticks)):
     loop._eager_frame()
     torch.cuda.synchronize()
     out = {}
-    for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "project_kernel", "knn_gemm_kernel",
+    for name in ("knn_tc2_kernel", "knn_exact_bits_kernel", "embed_fused_kernel", "project_kernel", "knn_gemm_kernel",
                  "knn_exact_group_kernel"):
         c = ctypes.c_int32(0)
         ms = L.esom_timing_query(name.encode(), ctypes.byref(c))
