@@ -19,7 +19,7 @@
 
 namespace esom {
 
-constexpr int kFusedThreads = kExactBitsThreads;  // 512: one CTA per SM, 128 registers
+constexpr int kFusedThreads = kExactBitsThreads;  // 512: one CTA per SM, 128 registers (384 threads at 168 registers: slower)
 
 __host__ __device__ inline size_t fused_rows_bytes(int gpad, int ls) { return ((size_t)gpad * ls * 4 + 127) / 128 * 128; }
 __host__ __device__ inline size_t fused_proj_offset(int gpad, int ls) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
         }
         int rj[KP];
         float rd[KP];
-        const ExactPoint ep = exact_bits_point<KP>(a, i, cnt, (uint32_t)info.y, Ls, bsm, rmap, rj, rd);
+        const ExactPoint ep = exact_bits_point<KP, kFusedThreads>(a, i, cnt, (uint32_t)info.y, Ls, bsm, rmap, rj, rd);
         int32_t* wi = const_cast<int32_t*>(q.idx) + i * k;  // point workspace rows (chunk-relative)
         float* wd = const_cast<float*>(q.sqd) + i * k;
         int b0 = ep.b0;

@@ -638,7 +638,7 @@ struct ExactPoint {
     int written;
 };
 
-template <int KP>
+template <int KP, int BS = kExactBitsThreads>  // BS: thread stride of the bitmap words in bsm
 __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t i, int cnt, uint32_t nzw,
                                                        const float* __restrict__ Ls, const uint32_t* bsm,
                                                        const int32_t* rmap, int (&rj)[KP], float (&rd)[KP]) {
@@ -672,7 +672,7 @@ __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t
                     if (m == 0u) {
                         wi = __ffs(nz) - 1;
                         nz &= nz - 1u;
-                        m = bsm[(wi < 0 ? 0 : wi) * kExactBitsThreads];
+                        m = bsm[(wi < 0 ? 0 : wi) * BS];
                     }
                     jq[u] = max(32 * wi + (__ffs(m) - 1), 0);  // past the last candidate: any valid row
                     m &= m - 1u;
