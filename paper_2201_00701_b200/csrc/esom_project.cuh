@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(proj_threads<KP>()) project_fast_kernel(ProjAr
     }
 }
 
-constexpr int kRegThreads = 256;  // project_reg3_kernel (255 registers: one CTA per SM)
+constexpr int kRegThreads = 512;  // project_reg3_kernel: 16 warps/SM at <= 128 registers
 
 // ---------------------------------------------------------------------------
 // k <= 16 (default; the pair triangle in shared memory up to g ~ 330): the
