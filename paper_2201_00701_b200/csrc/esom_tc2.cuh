@@ -403,9 +403,12 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         // the mask of non-empty words (gpad <= 1024: one 32-bit word) ----
         int cnt = 0;
         uint32_t nzw = 0;
-        int first = -1;  // lowest candidate (split mode: locality sort key)
-        for (int r = 0; r < R; ++r) {
-            const int nr = (R > 1) ? run_round(r) : min(kTc2SlotCols, gpad);
+        int first = -1;  // a candidate (split mode: locality sort key)
+        // the last round of pass A is still in the slot: pass B starts with it (no
+        // MMA recompute), then redoes rounds 0 .. R-2
+        for (int rr = 0; rr < R; ++rr) {
+            const int r = rr == 0 ? R - 1 : rr - 1;
+            const int nr = rr > 0 ? run_round(r) : min(kTc2SlotCols, gpad - kTc2SlotCols * r);
             const int wb = (kTc2SlotCols * r) >> 5;
             for (int c0 = 0; c0 < nr; c0 += 32) {
                 uint32_t v0[32];
@@ -415,6 +418,8 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
                 const int wd = wb + (c0 >> 5);
                 if (SPLIT) {
                     if (valid) a.cbits[(size_t)i * nwords + wd] = m;
+                    // locality key: the first candidate met (lowest one of the first round
+                    // visited that has any) -- any candidate groups a cluster's points
                     if (first < 0 && m) first = 32 * wd + __ffs(m) - 1;
                 } else {
                     bmap[(size_t)wd * 128] = m;
