@@ -27,8 +27,9 @@ __host__ __device__ inline size_t fused_proj_offset(int gpad, int ls) {
     return (fused_rows_bytes(gpad, ls) + (size_t)(gpad / 32) * kFusedThreads * 4 + (size_t)gpad * 4 + 127) / 128 * 128;
 }
 inline size_t fused_smem_bytes(int gpad, int ls, int g) { return fused_proj_offset(gpad, ls) + reg2_hi64_offset(g); }
+inline size_t fused_list_bytes() { return (size_t)kExactListCap * kFusedThreads * 2; }
 
-template <int KP>
+template <int KP, bool LIST>
 __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a, ProjArgs q) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar_load;
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
     float2* LO = reinterpret_cast<float2*>(pj);
     int* RB = reinterpret_cast<int*>(LO + g);
     float* tsm = reinterpret_cast<float*>(pj + reg2_tri_offset(g));
+    uint16_t* lst = reinterpret_cast<uint16_t*>(pj + reg2_hi64_offset(g)) + tid;  // LIST: candidate indices
     for (int j = tid; j < a.gpad; j += kFusedThreads) rmap[j] = a.rowmap ? __ldg(a.rowmap + j) : j;
     const int ntri = g * (g - 1) / 2;
     for (int e = tid; e < ntri; e += kFusedThreads) tsm[e] = __ldg(q.T + e);
@@ -85,7 +87,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
         }
         int rj[KP];
         float rd[KP];
-        const ExactPoint ep = exact_bits_point<KP, kFusedThreads>(a, i, cnt, (uint32_t)info.y, Ls, bsm, rmap, rj, rd);
+        const ExactPoint ep =
+            exact_bits_point<KP, kFusedThreads, LIST>(a, i, cnt, (uint32_t)info.y, Ls, bsm, rmap, rj, rd, lst);
         int32_t* wi = const_cast<int32_t*>(q.idx) + i * k;  // point workspace rows (chunk-relative)
         float* wd = const_cast<float*>(q.sqd) + i * k;
         int b0 = ep.b0;
@@ -118,9 +121,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
 // ESOM_ERR_UNSUPPORTED when the shape does not qualify (the caller runs the two kernels)
 inline int launch_embed_fused(Tc2Args a, ProjArgs q, cudaStream_t st) {
     if (a.k != 16 || a.d16 > 32 || !a.cbits || q.k != 16) return ESOM_ERR_UNSUPPORTED;
-    const size_t smem = fused_smem_bytes(a.gpad, a.ls, a.g);
-    if (smem > (size_t)esom_host::max_smem_optin() - 1024) return ESOM_ERR_UNSUPPORTED;
-    auto kern = embed_fused_kernel<16>;
+    size_t smem = fused_smem_bytes(a.gpad, a.ls, a.g);
+    const size_t cap = (size_t)esom_host::max_smem_optin() - 1024;
+    if (smem > cap) return ESOM_ERR_UNSUPPORTED;
+    const bool list = smem + fused_list_bytes() <= cap;
+    if (list) smem += fused_list_bytes();
+    auto kern = list ? embed_fused_kernel<16, true> : embed_fused_kernel<16, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t grid = (a.n + kFusedThreads - 1) / kFusedThreads;
     if (grid > esom_host::num_sms()) grid = esom_host::num_sms();

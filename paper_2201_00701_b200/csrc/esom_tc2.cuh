@@ -643,10 +643,18 @@ struct ExactPoint {
     int written;
 };
 
-template <int KP, int BS = kExactBitsThreads>  // BS: thread stride of the bitmap words in bsm
+// LIST: the candidates are first unpacked into a per-thread index list in shared
+// memory (lst: [e][BS] u16, up to kExactListCap entries) while the point's x row is
+// in flight, so the distance loop reads its next landmark with one independent
+// load instead of the bitmap word -> ffs -> row-address chain (points with more
+// candidates walk the bitmap as before).
+constexpr int kExactListCap = 32;
+
+template <int KP, int BS = kExactBitsThreads, bool LIST = false>  // BS: thread stride of bsm / lst
 __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t i, int cnt, uint32_t nzw,
                                                        const float* __restrict__ Ls, const uint32_t* bsm,
-                                                       const int32_t* rmap, int (&rj)[KP], float (&rd)[KP]) {
+                                                       const int32_t* rmap, int (&rj)[KP], float (&rd)[KP],
+                                                       uint16_t* lst = nullptr) {
     const int d = a.d, d16 = a.d16, k = a.k, ls = a.ls;
     const int off = KP - k;
     const f2 nz2 = f2_pack(-0.0f, -0.0f);
@@ -670,17 +678,42 @@ __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t
                 for (int c = 0; c < 32; ++c) x[c] = c < d ? __ldg(xr + c) : 0.0f;
             }
             const uint32_t nzw0 = nzw;
+            const bool listed = LIST && cnt <= kExactListCap;
+            if (listed) {  // unpack the bitmap (index order) while x is loading
+                int e = 0;
+                uint32_t nz = nzw;
+                while (nz) {
+                    const int w = __ffs(nz) - 1;
+                    nz &= nz - 1u;
+                    uint32_t m = bsm[w * BS];
+                    while (m) {
+                        lst[e * BS] = (uint16_t)(32 * w + __ffs(m) - 1);
+                        ++e;
+                        m &= m - 1u;
+                    }
+                }
+            }
+            int cur_e = 0;  // list cursor
             // exact distances of the next 4 candidates of the bitmap (index order)
             auto next4 = [&](int& wi, uint32_t& m, uint32_t& nz, int* jq, float* s4) {
+                if (LIST && listed) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (m == 0u) {
-                        wi = __ffs(nz) - 1;
-                        nz &= nz - 1u;
-                        m = bsm[(wi < 0 ? 0 : wi) * BS];
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = cur_e + u;
+                        jq[u] = e < cnt ? (int)lst[e * BS] : 0;  // past the last candidate: any valid row
                     }
-                    jq[u] = max(32 * wi + (__ffs(m) - 1), 0);  // past the last candidate: any valid row
-                    m &= m - 1u;
+                    cur_e += 4;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (m == 0u) {
+                            wi = __ffs(nz) - 1;
+                            nz &= nz - 1u;
+                            m = bsm[(wi < 0 ? 0 : wi) * BS];
+                        }
+                        jq[u] = max(32 * wi + (__ffs(m) - 1), 0);  // past the last candidate: any valid row
+                        m &= m - 1u;
+                    }
                 }
                 const float4* lr[4];
 #pragma unroll
@@ -749,6 +782,7 @@ __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t
                 }
                 int wi = 0;
                 uint32_t m = 0, nz = nzw0;
+                cur_e = 0;
                 for (int e = 0; e < cnt; e += 8) {
                     float bv[8];
                     int bj[8];
@@ -790,6 +824,7 @@ __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t
                 }
                 int wi = 0;
                 uint32_t m = 0, nz = nzw0;
+                cur_e = 0;
                 for (int e = 0; e < cnt; e += 4) {
                     int jq[4];
                     float s4[4];
@@ -818,7 +853,7 @@ __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t
     return ExactPoint{b0, d0, written};
 }
 
-template <int KP>
+template <int KP, bool LIST>
 __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc2Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar_load;
@@ -833,6 +868,7 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
     uint32_t* bsm = reinterpret_cast<uint32_t*>(smem_raw + ((r_bytes + 127) / 128) * 128) + tid;
     // screen row -> landmark index (after the bitmaps)
     int32_t* rmap = reinterpret_cast<int32_t*>(bsm - tid + (size_t)nwords * kExactBitsThreads);
+    uint16_t* lst = reinterpret_cast<uint16_t*>(rmap + a.gpad) + tid;  // LIST: [e][thread] candidate indices
     for (int j = tid; j < a.gpad; j += kExactBitsThreads) rmap[j] = a.rowmap ? __ldg(a.rowmap + j) : j;
     if (tid == 0) {
         mbar_init(&bar_load, 1);
@@ -869,7 +905,7 @@ __global__ void __launch_bounds__(kExactBitsThreads, 1) knn_exact_bits_kernel(Tc
         }
         int rj[KP];
         float rd[KP];
-        ExactPoint ep = exact_bits_point<KP>(a, i, cnt, nzw, Ls, bsm, rmap, rj, rd);
+        ExactPoint ep = exact_bits_point<KP, kExactBitsThreads, LIST>(a, i, cnt, nzw, Ls, bsm, rmap, rj, rd, lst);
         int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
         float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
         int b0 = ep.b0;
@@ -910,12 +946,15 @@ int launch_exact_bits_t(Tc2Args a, cudaStream_t st) {
                         (size_t)a.gpad * 4;  // + the row map
     if (smem > (size_t)esom_host::max_smem_optin())
         return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "exact rows exceed shared memory%s", "");
-    auto kern = knn_exact_bits_kernel<KP>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem_list = smem + (size_t)kExactListCap * kExactBitsThreads * 2;
+    const bool list = smem_list <= (size_t)esom_host::max_smem_optin();
+    auto kern = list ? knn_exact_bits_kernel<KP, true> : knn_exact_bits_kernel<KP, false>;
+    const size_t sm = list ? smem_list : smem;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int64_t grid = (a.n + kExactBitsThreads - 1) / kExactBitsThreads;
     if (grid > esom_host::num_sms()) grid = esom_host::num_sms();
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kExactBitsThreads, smem, st>>>(a);
+    kern<<<(unsigned)grid, kExactBitsThreads, sm, st>>>(a);
     return esom_host::cuda_check("knn_exact_bits_kernel");
 }
 
