@@ -500,7 +500,7 @@ __device__ __forceinline__ void reg2_point(const ProjArgs& a, int64_t i, const i
         for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
     }
 
-    float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
+    float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f;
     // all pairs u < v, fully unrolled (static register indices, no ring rotation).
     // Slot KP-1 never pairs: its score is exactly 0 (the reference's tail
     // s_{k-1} = 0 when k == KP, the uniform fallback's trailing 0, or padding).
@@ -513,9 +513,9 @@ __device__ __forceinline__ void reg2_point(const ProjArgs& a, int64_t i, const i
             const float tv = T[ti];
             const float ex = __fsub_rn(lx[v], lx[u]), ey = __fsub_rn(ly[v], ly[u]);
             const float ld2 = __fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey));
-            const bool keep = (w > 0.0f) & (tv >= 0.0f) & (ld2 >= kLd2Min);
-            tmax = keep ? fmaxf(tmax, tv) : tmax;
-            const float rr = keep ? rcp_approx(ld2) : 0.0f;  // g = 0 for skipped pairs (ld2 may be 0)
+            // skipped pairs (the reference's hd2 / ld2 tests) get g = 0; w = 0 pairs add 0 anyway
+            const bool keep = (tv >= 0.0f) & (ld2 >= kLd2Min);
+            const float rr = keep ? rcp_approx(ld2) : 0.0f;  // (ld2 may be 0)
             const float wr = w * rr;
             const float g1 = ex * rr, g2 = ey * rr;
             // dnum/hd2 by the law of cosines + g . (lo_u - o)
@@ -535,7 +535,10 @@ __device__ __forceinline__ void reg2_point(const ProjArgs& a, int64_t i, const i
 #pragma unroll
         for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
     }
-    const float kappa = 2.0f * spread * tmax;
+    // the model-wide max T bounds every kept pair's T: for a point that passed the
+    // prec test (2 sqmax T_max <= kKappaMax) this never trips; far points compare
+    // against the f64 path's bound
+    const float kappa = 2.0f * spread * tmax_model;
     const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
     const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
     if (far || illc) {
@@ -725,19 +728,17 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
 #pragma unroll
             for (int q = 0; q < KP; ++q) qe[q] = sq[q];
         }
-        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f, tmax = 0.0f;
-        // all pairs u < v fully unrolled; slot KP-1 has score 0 (see project_reg2_kernel)
+        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+        // all pairs u < v fully unrolled; slot KP-1 has score 0 (see project_reg2_kernel);
+        // skipped pairs' records are (-1, 0, 0, 0): g = 0, so they add nothing
 #pragma unroll
         for (int u = 0; u < KP - 2; ++u) {
 #pragma unroll
             for (int v = u + 1; v < KP - 1; ++v) {
                 const float w = sc[u] * sc[v];
                 const float4 rc = __ldg(rec + rowb[u] + jj[v]);
-                const bool keep = (w > 0.0f) & (rc.x >= 0.0f);
-                tmax = keep ? fmaxf(tmax, rc.x) : tmax;
-                const float wk = keep ? w : 0.0f;
                 const float h = fmaf(qe[u] - qe[v], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
-                const float wg1 = wk * rc.y, wg2 = wk * rc.z;
+                const float wg1 = w * rc.y, wg2 = w * rc.z;
                 a11 = fmaf(wg1, rc.y, a11);
                 a12 = fmaf(wg1, rc.z, a12);
                 a22 = fmaf(wg2, rc.z, a22);
@@ -752,7 +753,7 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
 #pragma unroll
             for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
         }
-        const float kappa = 2.0f * spread * tmax;
+        const float kappa = 2.0f * spread * tmax_model;  // (see reg2_point)
         const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
         const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
         if (far || illc) {
