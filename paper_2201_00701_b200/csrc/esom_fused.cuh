@@ -23,8 +23,8 @@ constexpr int kFusedThreads = kExactBitsThreads;  // 512: one CTA per SM, 128 re
 
 __host__ __device__ inline size_t fused_rows_bytes(int gpad, int ls) { return ((size_t)gpad * ls * 4 + 127) / 128 * 128; }
 __host__ __device__ inline size_t fused_proj_offset(int gpad, int ls) {
-    // rows | bitmaps [word][thread] | row map | (16-B aligned) projection tables (reg2 layout)
-    return (fused_rows_bytes(gpad, ls) + (size_t)(gpad / 32) * kFusedThreads * 4 + (size_t)gpad * 4 + 127) / 128 * 128;
+    // rows | bitmaps [word][thread] | row map | inverse row map | (aligned) projection tables (reg2 layout)
+    return (fused_rows_bytes(gpad, ls) + (size_t)(gpad / 32) * kFusedThreads * 4 + (size_t)gpad * 8 + 127) / 128 * 128;
 }
 inline size_t fused_smem_bytes(int gpad, int ls, int g) { return fused_proj_offset(gpad, ls) + reg2_hi64_offset(g); }
 inline size_t fused_list_bytes() { return (size_t)kExactListCap * kFusedThreads * 2; }
@@ -40,12 +40,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
     const uint32_t r_bytes = (uint32_t)a.gpad * a.ls * 4u;
     uint32_t* bsm = reinterpret_cast<uint32_t*>(smem_raw + fused_rows_bytes(a.gpad, a.ls)) + tid;
     int32_t* rmap = reinterpret_cast<int32_t*>(bsm - tid + (size_t)nwords * kFusedThreads);
+    int32_t* inv = rmap + a.gpad;  // landmark -> screen row (the far-point distances read the rows)
     unsigned char* pj = smem_raw + fused_proj_offset(a.gpad, a.ls);
     float2* LO = reinterpret_cast<float2*>(pj);
     int* RB = reinterpret_cast<int*>(LO + g);
     float* tsm = reinterpret_cast<float*>(pj + reg2_tri_offset(g));
     uint16_t* lst = reinterpret_cast<uint16_t*>(pj + reg2_hi64_offset(g)) + tid;  // LIST: candidate indices
-    for (int j = tid; j < a.gpad; j += kFusedThreads) rmap[j] = a.rowmap ? __ldg(a.rowmap + j) : j;
+    for (int j = tid; j < a.gpad; j += kFusedThreads) {
+        const int r = a.rowmap ? __ldg(a.rowmap + j) : j;
+        rmap[j] = r;
+        if (r < a.gpad) inv[r] = j;
+    }
     const int ntri = g * (g - 1) / 2;
     for (int e = tid; e < ntri; e += kFusedThreads) tsm[e] = __ldg(q.T + e);
     for (int j = tid; j < g; j += kFusedThreads) {
@@ -108,7 +113,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
         wi[0] = b0;  // the nearest landmark: batch-SOM statistics read column 0
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
-        reg2_point<KP, true, false, false, true>(q, i, rj, rd, LO, RB, tsm, nullptr, nullptr, 0, tmax_model);
+        reg2_point<KP, true, false, false, true, true>(q, i, rj, rd, LO, RB, tsm, nullptr, nullptr, 0, tmax_model, Ls,
+                                                       a.ls, inv);
     }
     if (a.stats && slow_local) atomicAdd(a.stats + 1, slow_local);
     if (a.qe_sum) {
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
 
 // ESOM_ERR_UNSUPPORTED when the shape does not qualify (the caller runs the two kernels)
 inline int launch_embed_fused(Tc2Args a, ProjArgs q, cudaStream_t st) {
-    if (a.k != 16 || a.d16 > 32 || !a.cbits || q.k != 16) return ESOM_ERR_UNSUPPORTED;
+    if (a.k != 16 || a.d != 32 || !a.cbits || q.k != 16) return ESOM_ERR_UNSUPPORTED;
     size_t smem = fused_smem_bytes(a.gpad, a.ls, a.g);
     const size_t cap = (size_t)esom_host::max_smem_optin() - 1024;
     if (smem > cap) return ESOM_ERR_UNSUPPORTED;

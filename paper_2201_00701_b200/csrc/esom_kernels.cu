@@ -1541,7 +1541,6 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         a.qe_sum = qe_sum;  // batch-SOM sums come from the BMU-sorted order below (no atomics)
         const size_t tbytes = (size_t)g * (g - 1) / 2 * 4;
         const bool l2_table = tbytes + (size_t)g * 12 + 1024 > (size_t)max_smem_optin() && m >= 4096 && g <= 8192;
-        const bool need_perm = l2_table || ((use_rec || bmu_order) && m >= 4096);
         ProjArgs q{};
         q.idx = idx;
         q.sqd = sqd;
@@ -1560,11 +1559,13 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         q.hn64 = reinterpret_cast<const double*>(mws + ml.hn64);
         q.d = d;
         q.rec = use_rec ? rec : nullptr;
-        // the exact phase and the projection in one kernel when the projection would
-        // run in natural order from the shared-memory pair triangle (not far-heavy)
-        const bool try_fuse = p.kp == 16 && k == 16 && !need_perm && !use_rec && !bmu_order;
+        // the exact phase and the projection in one kernel when the pair triangle sits in
+        // shared memory (the fused kernel visits the exact phase's locality order and
+        // reads far points' landmark rows from the exact phase's shared copy)
+        const bool try_fuse = p.kp == 16 && k == 16 && !l2_table && !use_rec;
         bool fused = false;
         if (int e = run_knn(p, ml, a, mws, stream, try_fuse ? &q : nullptr, &fused)) return e;
+        const bool need_perm = !fused && (l2_table || ((use_rec || bmu_order) && m >= 4096));
         const bool acc_smem = (acc_S || acc_C) && !need_perm && accum_smem_ok(g, d);
         if (acc_smem) {
             const size_t smem = ((size_t)g * d + g) * 8;

@@ -242,6 +242,50 @@ __device__ __forceinline__ void precise_sqd_fixed(const float* __restrict__ xg, 
     }
 }
 
+// precise_sqd from the exact phase's f32 landmark rows in shared memory (the
+// fused kernel; rows in screen order, located through inv = landmark -> row):
+// the same dot-product form in f64, each row element widened on the fly.
+template <int KP>
+__device__ __forceinline__ void precise_sqd_rows32(const float* __restrict__ xg, const float* Ls, int ls,
+                                                   const int32_t* inv, const double* __restrict__ hn,
+                                                   const int (&jj)[KP], int k, float (&qe)[KP]) {
+    constexpr int QC = KP < 4 ? KP : 4;
+    double s0 = 0.0;
+#pragma unroll
+    for (int q0 = 0; q0 < KP; q0 += QC) {
+        double acc[QC];
+        const float* rw[QC];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+            acc[q] = 0.0;
+            rw[q] = Ls + (size_t)inv[q0 + q < k ? jj[q0 + q] : 0] * ls;
+        }
+        float4 xn = __ldg(reinterpret_cast<const float4*>(xg));
+#pragma unroll 2
+        for (int c = 0; c < 32; c += 4) {
+            const float4 xc = xn;
+            if (c + 4 < 32) xn = __ldg(reinterpret_cast<const float4*>(xg + c + 4));
+            const double x0 = (double)xc.x, x1 = (double)xc.y, x2 = (double)xc.z, x3 = (double)xc.w;
+#pragma unroll
+            for (int q = 0; q < QC; ++q) {
+                const float4 h = *reinterpret_cast<const float4*>(rw[q] + c);
+                acc[q] = fma(x0, (double)h.x, acc[q]);
+                acc[q] = fma(x1, (double)h.y, acc[q]);
+                acc[q] = fma(x2, (double)h.z, acc[q]);
+                acc[q] = fma(x3, (double)h.w, acc[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+            const double hq = q0 + q < k ? __ldg(hn + jj[q0 + q]) : 0.0;
+            acc[q] = fma(-2.0, acc[q], hq);  // s_j - |x|^2
+        }
+        if (q0 == 0) s0 = acc[0];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) qe[q0 + q] = q0 + q < k ? (float)(acc[q] - s0) : 0.0f;
+    }
+}
+
 // Ill-conditioned systems (tr^2 > kCondMax det: the solution amplifies every
 // rounding) and far outliers: the reference's own scores and projection op
 // for op (esom_faithful.cuh) -- bit-faithful given the scores, so even the
@@ -426,10 +470,12 @@ __host__ __device__ inline int reg2_hi64_stride(int d) {
 // padding with zero weight).  Shared with the fused embed kernel
 // (esom_fused.cuh; STORE_ROW: the rows are in registers only, so the rare
 // faithful fallback first writes them to the point workspace).
-template <int KP, bool TSMEM, bool HSMEM, bool FARHEAVY, bool STORE_ROW>
+template <int KP, bool TSMEM, bool HSMEM, bool FARHEAVY, bool STORE_ROW, bool ROWS32 = false>
 __device__ __forceinline__ void reg2_point(const ProjArgs& a, int64_t i, const int (&jj)[KP], const float (&sq)[KP],
                                            const float2* LO, const int* RB, const float* T, const double* h64,
-                                           const double* hn_s, int hs, float tmax_model) {
+                                           const double* hn_s, int hs, float tmax_model,
+                                           const float* rows32 = nullptr, int ls32 = 0,
+                                           const int32_t* inv32 = nullptr) {
     const int k = a.k;
     int rb[KP];
     float sc[KP], lx[KP], ly[KP];
@@ -442,7 +488,9 @@ __device__ __forceinline__ void reg2_point(const ProjArgs& a, int64_t i, const i
     // offsets from the nearest (precise_sqd); first, while little else is live
     float qe[KP];
     if (prec) {
-        if (a.d == 32)
+        if (ROWS32)  // (d == 32, the fused kernel)
+            precise_sqd_rows32<KP>(a.X + i * 32, rows32, ls32, inv32, a.hn64, jj, k, qe);
+        else if (a.d == 32)
             precise_sqd_fixed<KP, 32, HSMEM, FARHEAVY>(a.X + i * 32, HSMEM ? h64 : a.hi64, HSMEM ? hs : 32,
                                              HSMEM ? hn_s : a.hn64, jj, k, qe);
         else
