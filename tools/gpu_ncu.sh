@@ -10,11 +10,11 @@ cap() {  # name, kernel regex, skip, command...
   python tools/ncu_lines.py /tmp/ncu_$name.ncu-rep 30 > gpurun_out/ncu/${name}_lines.txt 2>&1
   rm -f /tmp/ncu_$name.ncu-rep
 }
-cap exact_c2 knn_exact_bits 1 python tools/probe_trained.py 0 c2
+cap fused_c2 embed_fused 1 python tools/probe_trained.py 0 c2
 cap screen_c2 knn_tc2 1 python tools/probe_trained.py 0 c2
-cap proj_c2 project_reg2 1 python tools/probe_trained.py 0 c2
-cap proj_c2_trained project_reg2 3 python tools/probe_trained.py 40 c2 only
-cap exact_c2_trained knn_exact_bits 3 python tools/probe_trained.py 40 c2 only
+cap fused_c2_trained embed_fused 3 python tools/probe_trained.py 40 c2 only
+cap exact_c4 knn_exact_bits 1 python tools/probe_trained.py 0 c4
+cap proj_c4 project_reg3 1 python tools/probe_trained.py 0 c4
 cap screen_c4 knn_tc2 1 python tools/probe_trained.py 0 c4
 cap gemm_c5 knn_gemm 0 python tools/probe_c5.py
 cap group_c5 knn_exact_group 0 python tools/probe_c5.py
@@ -28,3 +28,4 @@ for w in c2 c3; do
 done
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29732 \
   bench.py --impl reference --gpus 2 --steps 2 --warmup 1 > gpurun_out/ncu/dry2_ref.json 2> gpurun_out/ncu/dry2_ref.err; echo dry2_ref=$?
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ncu/smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/ncu/smoke.log
