@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
                 rd[t] = wd[t];
             }
         }
-        wi[0] = b0;  // the nearest landmark: batch-SOM statistics read column 0
+        if (q.store_bmu) wi[0] = b0;  // the nearest landmark: batch-SOM statistics read column 0
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
         reg2_point<KP, true, false, false, true, true>(q, i, rj, rd, LO, RB, tsm, nullptr, nullptr, 0, tmax_model, Ls,

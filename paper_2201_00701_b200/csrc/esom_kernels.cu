@@ -1552,6 +1552,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
         q.tmax = reinterpret_cast<const float*>(mws + ml.lstats) + 2;
         q.prec_count = far_count;
         q.far_heavy = bmu_order ? 1 : 0;
+        q.store_bmu = (acc_S || acc_C) ? 1 : 0;
         q.xy = xy + 2 * s;
         q.X = X + s * d;
         q.hi = hi;

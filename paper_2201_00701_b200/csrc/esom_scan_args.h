@@ -43,6 +43,7 @@ struct ProjArgs {
     const float* tmax;       // device scalar: max kept T of the model (f64-distance decision)
     int32_t* prec_count;     // += points that took the f64 far-point path (nullable)
     int far_heavy;           // the caller expects most points far (nearest-landmark order): far-path codegen
+    int store_bmu;           // fused kernel: write the nearest landmark to idx[i * k] (batch-SOM statistics)
 };
 
 // tensor-core screened k-NN (esom_tc.cuh)
