@@ -697,6 +697,121 @@ static __global__ void pair_record_kernel(const float* __restrict__ T, const flo
     }
 }
 
+// One point of project_reg3_kernel (pair records {T, g, g.lo_u} in L2); shared
+// with the record-table variant of the fused kernel (esom_fused.cuh; STORE_ROW
+// and ROWS32 as in reg2_point).
+template <int KP, bool STORE_ROW, bool ROWS32 = false>
+__device__ __forceinline__ void reg3_point(const ProjArgs& a, int64_t i, const int (&jj)[KP], const float (&sq)[KP],
+                                           const float4* __restrict__ rec, float tmax_model,
+                                           const float* rows32 = nullptr, int ls32 = 0,
+                                           const int32_t* inv32 = nullptr) {
+    const int g = a.g, k = a.k;
+    int rowb[KP];
+    float sc[KP];
+    float sig = 0.0f, sqk = 0.0f, sqmax = 0.0f;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+        rowb[q] = jj[q] * g;
+        sig += q < k ? sqrt_approx(sq[q]) : 0.0f;
+        if (q == k - 1) sqk = sq[q];
+        sqmax = fmaxf(sqmax, sq[q]);
+    }
+    // scores as in v2 (scale-free f32 expm1 form)
+    sig = sig / (float)k;
+    bool uniform = sig < (float)kScoreEps;
+    const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
+    count_prec(a.prec_count, prec);
+    if (!uniform) {
+        const float inv = 1.0f / (2.0f * sig * sig);
+        const float tail = ex2_approx(-1.44269504f * sqk * inv);
+        float dls[KP];
+        if (prec) {  // far points: exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
+            const double dk = (double)__fsqrt_rn(sqk);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                const double dq = (double)__fsqrt_rn(sq[q]);
+                dls[q] = q < k ? (float)((dk * dk - dq * dq) * (double)inv) : 0.0f;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) dls[q] = q < k ? (sqk - sq[q]) * inv : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const float dl = dls[q];
+            const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
+                                                                   1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+            sc[q] = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
+            if (q == 0) uniform = ex2_approx(-1.44269504f * sq[0] * inv) - tail < (float)kScoreEps;
+        }
+    }
+    if (uniform) {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
+    }
+
+    float qe[KP];
+    if (prec) {
+        if (ROWS32)  // (d == 32, the fused kernel)
+            precise_sqd_rows32<KP>(a.X + i * 32, rows32, ls32, inv32, a.hn64, jj, k, qe);
+        else
+            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, a.d, jj, k, qe);
+    } else {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) qe[q] = sq[q];
+    }
+    float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+    // all pairs u < v fully unrolled; slot KP-1 has score 0 (see project_reg2_kernel);
+    // skipped pairs' records are (-1, 0, 0, 0): g = 0, so they add nothing
+#pragma unroll
+    for (int u = 0; u < KP - 2; ++u) {
+#pragma unroll
+        for (int v = u + 1; v < KP - 1; ++v) {
+            const float w = sc[u] * sc[v];
+            const float4 rc = __ldg(rec + rowb[u] + jj[v]);
+            const float h = fmaf(qe[u] - qe[v], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
+            const float wg1 = w * rc.y, wg2 = w * rc.z;
+            a11 = fmaf(wg1, rc.y, a11);
+            a12 = fmaf(wg1, rc.z, a12);
+            a22 = fmaf(wg2, rc.z, a22);
+            c1 = fmaf(wg1, h, c1);
+            c2 = fmaf(wg2, h, c2);
+        }
+    }
+    double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
+    float spread = sqmax;  // prec: the error of qe_u - qe_v scales with the offsets' spread
+    if (prec) {
+        spread = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
+    }
+    const float kappa = 2.0f * spread * tmax_model;  // (see reg2_point)
+    const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
+    const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
+    if (far || illc) {
+        if (STORE_ROW) {  // the fused kernel keeps the rows in registers: hand them over
+#pragma unroll
+            for (int q = 0; q < KP; ++q)
+                if (q < k) {
+                    const_cast<int32_t*>(a.idx)[i * k + q] = jj[q];
+                    const_cast<float*>(a.sqd)[i * k + q] = sq[q];
+                }
+        }
+        faithful_point(a, i);
+        return;
+    }
+    const double det = A11 * A22 - A12 * A12;
+    const double tr = A11 + A22;
+    float2 out;
+    if (det < kDetRel * tr * tr + kDetAbs) {
+        out = make_float2(__ldg(a.lo + 2 * jj[0]), __ldg(a.lo + 2 * jj[0] + 1));
+    } else {
+        out.x = (float)((C1 * A22 - C2 * A12) / det);
+        out.y = (float)((A11 * C2 - A12 * C1) / det);
+    }
+    reinterpret_cast<float2*>(a.xy)[i] = out;
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a) {
     constexpr int PT = kRegThreads;
@@ -708,8 +823,8 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
 
     for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
         const int64_t i = a.perm ? (int64_t)__ldg(a.perm + pos) : pos;
-        int jj[KP], rowb[KP];
-        float sq[KP], sc[KP];
+        int jj[KP];
+        float sq[KP];
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
         if (vec) {
@@ -727,97 +842,7 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
                 sq[q] = q < k ? __ldg(drow + q) : 0.0f;
             }
         }
-        float sig = 0.0f, sqk = 0.0f, sqmax = 0.0f;
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            rowb[q] = jj[q] * g;
-            sig += q < k ? sqrt_approx(sq[q]) : 0.0f;
-            if (q == k - 1) sqk = sq[q];
-            sqmax = fmaxf(sqmax, sq[q]);
-        }
-        // scores as in v2 (scale-free f32 expm1 form)
-        sig = sig / (float)k;
-        bool uniform = sig < (float)kScoreEps;
-        const bool prec = 2.0f * sqmax * tmax_model > (float)kKappaMax;  // far: f64 distance paths
-        count_prec(a.prec_count, prec);
-        if (!uniform) {
-            const float inv = 1.0f / (2.0f * sig * sig);
-            const float tail = ex2_approx(-1.44269504f * sqk * inv);
-            float dls[KP];
-            if (prec) {  // far points: exponent differences from the reference's own d_t^2 = (f64 sqrtf(sq))^2
-                const double dk = (double)__fsqrt_rn(sqk);
-#pragma unroll
-                for (int q = 0; q < KP; ++q) {
-                    const double dq = (double)__fsqrt_rn(sq[q]);
-                    dls[q] = q < k ? (float)((dk * dk - dq * dq) * (double)inv) : 0.0f;
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < KP; ++q) dls[q] = q < k ? (sqk - sq[q]) * inv : 0.0f;
-            }
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                const float dl = dls[q];
-                const float poly = dl * fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, fmaf(dl, 1.0f / 720.0f, 1.0f / 120.0f),
-                                                                       1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
-                sc[q] = dl < 0.3f ? poly : ex2_approx(1.44269504f * dl) - 1.0f;
-                if (q == 0) uniform = ex2_approx(-1.44269504f * sq[0] * inv) - tail < (float)kScoreEps;
-            }
-        }
-        if (uniform) {
-#pragma unroll
-            for (int q = 0; q < KP; ++q) sc[q] = q < k - 1 ? 1.0f : 0.0f;
-        }
-
-        float qe[KP];
-        if (prec) {
-            precise_sqd<KP>(a.X + i * a.d, a.d, a.hi64, a.d, jj, k, qe);
-        } else {
-#pragma unroll
-            for (int q = 0; q < KP; ++q) qe[q] = sq[q];
-        }
-        float a11 = 0.0f, a12 = 0.0f, a22 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-        // all pairs u < v fully unrolled; slot KP-1 has score 0 (see project_reg2_kernel);
-        // skipped pairs' records are (-1, 0, 0, 0): g = 0, so they add nothing
-#pragma unroll
-        for (int u = 0; u < KP - 2; ++u) {
-#pragma unroll
-            for (int v = u + 1; v < KP - 1; ++v) {
-                const float w = sc[u] * sc[v];
-                const float4 rc = __ldg(rec + rowb[u] + jj[v]);
-                const float h = fmaf(qe[u] - qe[v], rc.x, 0.5f + rc.w);  // dnum/hd2 + g . lo_u
-                const float wg1 = w * rc.y, wg2 = w * rc.z;
-                a11 = fmaf(wg1, rc.y, a11);
-                a12 = fmaf(wg1, rc.z, a12);
-                a22 = fmaf(wg2, rc.z, a22);
-                c1 = fmaf(wg1, h, c1);
-                c2 = fmaf(wg2, h, c2);
-            }
-        }
-        double A11 = a11, A12 = a12, A22 = a22, C1 = c1, C2 = c2;
-        float spread = sqmax;  // prec: the error of qe_u - qe_v scales with the offsets' spread
-        if (prec) {
-            spread = 0.0f;
-#pragma unroll
-            for (int q = 0; q < KP; ++q) spread = fmaxf(spread, fabsf(qe[q]));
-        }
-        const float kappa = 2.0f * spread * tmax_model;  // (see reg2_point)
-        const bool illc = a11 * a22 - a12 * a12 < (a11 + a22) * (a11 + a22) * (1.0f / kCondMax);
-        const bool far = kappa > (float)(prec ? kKappaMax64 : kKappaMax);
-        if (far || illc) {
-            faithful_point(a, i);
-            continue;
-        }
-        const double det = A11 * A22 - A12 * A12;
-        const double tr = A11 + A22;
-        float2 out;
-        if (det < kDetRel * tr * tr + kDetAbs) {
-            out = make_float2(__ldg(a.lo + 2 * jj[0]), __ldg(a.lo + 2 * jj[0] + 1));
-        } else {
-            out.x = (float)((C1 * A22 - C2 * A12) / det);
-            out.y = (float)((A11 * C2 - A12 * C1) / det);
-        }
-        reinterpret_cast<float2*>(a.xy)[i] = out;
+        reg3_point<KP, false>(a, i, jj, sq, rec, tmax_model);
     }
 }
 
