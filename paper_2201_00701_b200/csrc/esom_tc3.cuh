@@ -521,12 +521,20 @@ __global__ void __launch_bounds__(kT3ExactWarps * 32) knn_exact_warp_kernel(T3Ex
 }
 
 // ---------------------------------------------------------------------------
-// Grouped exact re-evaluation (d % 8 == 0): a warp takes 8 consecutive points
+// Grouped exact re-evaluation (d % 8 == 0): a warp takes 4 consecutive points
 // of the approximate-BMU order, forms the union U of their candidate lists
 // (<= kT3UMax landmarks; points of one Voronoi cell share most candidates) and
-// lane e evaluates landmark U_e against all 8 points (each candidate row is
-// read once per group, 8 sequential f32 chains per landmark).  U contains
+// lane e evaluates landmark U_e against all 4 points (each candidate row is
+// read once per group, 4 sequential f32 chains per landmark).  U contains
 // every point's true top k, so the top k of U by (distance, index) is exact.
+//
+// The lanes' row reads are the bound (every lane a different row: one L1
+// wavefront per lane per load), so each lane fetches its 32-byte row sector
+// with ONE 256-bit load (ld.global.nc.v8.f32 -> LDG.E.ENL2.256) instead of two
+// 128-bit loads: 14.6 -> 11.5 ms per 2^20 points at C5.  (A CTA-shared
+// cp.async ring of the tile's union rows in shared memory removed the L1
+// bound but was slower, 15.7 ms: per-tile barriers at 8-16 warps per SM and
+// 3.8-way bank conflicts on the lane-divergent rows.)
 // ---------------------------------------------------------------------------
 constexpr int kT3GP = 4;       // points per warp group
 constexpr int kT3UMax = 96;    // union capacity (three landmark slots per lane)
@@ -543,225 +551,285 @@ __device__ __forceinline__ float acc8f(float s, const float4& la, const float4& 
     return __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, q4), q5), q6), q7);
 }
 
-__host__ __device__ constexpr int t3_group_stride(int dpad, int g) {  // floats per warp, 16-B aligned
-    return (kT3GP * dpad + (g + 31) / 32 + kT3UMax + 3) / 4 * 4;
+// 32 bytes per lane in one load (LDG.E.ENL2.256: half the L1 wavefronts of two
+// 16-byte loads when every lane reads a different row); p 32-byte aligned.
+__device__ __forceinline__ void ldg_nc_v8(const float* p, float4& lo, float4& hi) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+                 : "l"(p));
 }
 
-template <int KP>
+__host__ __device__ constexpr int t3_group_stride(int dpad, int g) {  // floats per warp, 16-B aligned
+    return (kT3GP * dpad + 2 * ((g + 31) / 32) + kT3UMax + 3) / 4 * 4;  // x rows | bitmap | word prefix | list
+}
+
+// Set bits of bm[0, gw) -> ascending landmark list out[0, min(U, cap)); returns U.
+// pre (nullable): exclusive prefix popcount per word (the list position of the word's first bit).
+__device__ __forceinline__ int t3_bits_to_list(const uint32_t* bm, int gw, int* out, int cap, int* pre, int lane) {
+    int U = 0;
+    for (int w0 = 0; w0 < gw; w0 += 32) {
+        const uint32_t m = w0 + lane < gw ? bm[w0 + lane] : 0u;
+        const int c = __popc(m);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        int pos = U + incl - c;
+        if (pre && w0 + lane < gw) pre[w0 + lane] = pos;
+        uint32_t mm = m;
+        while (mm) {
+            const int b = __ffs(mm) - 1;
+            mm &= mm - 1u;
+            if (pos < cap) out[pos] = ((w0 + lane) << 5) + b;
+            ++pos;
+        }
+        U += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return U;
+}
+
+// Per point of subset sm: rank its OWN candidates (its list contains its true top
+// k, so the top k of the list is exact; ref: knn.py:84-90) by (distance, index)
+// and write the k-NN row and the statistics.  The evaluated distances sit in
+// union slots (lane u & 31, slot u >> 5); a candidate's union position u comes
+// from the subset's union bitmap bm and its per-word prefix pre.  Lane e takes
+// the point's candidates e and e + 32, so the rank loop runs over cnt (~k + 10)
+// sources instead of the union (~3k).
+// xs (nullable): the points' rows in shared memory (dpad apart), else read from X.
+__device__ __forceinline__ void t3_rank_write(const T3ExactArgs& a, int lane, unsigned sm, int64_t ip, int cp,
+                                              const uint32_t* bm, const int* pre, const float (&acc)[3][kT3GP],
+                                              const float* xs, int dpad, double& qe_local) {
+    const int d = a.d, k = a.k;
+#pragma unroll
+    for (int p = 0; p < kT3GP; ++p) {
+        if (!((sm >> p) & 1u)) continue;
+        const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+        const int c = __shfl_sync(0xffffffffu, cp, p);
+        const unsigned short* cr = a.cand + (size_t)i * kT3CMax;
+        float cv[2];
+        int ck[2], rk[2] = {0, 0};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = 32 * q + lane;
+            const bool has = e < c;
+            const int j = has ? (int)cr[e] : 0;
+            const int u = has ? pre[j >> 5] + __popc(bm[j >> 5] & ((1u << (j & 31)) - 1u)) : 0;
+            const float a0 = __shfl_sync(0xffffffffu, acc[0][p], u & 31);
+            const float a1 = __shfl_sync(0xffffffffu, acc[1][p], u & 31);
+            const float a2 = __shfl_sync(0xffffffffu, acc[2][p], u & 31);
+            cv[q] = has ? (u < 32 ? a0 : (u < 64 ? a1 : a2)) : kInf;
+            ck[q] = has ? j : 0x7fffffff;
+        }
+        const int n0 = c < 32 ? c : 32;
+        for (int src = 0; src < n0; ++src) {
+            const float wv = __shfl_sync(0xffffffffu, cv[0], src);
+            const int wj = __shfl_sync(0xffffffffu, ck[0], src);
+            rk[0] += t3_less(wv, wj, cv[0], ck[0]) ? 1 : 0;
+            rk[1] += t3_less(wv, wj, cv[1], ck[1]) ? 1 : 0;
+        }
+        for (int src = 0; src < c - 32; ++src) {
+            const float wv = __shfl_sync(0xffffffffu, cv[1], src);
+            const int wj = __shfl_sync(0xffffffffu, ck[1], src);
+            rk[0] += t3_less(wv, wj, cv[0], ck[0]) ? 1 : 0;
+            rk[1] += t3_less(wv, wj, cv[1], ck[1]) ? 1 : 0;
+        }
+        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+        if (oi) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (32 * q + lane < c && rk[q] < k) {
+                    oi[rk[q]] = ck[q];
+                    od[rk[q]] = cv[q];
+                }
+        }
+        const unsigned m0 = __ballot_sync(0xffffffffu, lane < c && rk[0] == 0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, 32 + lane < c && rk[1] == 0);
+        const int src0 = m0 ? __ffs(m0) - 1 : __ffs(m1) - 1;
+        const float d0 = __shfl_sync(0xffffffffu, m0 ? cv[0] : cv[1], src0);
+        const int b0 = __shfl_sync(0xffffffffu, m0 ? ck[0] : ck[1], src0);
+        if (lane == 0) {
+            if (a.bmu) a.bmu[i] = b0;
+            if (a.qe_sum) qe_local += (double)d0;
+            if (a.accC) atomicAdd(a.accC + b0, 1ull);
+        }
+        if (a.accS) {
+            const float* xr = a.X + i * d;
+            for (int cc = lane; cc < d; cc += 32)
+                atomicAdd(a.accS + (int64_t)b0 * d + cc, acc_fx(xs ? xs[p * dpad + cc] : __ldg(xr + cc), a.acc_scale));
+        }
+    }
+}
+
+// Points of the group the screen could not bound (log overflow / too few
+// candidates): the reference insertion scan.
+__device__ __forceinline__ void t3_slow_points(const T3ExactArgs& a, int lane, int64_t gpos, int64_t p1, unsigned nmask,
+                                               int64_t ip, double& qe_local) {
+    const int d = a.d, k = a.k;
+    for (int p = 0; p < kT3GP; ++p) {
+        if (gpos + p >= p1) break;
+        if ((nmask >> p) & 1u) continue;
+        const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+        int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
+        float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
+        const float* xr = a.X + i * d;
+        int b0 = 0;
+        if (lane == 0) {
+            const SlowNearest sn = knn_point_slow(xr, d, a.L, a.g, k, oi, od);
+            b0 = sn.b0;
+            if (a.bmu) a.bmu[i] = b0;
+            if (a.qe_sum) qe_local += (double)sn.d0;
+            if (a.accC) atomicAdd(a.accC + b0, 1ull);
+        }
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (a.accS)
+            for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(__ldg(xr + c), a.acc_scale));
+    }
+}
+
+// One warp group from L2: stage the normal points' rows in xs, then per subset
+// (all points, else halves, else single points) union -> evaluate -> rank.
+template <bool V8>
+__device__ __forceinline__ void t3_group_l2(const T3ExactArgs& a, int lane, float* xs, uint32_t* bm, int* pre,
+                                            int* ul, int64_t ip, int cp, unsigned nmask, double& qe_local) {
+    const int d = a.d, dpad = a.dpad;
+    const int gw = (a.g + 31) >> 5;
+    const f2 nz = f2_pack(-0.0f, -0.0f);
+    for (int p = 0; p < kT3GP; ++p) {
+        if (!((nmask >> p) & 1u)) continue;
+        const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+        const float* xr = a.X + i * d;
+        for (int c = lane * 4; c < d; c += 128)
+            *reinterpret_cast<float4*>(xs + p * dpad + c) = __ldg(reinterpret_cast<const float4*>(xr + c));
+    }
+    // (a single point's list has <= kT3CMax <= kT3UMax landmarks, so the split always terminates)
+    unsigned todo[8];
+    int ntodo = 0;
+    if (nmask) todo[ntodo++] = nmask;
+    while (ntodo > 0) {
+        const unsigned sm = todo[--ntodo];
+        __syncwarp();
+        for (int w = lane; w < gw; w += 32) bm[w] = 0u;
+        __syncwarp();
+        for (int p = 0; p < kT3GP; ++p) {
+            if (!((sm >> p) & 1u)) continue;
+            const int64_t i = __shfl_sync(0xffffffffu, ip, p);
+            const int c = __shfl_sync(0xffffffffu, cp, p);
+            const unsigned short* cr = a.cand + (size_t)i * kT3CMax;
+            for (int e = lane; e < c; e += 32) {
+                const int j = cr[e];
+                atomicOr(bm + (j >> 5), 1u << (j & 31));
+            }
+        }
+        __syncwarp();
+        const int U = t3_bits_to_list(bm, gw, ul, kT3UMax, pre, lane);
+        if (a.stats && lane == 0) {
+            atomicAdd(a.stats + 2, U);
+            atomicAdd(a.stats + (U > kT3UMax ? 4 : 3), 1);
+        }
+        if (U > kT3UMax) {  // split the subset in two halves
+            unsigned lo = 0u, rest = sm;
+            const int half = __popc(sm) / 2;
+            for (int q = 0; q < half; ++q) {
+                const unsigned bit = rest & (0u - rest);
+                lo |= bit;
+                rest ^= bit;
+            }
+            todo[ntodo++] = rest;
+            todo[ntodo++] = lo;
+            continue;
+        }
+        __syncwarp();
+        int jj[3];
+        bool hv[3];
+        const float* lr[3];
+#pragma unroll
+        for (int sl = 0; sl < 3; ++sl) {
+            hv[sl] = 32 * sl + lane < U;
+            jj[sl] = hv[sl] ? ul[32 * sl + lane] : 0;
+            lr[sl] = a.L + (size_t)jj[sl] * d;
+        }
+        float acc[3][kT3GP];
+#pragma unroll
+        for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+            for (int p = 0; p < kT3GP; ++p) acc[sl][p] = 0.0f;
+        const bool two = U > 32, three = U > 64;  // warp-uniform slot counts
+        // landmark rows stream from L2: the next 8-dim chunk is loaded while the
+        // current one is accumulated (one-chunk register prefetch)
+        float4 la[3], lb[3];
+#pragma unroll
+        for (int sl = 0; sl < 3; ++sl) {
+            la[sl] = lb[sl] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (sl == 0 || (sl == 1 && two) || (sl == 2 && three)) {
+                if (V8) {
+                    ldg_nc_v8(lr[sl], la[sl], lb[sl]);
+                } else {
+                    la[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl]));
+                    lb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + 4));
+                }
+            }
+        }
+        for (int c = 0; c < d; c += 8) {
+            float4 na[3], nb[3];
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl) {
+                na[sl] = la[sl];
+                nb[sl] = lb[sl];
+                if (c + 8 < d && (sl == 0 || (sl == 1 && two) || (sl == 2 && three))) {
+                    if (V8) {
+                        ldg_nc_v8(lr[sl] + c + 8, na[sl], nb[sl]);
+                    } else {
+                        na[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 8));
+                        nb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 12));
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < kT3GP; ++p) {
+                if (!((sm >> p) & 1u)) continue;
+                const float4 xa = *reinterpret_cast<const float4*>(xs + p * dpad + c);
+                const float4 xb = *reinterpret_cast<const float4*>(xs + p * dpad + c + 4);
+                acc[0][p] = acc8f(acc[0][p], la[0], lb[0], xa, xb, nz);
+                if (two) acc[1][p] = acc8f(acc[1][p], la[1], lb[1], xa, xb, nz);
+                if (three) acc[2][p] = acc8f(acc[2][p], la[2], lb[2], xa, xb, nz);
+            }
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl) {
+                la[sl] = na[sl];
+                lb[sl] = nb[sl];
+            }
+        }
+        __syncwarp();
+        t3_rank_write(a, lane, sm, ip, cp, bm, pre, acc, xs, dpad, qe_local);
+    }
+}
+
+template <int KP, bool V8>
 __global__ void __launch_bounds__(kT3GWarps * 32, 2) knn_exact_group_kernel(T3ExactArgs a) {
     extern __shared__ __align__(16) float sm_all[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int d = a.d, k = a.k, dpad = a.dpad;
+    const int k = a.k, dpad = a.dpad;
     const int gw = (a.g + 31) >> 5;  // bitmap words
     float* xs = sm_all + (size_t)wib * t3_group_stride(dpad, a.g);
     uint32_t* bm = reinterpret_cast<uint32_t*>(xs + kT3GP * dpad);
-    int* ul = reinterpret_cast<int*>(bm + gw);
-    const f2 nz = f2_pack(-0.0f, -0.0f);
+    int* pre = reinterpret_cast<int*>(bm + gw);
+    int* ul = pre + gw;
     double qe_local = 0.0;
     const int64_t per = ((a.n + gridDim.x - 1) / gridDim.x + kT3GP - 1) / kT3GP * kT3GP;
     const int64_t p0 = (int64_t)blockIdx.x * per, p1 = p0 + per < a.n ? p0 + per : a.n;
     for (int64_t gpos = p0 + (int64_t)wib * kT3GP; gpos < p1; gpos += (int64_t)kT3GWarps * kT3GP) {
-        // ---- the group's points ----
         int64_t ip = 0;
         int cp = -1;
         if (lane < kT3GP && gpos + lane < p1) {
             ip = a.perm ? (int64_t)__ldg(a.perm + gpos + lane) : gpos + lane;
             cp = __ldg(a.ccount + ip);
         }
-        const bool normal_l = lane < kT3GP && cp >= k && cp <= kT3CMax;
-        const unsigned nmask = __ballot_sync(0xffffffffu, normal_l);
-        // stage the normal points' rows once
-        for (int p = 0; p < kT3GP; ++p) {
-            if (!((nmask >> p) & 1u)) continue;
-            const int64_t i = __shfl_sync(0xffffffffu, ip, p);
-            const float* xr = a.X + i * d;
-            for (int c = lane * 4; c < d; c += 128)
-                *reinterpret_cast<float4*>(xs + p * dpad + c) = __ldg(reinterpret_cast<const float4*>(xr + c));
-        }
-        // subsets of the group: all 8, else halves, else single points (a single point's list
-        // has <= kT3CMax <= kT3UMax landmarks, so the split always terminates)
-        unsigned todo[8];
-        int ntodo = 0;
-        if (nmask) todo[ntodo++] = nmask;
-        while (ntodo > 0) {
-            const unsigned sm = todo[--ntodo];
-            // ---- union of the subset's candidates ----
-            __syncwarp();
-            for (int w = lane; w < gw; w += 32) bm[w] = 0u;
-            __syncwarp();
-            for (int p = 0; p < kT3GP; ++p) {
-                if (!((sm >> p) & 1u)) continue;
-                const int64_t i = __shfl_sync(0xffffffffu, ip, p);
-                const int c = __shfl_sync(0xffffffffu, cp, p);
-                const unsigned short* cr = a.cand + (size_t)i * kT3CMax;
-                for (int e = lane; e < c; e += 32) {
-                    const int j = cr[e];
-                    atomicOr(bm + (j >> 5), 1u << (j & 31));
-                }
-            }
-            __syncwarp();
-            int U = 0;
-            for (int w0 = 0; w0 < gw; w0 += 32) {
-                const uint32_t m = w0 + lane < gw ? bm[w0 + lane] : 0u;
-                const int c = __popc(m);
-                int incl = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                int pos = U + incl - c;
-                uint32_t mm = m;
-                while (mm) {
-                    const int b = __ffs(mm) - 1;
-                    mm &= mm - 1u;
-                    if (pos < kT3UMax) ul[pos] = ((w0 + lane) << 5) + b;
-                    ++pos;
-                }
-                U += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (a.stats && lane == 0) {
-                atomicAdd(a.stats + 2, U);
-                atomicAdd(a.stats + (U > kT3UMax ? 4 : 3), 1);
-            }
-            if (U > kT3UMax) {  // split the subset in two halves
-                unsigned lo = 0u, rest = sm;
-                const int half = __popc(sm) / 2;
-                for (int q = 0; q < half; ++q) {
-                    const unsigned bit = rest & (0u - rest);
-                    lo |= bit;
-                    rest ^= bit;
-                }
-                todo[ntodo++] = rest;
-                todo[ntodo++] = lo;
-                continue;
-            }
-            __syncwarp();
-            int jj[3];
-            bool hv[3];
-            const float* lr[3];
-#pragma unroll
-            for (int sl = 0; sl < 3; ++sl) {
-                hv[sl] = 32 * sl + lane < U;
-                jj[sl] = hv[sl] ? ul[32 * sl + lane] : 0;
-                lr[sl] = a.L + (size_t)jj[sl] * d;
-            }
-            float acc[3][kT3GP];
-#pragma unroll
-            for (int sl = 0; sl < 3; ++sl)
-#pragma unroll
-                for (int p = 0; p < kT3GP; ++p) acc[sl][p] = 0.0f;
-            const bool two = U > 32, three = U > 64;  // warp-uniform slot counts
-            // landmark rows stream from L2: the next 8-dim chunk is loaded while the
-            // current one is accumulated (one-chunk register prefetch)
-            float4 la[3], lb[3];
-#pragma unroll
-            for (int sl = 0; sl < 3; ++sl) {
-                la[sl] = lb[sl] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (sl == 0 || (sl == 1 && two) || (sl == 2 && three)) {
-                    la[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl]));
-                    lb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + 4));
-                }
-            }
-            for (int c = 0; c < d; c += 8) {
-                float4 na[3], nb[3];
-#pragma unroll
-                for (int sl = 0; sl < 3; ++sl) {
-                    na[sl] = la[sl];
-                    nb[sl] = lb[sl];
-                    if (c + 8 < d && (sl == 0 || (sl == 1 && two) || (sl == 2 && three))) {
-                        na[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 8));
-                        nb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 12));
-                    }
-                }
-#pragma unroll
-                for (int p = 0; p < kT3GP; ++p) {
-                    if (!((sm >> p) & 1u)) continue;
-                    const float4 xa = *reinterpret_cast<const float4*>(xs + p * dpad + c);
-                    const float4 xb = *reinterpret_cast<const float4*>(xs + p * dpad + c + 4);
-                    acc[0][p] = acc8f(acc[0][p], la[0], lb[0], xa, xb, nz);
-                    if (two) acc[1][p] = acc8f(acc[1][p], la[1], lb[1], xa, xb, nz);
-                    if (three) acc[2][p] = acc8f(acc[2][p], la[2], lb[2], xa, xb, nz);
-                }
-#pragma unroll
-                for (int sl = 0; sl < 3; ++sl) {
-                    la[sl] = na[sl];
-                    lb[sl] = nb[sl];
-                }
-            }
-            // ---- per point: rank (distance, index) over U, write the k-NN row ----
-#pragma unroll
-            for (int p = 0; p < kT3GP; ++p) {
-                if (!((sm >> p) & 1u)) continue;
-                const int64_t i = __shfl_sync(0xffffffffu, ip, p);
-                float v[3];
-                int key[3], rk[3] = {0, 0, 0};
-#pragma unroll
-                for (int sl = 0; sl < 3; ++sl) {
-                    v[sl] = hv[sl] ? acc[sl][p] : kInf;
-                    key[sl] = hv[sl] ? jj[sl] : 0x7fffffff;
-                }
-#pragma unroll
-                for (int ss = 0; ss < 3; ++ss) {
-                    if (32 * ss >= U) break;
-                    const int nsrc = U - 32 * ss < 32 ? U - 32 * ss : 32;
-                    for (int src = 0; src < nsrc; ++src) {
-                        const float wv = __shfl_sync(0xffffffffu, v[ss], src);
-                        const int wj = __shfl_sync(0xffffffffu, key[ss], src);
-#pragma unroll
-                        for (int sl = 0; sl < 3; ++sl) rk[sl] += t3_less(wv, wj, v[sl], key[sl]) ? 1 : 0;
-                    }
-                }
-                int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
-                float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
-                int src0 = 0, sl0 = 0;
-                bool found = false;
-#pragma unroll
-                for (int sl = 0; sl < 3; ++sl) {
-                    if (hv[sl] && rk[sl] < k && oi) {
-                        oi[rk[sl]] = key[sl];
-                        od[rk[sl]] = v[sl];
-                    }
-                    const unsigned m0 = __ballot_sync(0xffffffffu, hv[sl] && rk[sl] == 0);
-                    if (m0 && !found) {
-                        found = true;
-                        src0 = __ffs(m0) - 1;
-                        sl0 = sl;
-                    }
-                }
-                const float dv = sl0 == 0 ? v[0] : (sl0 == 1 ? v[1] : v[2]);
-                const int dj = sl0 == 0 ? key[0] : (sl0 == 1 ? key[1] : key[2]);
-                const float d0 = __shfl_sync(0xffffffffu, dv, src0);
-                const int b0 = __shfl_sync(0xffffffffu, dj, src0);
-                if (lane == 0) {
-                    if (a.bmu) a.bmu[i] = b0;
-                    if (a.qe_sum) qe_local += (double)d0;
-                    if (a.accC) atomicAdd(a.accC + b0, 1ull);
-                }
-                if (a.accS)
-                    for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(xs[p * dpad + c], a.acc_scale));
-            }
-        }
-        // ---- points the screen could not bound (log overflow / too few candidates): reference scan ----
-        for (int p = 0; p < kT3GP; ++p) {
-            if (gpos + p >= p1) break;
-            if ((nmask >> p) & 1u) continue;
-            const int64_t i = __shfl_sync(0xffffffffu, ip, p);
-            int32_t* oi = a.out_idx ? a.out_idx + i * k : nullptr;
-            float* od = a.out_sqd ? a.out_sqd + i * k : nullptr;
-            const float* xr = a.X + i * d;
-            int b0 = 0;
-            if (lane == 0) {
-                const SlowNearest sn = knn_point_slow(xr, d, a.L, a.g, k, oi, od);
-                b0 = sn.b0;
-                if (a.bmu) a.bmu[i] = b0;
-                if (a.qe_sum) qe_local += (double)sn.d0;
-                if (a.accC) atomicAdd(a.accC + b0, 1ull);
-            }
-            b0 = __shfl_sync(0xffffffffu, b0, 0);
-            if (a.accS)
-                for (int c = lane; c < d; c += 32) atomicAdd(a.accS + (int64_t)b0 * d + c, acc_fx(__ldg(xr + c), a.acc_scale));
-        }
+        const unsigned nmask = __ballot_sync(0xffffffffu, lane < kT3GP && cp >= k && cp <= kT3CMax);
+        t3_group_l2<V8>(a, lane, xs, bm, pre, ul, ip, cp, nmask, qe_local);
+        t3_slow_points(a, lane, gpos, p1, nmask, ip, qe_local);
         __syncwarp();
     }
     if (a.qe_sum && lane == 0 && qe_local != 0.0) atomicAdd(a.qe_sum, qe_local);
@@ -773,7 +841,8 @@ int launch_exact_warp_t(T3ExactArgs a, cudaStream_t st) {
         const size_t per_warp = (size_t)t3_group_stride(a.dpad, a.g) * 4;
         const size_t smem = (size_t)kT3GWarps * per_warp;
         if (smem <= (size_t)esom_host::max_smem_optin()) {
-            auto kern = knn_exact_group_kernel<KP>;
+            const bool v8 = (reinterpret_cast<uintptr_t>(a.L) & 31) == 0;  // 256-bit loads need 32-B rows
+            auto kern = v8 ? knn_exact_group_kernel<KP, true> : knn_exact_group_kernel<KP, false>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT3GWarps * 32, smem);

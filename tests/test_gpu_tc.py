@@ -147,3 +147,25 @@ def test_gemm_screen_equals_scan_and_oracle(case):
     rows = np.arange(0, p.shape[0], max(1, p.shape[0] // 500))
     wi, wd = oracle.knn(p[rows], l, k)
     assert np.array_equal(a.indices[rows], wi) and np.array_equal(a.sqdists[rows], wd), case
+
+
+def test_gemm_exact_phase_unaligned_landmarks():
+    """The grouped exact phase reads each lane's landmark-row sector with one
+    256-bit load when the landmark matrix is 32-byte aligned, else with two
+    128-bit loads: a landmark matrix at a 16-byte offset gives the same rows."""
+    import torch
+    gen = np.random.default_rng(11)
+    p = (gen.normal(size=(5000, 64)) * 3).astype(np.float32)
+    l = (gen.normal(size=(600, 64)) * 3).astype(np.float32)
+    X = torch.from_numpy(p).cuda()
+    buf = torch.zeros(l.size + 4, dtype=torch.float32, device="cuda")
+    buf[4:] = torch.from_numpy(l.ravel()).cuda()
+    H_off = buf[4:].view(l.shape)
+    assert H_off.data_ptr() % 32 == 16
+    H = torch.from_numpy(l).cuda()
+    a = esom.knn(X, H, 32)
+    b = esom.knn(X, H_off, 32)
+    assert torch.equal(a.indices, b.indices) and torch.equal(a.sqdists, b.sqdists)
+    rows = np.arange(0, p.shape[0], 37)
+    wi, wd = oracle.knn(p[rows], l, 32)
+    assert np.array_equal(b.indices.cpu().numpy()[rows], wi) and np.array_equal(b.sqdists.cpu().numpy()[rows], wd)

@@ -54,7 +54,7 @@ for spec in ["default"] + sys.argv[1:]:
     torch.cuda.synchronize()
     kt = {}
     import ctypes
-    for name in ("knn_gemm_kernel", "knn_exact_group_kernel"):
+    for name in ("knn_gemm_kernel", "knn_exact_group_kernel", "knn_exact_stage_kernel"):
         c = ctypes.c_int32(0)
         ms = L.esom_timing_query(name.encode(), ctypes.byref(c))
         if c.value:
@@ -69,7 +69,7 @@ for spec in ["default"] + sys.argv[1:]:
         ref = (idx, sqd)
     same = torch.equal(idx, ref[0]) and torch.equal(sqd, ref[1])
     print(json.dumps({"variant": spec, "ms": statistics.median(ts[1:]), "kernels": kt,
-                      "cand_per_pt": int(cnt[0].item()) / n, "slow_pts": int(cnt[1].item()),
+                      "cand_per_pt": int(cnt[0].item()) / n, "slow_pts": int(cnt[1].item()), "stats": cnt.tolist(),
                       "bit_equal_default": same}), flush=True)
     for key in env:
         os.environ.pop(key)
