@@ -61,6 +61,23 @@ __device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
     return r;
 }
 
+// 32 bytes per lane in ONE 256-bit load (ld.global.nc.v8 -> LDG.E.ENL2.256):
+// when every lane of a warp reads its own row, each load costs one L1 wavefront
+// per lane, so halving the load count halves the L1 work.  p: 32-byte aligned.
+__device__ __forceinline__ void ldg8(const float* p, float4& a, float4& b) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
+__device__ __forceinline__ void ldg8(const int32_t* p, int4& a, int4& b) {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
+}
+__device__ __forceinline__ bool rows32(const void* base, int row_floats) {  // every row 32-byte aligned
+    return ((reinterpret_cast<uintptr_t>(base) | (uintptr_t)(row_floats * 4)) & 31) == 0;
+}
+
 __device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
 
 // mbarrier + 1-D TMA bulk copy (cp.async.bulk) helpers.

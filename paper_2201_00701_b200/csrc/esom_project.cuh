@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs 
     __syncthreads();
     const float* T = TSMEM ? tsm : a.T;
     const bool vec = (k == KP) && ((KP & 3) == 0);
+    const bool vec8 = vec && (KP & 7) == 0 && rows32(a.idx, k) && rows32(a.sqd, k);
     const float tmax_model = a.tmax ? __ldg(a.tmax) : 0.0f;
 
     for (int64_t pos = blockIdx.x * (int64_t)PT + tid; pos < a.n; pos += (int64_t)gridDim.x * PT) {
@@ -649,7 +650,19 @@ __global__ void __launch_bounds__(kReg2Threads, 1) project_reg2_kernel(ProjArgs 
         float sq[KP];
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
-        if (vec) {
+        if (vec8) {
+#pragma unroll
+            for (int q = 0; q + 8 <= KP; q += 8) {
+                int4 iv, iw;
+                float4 dv, dw;
+                ldg8(irow + q, iv, iw);
+                ldg8(drow + q, dv, dw);
+                jj[q] = iv.x; jj[q + 1] = iv.y; jj[q + 2] = iv.z; jj[q + 3] = iv.w;
+                jj[q + 4] = iw.x; jj[q + 5] = iw.y; jj[q + 6] = iw.z; jj[q + 7] = iw.w;
+                sq[q] = dv.x; sq[q + 1] = dv.y; sq[q + 2] = dv.z; sq[q + 3] = dv.w;
+                sq[q + 4] = dw.x; sq[q + 5] = dw.y; sq[q + 6] = dw.z; sq[q + 7] = dw.w;
+            }
+        } else if (vec) {
 #pragma unroll
             for (int q = 0; q < KP; q += 4) {
                 const int4 iv = __ldg(reinterpret_cast<const int4*>(irow + q));
@@ -818,6 +831,7 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
     const int tid = threadIdx.x;
     const int g = a.g, k = a.k;
     const bool vec = (k == KP) && ((KP & 3) == 0);
+    const bool vec8 = vec && (KP & 7) == 0 && rows32(a.idx, k) && rows32(a.sqd, k);
     const float4* __restrict__ rec = a.rec;
     const float tmax_model = a.tmax ? __ldg(a.tmax) : 0.0f;
 
@@ -827,7 +841,19 @@ __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a
         float sq[KP];
         const int32_t* irow = a.idx + i * k;
         const float* drow = a.sqd + i * k;
-        if (vec) {
+        if (vec8) {
+#pragma unroll
+            for (int q = 0; q + 8 <= KP; q += 8) {
+                int4 iv, iw;
+                float4 dv, dw;
+                ldg8(irow + q, iv, iw);
+                ldg8(drow + q, dv, dw);
+                jj[q] = iv.x; jj[q + 1] = iv.y; jj[q + 2] = iv.z; jj[q + 3] = iv.w;
+                jj[q + 4] = iw.x; jj[q + 5] = iw.y; jj[q + 6] = iw.z; jj[q + 7] = iw.w;
+                sq[q] = dv.x; sq[q + 1] = dv.y; sq[q + 2] = dv.z; sq[q + 3] = dv.w;
+                sq[q + 4] = dw.x; sq[q + 5] = dw.y; sq[q + 6] = dw.z; sq[q + 7] = dw.w;
+            }
+        } else if (vec) {
 #pragma unroll
             for (int q = 0; q < KP; q += 4) {
                 const int4 iv = __ldg(reinterpret_cast<const int4*>(irow + q));

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
 
     const int tid = threadIdx.x;
     const int w = tid >> 7;        // warpgroup
+    const bool x32 = rows32(a.X, a.d);
     const int wt = tid & 127;      // TMEM lane / row of the tile
     const int d = a.d, d16 = a.d16, gpad = a.gpad, k = a.k;
     const int off = KP - k;
@@ -293,8 +294,13 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
             for (int c0 = 0; c0 < d16; c0 += 8) {
                 float v[8];
                 if (valid && (d & 3) == 0 && c0 + 8 <= d) {
-                    const float4 u0 = __ldg(reinterpret_cast<const float4*>(xr + c0));
-                    const float4 u1 = __ldg(reinterpret_cast<const float4*>(xr + c0 + 4));
+                    float4 u0, u1;
+                    if (x32) {
+                        ldg8(xr + c0, u0, u1);
+                    } else {
+                        u0 = __ldg(reinterpret_cast<const float4*>(xr + c0));
+                        u1 = __ldg(reinterpret_cast<const float4*>(xr + c0 + 4));
+                    }
                     v[0] = u0.x; v[1] = u0.y; v[2] = u0.z; v[3] = u0.w;
                     v[4] = u1.x; v[5] = u1.y; v[6] = u1.z; v[7] = u1.w;
                 } else {
@@ -488,7 +494,15 @@ __global__ void __launch_bounds__(128 * W, 1) knn_tc2_kernel(Tc2Args a) {
         if (!xbad) {
             float x[32];
             const float* xr = a.X + i * d;
-            if ((d & 3) == 0) {
+            if (x32) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) {
+                    float4 u = make_float4(0.f, 0.f, 0.f, 0.f), u2 = u;
+                    if (c < d) ldg8(xr + c, u, u2);
+                    x[c] = u.x; x[c + 1] = u.y; x[c + 2] = u.z; x[c + 3] = u.w;
+                    x[c + 4] = u2.x; x[c + 5] = u2.y; x[c + 6] = u2.z; x[c + 7] = u2.w;
+                }
+            } else if ((d & 3) == 0) {
 #pragma unroll
                 for (int c = 0; c < 32; c += 4) {
                     float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -660,13 +674,22 @@ __device__ __forceinline__ ExactPoint exact_bits_point(const Tc2Args& a, int64_t
     const f2 nz2 = f2_pack(-0.0f, -0.0f);
     const int d4 = (d16 + 3) >> 2;
     const bool full = d4 == 8;
+    const bool x32 = rows32(a.X, d);
         int b0 = 0;
         float d0 = 0.0f;
         int written = 0;
         if (cnt >= 0) {
             float x[32];
             const float* xr = a.X + i * d;
-            if ((d & 3) == 0) {
+            if (x32) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) {
+                    float4 u = make_float4(0.f, 0.f, 0.f, 0.f), u2 = u;
+                    if (c < d) ldg8(xr + c, u, u2);
+                    x[c] = u.x; x[c + 1] = u.y; x[c + 2] = u.z; x[c + 3] = u.w;
+                    x[c + 4] = u2.x; x[c + 5] = u2.y; x[c + 6] = u2.z; x[c + 7] = u2.w;
+                }
+            } else if ((d & 3) == 0) {
 #pragma unroll
                 for (int c = 0; c < 32; c += 4) {
                     float4 u = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -551,14 +551,6 @@ __device__ __forceinline__ float acc8f(float s, const float4& la, const float4& 
     return __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, q4), q5), q6), q7);
 }
 
-// 32 bytes per lane in one load (LDG.E.ENL2.256: half the L1 wavefronts of two
-// 16-byte loads when every lane reads a different row); p 32-byte aligned.
-__device__ __forceinline__ void ldg_nc_v8(const float* p, float4& lo, float4& hi) {
-    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
-                 : "l"(p));
-}
-
 __host__ __device__ constexpr int t3_group_stride(int dpad, int g) {  // floats per warp, 16-B aligned
     return (kT3GP * dpad + 2 * ((g + 31) / 32) + kT3UMax + 3) / 4 * 4;  // x rows | bitmap | word prefix | list
 }
@@ -765,7 +757,7 @@ __device__ __forceinline__ void t3_group_l2(const T3ExactArgs& a, int lane, floa
             la[sl] = lb[sl] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (sl == 0 || (sl == 1 && two) || (sl == 2 && three)) {
                 if (V8) {
-                    ldg_nc_v8(lr[sl], la[sl], lb[sl]);
+                    ldg8(lr[sl], la[sl], lb[sl]);
                 } else {
                     la[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl]));
                     lb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + 4));
@@ -780,7 +772,7 @@ __device__ __forceinline__ void t3_group_l2(const T3ExactArgs& a, int lane, floa
                 nb[sl] = lb[sl];
                 if (c + 8 < d && (sl == 0 || (sl == 1 && two) || (sl == 2 && three))) {
                     if (V8) {
-                        ldg_nc_v8(lr[sl] + c + 8, na[sl], nb[sl]);
+                        ldg8(lr[sl] + c + 8, na[sl], nb[sl]);
                     } else {
                         na[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 8));
                         nb[sl] = __ldg(reinterpret_cast<const float4*>(lr[sl] + c + 12));
