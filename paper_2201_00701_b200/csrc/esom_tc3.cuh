@@ -13,17 +13,19 @@
 //     streams A/B chunks with 1-D TMA bulk copies through a 2-stage smem ring,
 //     one MMA warp issues 3 x kind::f16 MMAs per 16-wide K step per tile
 //     (x_hi l_hi + x_hi l_lo + x_lo l_hi) into TMEM (2 x 256 columns), and
-//     8 epilogue warps (thread = point = TMEM lane) read the accumulators:
-//       pass 1 (all landmark rounds): minima of 64 landmark groups j = q mod 64
-//         -> tau = k-th smallest group minimum >= k-th smallest D~;
-//       pass 2 (GEMM recomputed): log every landmark with D~_j <= tau + 2E
-//         (E: per-point error bound, t3_eps), refine to the k-th smallest
-//         logged D~ and write the candidate list (u16, <= kT3CMax per point)
-//         plus the approximate nearest landmark (for a locality sort).
-//  3. knn_exact_warp_kernel: one warp per point in approximate-BMU order (so a
-//     CTA's points share candidate rows in L1); lane e re-evaluates candidate
-//     e with the reference's sequential f32 sum (ref: knn.py:56-62), then the
-//     warp ranks (distance, index) across lanes and writes the k-NN row.
+//     8 epilogue warps (thread = point = TMEM lane) read the accumulators in
+//     ONE pass over the landmark rounds: every landmark with D~_j <= cut is
+//     logged in smem (<= 64 per thread); when a lane's log could overflow, the
+//     warp's lanes with more than k entries compact it (cut -> the k-th smallest
+//     logged D~ + 2E, E: per-point error bound, t3_eps; the cut only falls, and
+//     the k-th smallest logged D~ bounds the k-th smallest overall).  The final
+//     log (<= kT3CMax candidates, index order) and the approximate nearest
+//     landmark (for a locality sort) go to the exact kernel.
+//  3. knn_exact_group_kernel (d % 8 == 0; else knn_exact_warp_kernel, one warp
+//     per point): points in approximate-BMU order, a warp per 4 points; lanes
+//     re-evaluate the union of their candidates with the reference's sequential
+//     f32 sum (ref: knn.py:56-62), each point ranks its own candidates by
+//     (distance, index) and writes the k-NN row.
 // A point whose log overflows or whose candidate list exceeds kT3CMax is
 // flagged and re-done by the reference insertion scan (knn_point_slow).
 #pragma once
@@ -38,7 +40,6 @@ constexpr int kT3Epi = 256;          // epilogue threads: two 128-point tiles
 constexpr int kT3Threads = kT3Epi + 64;
 constexpr int kT3CMax = 64;          // candidates handed to the exact kernel per point
 constexpr int kT3LogCap = 64;        // per-thread candidate log in smem
-constexpr int kT3Groups = 64;        // landmark groups of the pass-1 bound
 constexpr uint32_t kT3AChunk = 128u * kT3Kc * 2u;   // one A tile chunk (hi or lo), bytes
 constexpr uint32_t kT3BChunk = 256u * kT3Kc * 2u;   // one B round chunk (hi or lo), bytes
 // MMA N = 128: a 256-landmark round is issued as two half-rounds into
@@ -77,7 +78,10 @@ __device__ __noinline__ T3Compacted<KP> t3_compact(float* logv, unsigned short* 
                                                    float lmax, float lnmax, int d, int dk, float tcut) {
     float vd[KP];
     vlist_init<KP>(vd, k);
-    for (int e = 0; e < cnt; ++e) vlist_insert<KP>(vd, logv[e * kT3Epi]);
+    for (int e = 0; e < cnt; ++e) {
+        const float v = logv[e * kT3Epi];
+        if (v < vd[KP - 1]) vlist_insert<KP>(vd, v);  // (no effect otherwise)
+    }
     const float tau = vd[KP - 1];
     const float E2 = 2.0f * t3_eps(xnorm, lmax, lnmax, d, dk, tau);
     const float nt = tau + E2 + 9.6e-7f * fabsf(tau);
@@ -94,16 +98,6 @@ __device__ __noinline__ T3Compacted<KP> t3_compact(float* logv, unsigned short* 
     }
     r.m = m;
     return r;
-}
-
-// k-th smallest of the 64 group minima (vlist for k < KP; two sorted halves for k == 32)
-template <int KP>
-__device__ __forceinline__ float kth_of_64(const float (&gm)[kT3Groups], int k) {
-    float vd[KP];
-    vlist_init<KP>(vd, k);
-#pragma unroll
-    for (int q = 0; q < kT3Groups; ++q) vlist_insert<KP>(vd, gm[q]);
-    return vd[KP - 1];
 }
 
 template <int KP>
@@ -147,23 +141,22 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
         if ((tid & 31) == 0) {
             uint32_t q = 0;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
-                for (int pass = 0; pass < 2; ++pass)
-                    for (int r = 0; r < R; ++r)
-                        for (int kc = 0; kc < nkc; ++kc, ++q) {
-                            const int s = (int)(q % kT3Stages);
-                            mbar_wait(&empty[s], ((q / kT3Stages) & 1u) ^ 1u);
-                            unsigned char* sb = stage + (size_t)s * kT3Stage;
-                            mbar_expect_tx(&full[s], kT3Stage);
-                            for (int t = 0; t < 2; ++t) {
-                                const size_t ao = ((size_t)(2 * st + t) * nkc + kc) * (kT3AChunk / 2);
-                                tma_bulk_g2s(sb + (2 * t) * kT3AChunk, a.Ahi + ao, kT3AChunk, &full[s]);
-                                tma_bulk_g2s(sb + (2 * t + 1) * kT3AChunk, a.Alo + ao, kT3AChunk, &full[s]);
-                            }
-                            const size_t bo = ((size_t)(r >> 1) * nkc + kc) * (kT3BChunk / 2) +
-                                              (size_t)(r & 1) * (kT3BHalf / 2);  // bf16 elements
-                            tma_bulk_g2s(sb + 4 * kT3AChunk, a.Bhi + bo, kT3BHalf, &full[s]);
-                            tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BHalf, a.Blo + bo, kT3BHalf, &full[s]);
+                for (int r = 0; r < R; ++r)
+                    for (int kc = 0; kc < nkc; ++kc, ++q) {
+                        const int s = (int)(q % kT3Stages);
+                        mbar_wait(&empty[s], ((q / kT3Stages) & 1u) ^ 1u);
+                        unsigned char* sb = stage + (size_t)s * kT3Stage;
+                        mbar_expect_tx(&full[s], kT3Stage);
+                        for (int t = 0; t < 2; ++t) {
+                            const size_t ao = ((size_t)(2 * st + t) * nkc + kc) * (kT3AChunk / 2);
+                            tma_bulk_g2s(sb + (2 * t) * kT3AChunk, a.Ahi + ao, kT3AChunk, &full[s]);
+                            tma_bulk_g2s(sb + (2 * t + 1) * kT3AChunk, a.Alo + ao, kT3AChunk, &full[s]);
                         }
+                        const size_t bo = ((size_t)(r >> 1) * nkc + kc) * (kT3BChunk / 2) +
+                                          (size_t)(r & 1) * (kT3BHalf / 2);  // bf16 elements
+                        tma_bulk_g2s(sb + 4 * kT3AChunk, a.Bhi + bo, kT3BHalf, &full[s]);
+                        tma_bulk_g2s(sb + 4 * kT3AChunk + kT3BHalf, a.Blo + bo, kT3BHalf, &full[s]);
+                    }
         }
     } else if (warp == kT3Epi / 32 + 1) {
         // ---------------- MMA issuer ----------------
@@ -172,35 +165,34 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             const uint32_t idesc = umma_idesc_bf16(128, kT3N);
             const uint32_t sboA = (kT3Kc / 8) * 128, sboB = (kT3Kc / 8) * 128, lbo = 128;
             for (int64_t st = blockIdx.x; st < nsup; st += gridDim.x)
-                for (int pass = 0; pass < 2; ++pass)
-                    for (int r = 0; r < R; ++r, ++rr) {
-                        const uint32_t buf = rr & 1u;
-                        mbar_wait(&tmem_empty[buf], ((rr >> 1) & 1u) ^ 1u);  // epilogue read this buffer's last use
+                for (int r = 0; r < R; ++r, ++rr) {
+                    const uint32_t buf = rr & 1u;
+                    mbar_wait(&tmem_empty[buf], ((rr >> 1) & 1u) ^ 1u);  // epilogue read this buffer's last use
+                    tc_fence_after();
+                    for (int kc = 0; kc < nkc; ++kc, ++q) {
+                        const int s = (int)(q % kT3Stages);
+                        mbar_wait(&full[s], (q / kT3Stages) & 1u);
                         tc_fence_after();
-                        for (int kc = 0; kc < nkc; ++kc, ++q) {
-                            const int s = (int)(q % kT3Stages);
-                            mbar_wait(&full[s], (q / kT3Stages) & 1u);
-                            tc_fence_after();
-                            const uint32_t sb = smem_u32(stage + (size_t)s * kT3Stage);
-                            const uint32_t bh = sb + 4 * kT3AChunk, bl = bh + kT3BHalf;
-                            for (int ks = 0; ks < kT3Kc / 16; ++ks) {
-                                const uint32_t ko = (uint32_t)ks * 256u;
-                                for (int t = 0; t < 2; ++t) {
-                                    const uint32_t ah = sb + (2 * t) * kT3AChunk, al = ah + kT3AChunk;
-                                    const uint32_t dcol = tmem + buf * 256u + (uint32_t)(kT3N * t);
-                                    const uint32_t acc0 = (kc | ks) ? 1u : 0u;
-                                    umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
-                                              acc0);
-                                    umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bl + ko, lbo, sboB), idesc,
-                                              1);
-                                    umma_bf16(dcol, umma_desc(al + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
-                                              1);
-                                }
+                        const uint32_t sb = smem_u32(stage + (size_t)s * kT3Stage);
+                        const uint32_t bh = sb + 4 * kT3AChunk, bl = bh + kT3BHalf;
+                        for (int ks = 0; ks < kT3Kc / 16; ++ks) {
+                            const uint32_t ko = (uint32_t)ks * 256u;
+                            for (int t = 0; t < 2; ++t) {
+                                const uint32_t ah = sb + (2 * t) * kT3AChunk, al = ah + kT3AChunk;
+                                const uint32_t dcol = tmem + buf * 256u + (uint32_t)(kT3N * t);
+                                const uint32_t acc0 = (kc | ks) ? 1u : 0u;
+                                umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
+                                          acc0);
+                                umma_bf16(dcol, umma_desc(ah + ko, lbo, sboA), umma_desc(bl + ko, lbo, sboB), idesc,
+                                          1);
+                                umma_bf16(dcol, umma_desc(al + ko, lbo, sboA), umma_desc(bh + ko, lbo, sboB), idesc,
+                                          1);
                             }
-                            umma_commit(&empty[s]);  // stage reusable once these MMAs retire
                         }
-                        umma_commit(&tmem_full[buf]);
+                        umma_commit(&empty[s]);  // stage reusable once these MMAs retire
                     }
+                    umma_commit(&tmem_full[buf]);
+                }
         }
     } else {
         // ---------------- epilogue: thread = point = TMEM lane ----------------
@@ -218,43 +210,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             const int64_t i = st * 256 + t * 128 + lane_row;
             const bool valid = i < a.n;
             const float xnorm = valid ? __ldg(a.xnorm + i) : 0.0f;
-            float gm[kT3Groups];
-#pragma unroll
-            for (int q = 0; q < kT3Groups; ++q) gm[q] = kInf;
-            // ---- pass 1: group minima over all rounds ----
-            for (int r = 0; r < R; ++r, ++rr) {
-                const uint32_t buf = rr & 1u, tcol = tcol0 + buf * 256u;
-                mbar_wait(&tmem_full[buf], (rr >> 1) & 1u);
-                tc_fence_after();
-                const float* lnr = a.ln + (size_t)r * kT3N;
-#pragma unroll 1
-                for (int c0 = 0; c0 < kT3N; c0 += 64) {
-                    uint32_t v0[32], v1[32];
-                    tmem_ld32_async(tcol + (uint32_t)c0, v0);
-                    tmem_ld32_async(tcol + (uint32_t)(c0 + 32), v1);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) {  // column c0 + q -> group q, c0 + 32 + q -> group 32 + q
-                        gm[q] = fminf(gm[q], __uint_as_float(v0[q]) + __ldg(lnr + c0 + q));
-                        gm[32 + q] = fminf(gm[32 + q], __uint_as_float(v1[q]) + __ldg(lnr + c0 + 32 + q));
-                    }
-                }
-                tc_fence_before();
-                mbar_arrive(&tmem_empty[buf]);
-            }
-            // k-th smallest T_j = d_ref_j - |x'|^2 <= tau + E, so every true top-k
-            // member has D~_j <= T_j + E <= tau + 2E.  (Measured and dropped: a
-            // one-pass mode with log compaction, 70 ms, and an x_hi.l_hi-only bound
-            // pass, 36 ms -- its looser cut overflows the log; this mode: 22 ms.)
-            float tcut;
-            {
-                const float tau = kth_of_64<KP>(gm, k);
-                const float e_full = t3_eps(xnorm, lmax, lnmax, a.d, a.dk, tau);
-                tcut = tau + 2.0f * e_full + 9.6e-7f * fabsf(tau);
-            }
-            // ---- pass 2: log candidates (index order) ----
             int cnt = 0;
             bool ovf = false;
+            // ---- one pass: log under a running cut (t3_compact: the k-th smallest
+            // logged D~ + 2E).  Whenever a lane's log could overflow with the next 32
+            // columns, every lane holding more than k entries compacts: one warp-wide
+            // event instead of one per lane (divergent per-lane compactions made an
+            // earlier one-pass mode slower than two passes). ----
+            float tcut = kInf;
             for (int r = 0; r < R; ++r, ++rr) {
                 const uint32_t buf = rr & 1u, tcol = tcol0 + buf * 256u;
                 mbar_wait(&tmem_full[buf], (rr >> 1) & 1u);
@@ -265,12 +228,28 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                     uint32_t v0[32];
                     tmem_ld32_async(tcol + (uint32_t)c0, v0);
                     tmem_wait_ld();
+                    float vv[32];
+                    int need = 0;
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        const float v = __uint_as_float(v0[q]) + __ldg(lnr + c0 + q);
+                        vv[q] = __uint_as_float(v0[q]) + __ldg(lnr + c0 + q);
+                        need += vv[q] <= tcut ? 1 : 0;
+                    }
+                    const bool ev = __any_sync(0xffffffffu, cnt + need > kT3LogCap);
+                    if (ev && cnt > k) {
+                        const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
+                        cnt = cr.m;
+                        tcut = cr.tcut;
+                    }
+                    if (a.stats && ev && (tid & 31) == 0) atomicAdd(a.stats + 5, 1);  // warp compaction events
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float v = vv[q];
                         if (v <= tcut) {
                             if (cnt == kT3LogCap) {
-                                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
+                                if (a.stats) atomicAdd(a.stats + 6, 1);  // per-lane (divergent) compactions
+                                const T3Compacted<KP> cr =
+                                    t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
                                 cnt = cr.m;
                                 tcut = cr.tcut;
                                 ovf |= cnt == kT3LogCap;
