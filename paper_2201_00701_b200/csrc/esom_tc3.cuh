@@ -39,7 +39,7 @@ constexpr int kT3Stages = 2;
 constexpr int kT3Epi = 256;          // epilogue threads: two 128-point tiles
 constexpr int kT3Threads = kT3Epi + 64;
 constexpr int kT3CMax = 64;          // candidates handed to the exact kernel per point
-constexpr int kT3LogCap = 64;        // per-thread candidate log in smem
+constexpr int kT3LogCap = 80;        // per-thread candidate log in smem
 constexpr uint32_t kT3AChunk = 128u * kT3Kc * 2u;   // one A tile chunk (hi or lo), bytes
 constexpr uint32_t kT3BChunk = 256u * kT3Kc * 2u;   // one B round chunk (hi or lo), bytes
 // MMA N = 128: a 256-landmark round is issued as two half-rounds into
