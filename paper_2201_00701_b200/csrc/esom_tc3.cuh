@@ -231,9 +231,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                     float vv[32];
                     int need = 0;
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        vv[q] = __uint_as_float(v0[q]) + __ldg(lnr + c0 + q);
-                        need += vv[q] <= tcut ? 1 : 0;
+                    for (int q = 0; q < 32; q += 8) {  // |l'|^2 of 8 columns per 256-bit load (uniform address)
+                        float4 l0, l1;
+                        ldg8(lnr + c0 + q, l0, l1);
+                        const float lq[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            vv[q + u] = __uint_as_float(v0[q + u]) + lq[u];
+                            need += vv[q + u] <= tcut ? 1 : 0;
+                        }
                     }
                     const bool ev = __any_sync(0xffffffffu, cnt + need > kT3LogCap);
                     if (ev && cnt > k) {
