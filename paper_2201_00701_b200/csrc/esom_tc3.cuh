@@ -39,7 +39,7 @@ constexpr int kT3Stages = 2;
 constexpr int kT3Epi = 256;          // epilogue threads: two 128-point tiles
 constexpr int kT3Threads = kT3Epi + 64;
 constexpr int kT3CMax = 64;          // candidates handed to the exact kernel per point
-constexpr int kT3LogCap = 80;        // per-thread candidate log in smem
+constexpr int kT3LogCap = 64;        // per-thread candidate log in smem
 constexpr uint32_t kT3AChunk = 128u * kT3Kc * 2u;   // one A tile chunk (hi or lo), bytes
 constexpr uint32_t kT3BChunk = 256u * kT3Kc * 2u;   // one B round chunk (hi or lo), bytes
 // MMA N = 128: a 256-landmark round is issued as two half-rounds into
@@ -71,20 +71,26 @@ struct T3Compacted {
     float tcut;
 };
 
-// log full: tighten the cut to the k-th smallest logged D~ (+2E) and keep the
-// survivors in index order (rare; out of line)
+// One-pass compaction: the k smallest logged D~ persist in shared memory
+// (vds, KP slots strided by kT3Epi) across compactions -- an entry a compaction
+// drops lies above the cut, so it is never among them -- and only the entries
+// logged since the last compaction, [ins, cnt), are inserted.  Then the cut
+// falls to the k-th smallest + 2E and the log keeps the entries at or below it.
 template <int KP>
-__device__ __noinline__ T3Compacted<KP> t3_compact(float* logv, unsigned short* logj, int cnt, int k, float xnorm,
-                                                   float lmax, float lnmax, int d, int dk, float tcut) {
+__device__ __noinline__ T3Compacted<KP> t3_compact_keep(float* logv, unsigned short* logj, float* vds, int cnt, int ins,
+                                                        float xnorm, float lmax, float lnmax, int d, int dk,
+                                                        float tcut) {
     float vd[KP];
-    vlist_init<KP>(vd, k);
-    for (int e = 0; e < cnt; ++e) {
+#pragma unroll
+    for (int q = 0; q < KP; ++q) vd[q] = vds[q * kT3Epi];
+    for (int e = ins; e < cnt; ++e) {
         const float v = logv[e * kT3Epi];
-        if (v < vd[KP - 1]) vlist_insert<KP>(vd, v);  // (no effect otherwise)
+        if (v < vd[KP - 1]) vlist_insert<KP>(vd, v);
     }
+#pragma unroll
+    for (int q = 0; q < KP; ++q) vds[q * kT3Epi] = vd[q];
     const float tau = vd[KP - 1];
-    const float E2 = 2.0f * t3_eps(xnorm, lmax, lnmax, d, dk, tau);
-    const float nt = tau + E2 + 9.6e-7f * fabsf(tau);
+    const float nt = tau + 2.0f * t3_eps(xnorm, lmax, lnmax, d, dk, tau) + 9.6e-7f * fabsf(tau);
     T3Compacted<KP> r;
     r.tcut = nt < tcut ? nt : tcut;
     int m = 0;
@@ -114,6 +120,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
     unsigned char* stage = smem_raw;
     float* logv = reinterpret_cast<float*>(smem_raw + kT3Stages * kT3Stage);
     unsigned short* logj = reinterpret_cast<unsigned short*>(logv + kT3LogCap * kT3Epi);
+    float* vdsm = reinterpret_cast<float*>(logj + kT3LogCap * kT3Epi);  // [KP][kT3Epi]: the k smallest logged
 
     if (tid == 0) {
         for (int s = 0; s < kT3Stages; ++s) {
@@ -203,6 +210,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
         const float lmax = __ldg(a.lstats), lnmax = __ldg(a.lstats + 1);
         float* lv = logv + tid;
         unsigned short* lj = logj + tid;
+        float* vs = vdsm + tid;
         const int k = a.k;
         uint32_t rr = 0;
         int stat_local = 0, ovf_local = 0;
@@ -212,12 +220,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             const float xnorm = valid ? __ldg(a.xnorm + i) : 0.0f;
             int cnt = 0;
             bool ovf = false;
-            // ---- one pass: log under a running cut (t3_compact: the k-th smallest
+            // ---- one pass: log under a running cut (t3_compact_keep: the k-th smallest
             // logged D~ + 2E).  Whenever a lane's log could overflow with the next 32
             // columns, every lane holding more than k entries compacts: one warp-wide
             // event instead of one per lane (divergent per-lane compactions made an
             // earlier one-pass mode slower than two passes). ----
             float tcut = kInf;
+            int ins = 0;  // log entries [ins, cnt) are not among the kept k smallest yet
+#pragma unroll
+            for (int q = 0; q < KP; ++q) vs[q * kT3Epi] = q >= KP - k ? kInf : -kInf;  // (vlist_init)
             for (int r = 0; r < R; ++r, ++rr) {
                 const uint32_t buf = rr & 1u, tcol = tcol0 + buf * 256u;
                 mbar_wait(&tmem_full[buf], (rr >> 1) & 1u);
@@ -243,8 +254,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                     }
                     const bool ev = __any_sync(0xffffffffu, cnt + need > kT3LogCap);
                     if (ev && cnt > k) {
-                        const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
-                        cnt = cr.m;
+                        const T3Compacted<KP> cr =
+                            t3_compact_keep<KP>(lv, lj, vs, cnt, ins, xnorm, lmax, lnmax, a.d, a.dk, tcut);
+                        cnt = ins = cr.m;
                         tcut = cr.tcut;
                     }
                     if (a.stats && ev && (tid & 31) == 0) atomicAdd(a.stats + 5, 1);  // warp compaction events
@@ -255,8 +267,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                             if (cnt == kT3LogCap) {
                                 if (a.stats) atomicAdd(a.stats + 6, 1);  // per-lane (divergent) compactions
                                 const T3Compacted<KP> cr =
-                                    t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
-                                cnt = cr.m;
+                                    t3_compact_keep<KP>(lv, lj, vs, cnt, ins, xnorm, lmax, lnmax, a.d, a.dk, tcut);
+                                cnt = ins = cr.m;
                                 tcut = cr.tcut;
                                 ovf |= cnt == kT3LogCap;
                             }
@@ -274,7 +286,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
             if (!valid) continue;
             // ---- refine and hand the candidates to the exact kernel ----
             if (!ovf && cnt > k) {
-                const T3Compacted<KP> cr = t3_compact<KP>(lv, lj, cnt, k, xnorm, lmax, lnmax, a.d, a.dk, tcut);
+                const T3Compacted<KP> cr =
+                    t3_compact_keep<KP>(lv, lj, vs, cnt, ins, xnorm, lmax, lnmax, a.d, a.dk, tcut);
                 cnt = cr.m;
             }
             int best = 0;
@@ -307,7 +320,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
 
 template <int KP>
 int launch_gemm_t(Tc3Args a, cudaStream_t st) {
-    const size_t smem = (size_t)kT3Stages * kT3Stage + (size_t)kT3LogCap * kT3Epi * 6 + 128;
+    const size_t smem = (size_t)kT3Stages * kT3Stage + (size_t)kT3LogCap * kT3Epi * 6 + (size_t)KP * kT3Epi * 4 + 128;
     if (smem > (size_t)esom_host::max_smem_optin())
         return esom_host::set_err(ESOM_ERR_UNSUPPORTED, "gemm screen: shared memory%s", "");
     auto kern = knn_gemm_kernel<KP>;
