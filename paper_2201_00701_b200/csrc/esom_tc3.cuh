@@ -260,22 +260,35 @@ __global__ void __launch_bounds__(kT3Threads, 1) knn_gemm_kernel(Tc3Args a) {
                         tcut = cr.tcut;
                     }
                     if (a.stats && ev && (tid & 31) == 0) atomicAdd(a.stats + 5, 1);  // warp compaction events
+                    const uint16_t j0 = (uint16_t)(r * kT3N + c0);
+                    if (__all_sync(0xffffffffu, cnt + need <= kT3LogCap)) {  // (the common case) no overflow: predicated appends
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        const float v = vv[q];
-                        if (v <= tcut) {
-                            if (cnt == kT3LogCap) {
-                                if (a.stats) atomicAdd(a.stats + 6, 1);  // per-lane (divergent) compactions
-                                const T3Compacted<KP> cr =
-                                    t3_compact_keep<KP>(lv, lj, vs, cnt, ins, xnorm, lmax, lnmax, a.d, a.dk, tcut);
-                                cnt = ins = cr.m;
-                                tcut = cr.tcut;
-                                ovf |= cnt == kT3LogCap;
+                        for (int q = 0; q < 32; ++q) {
+                            const bool lg = vv[q] <= tcut;
+                            if (lg) {
+                                lv[cnt * kT3Epi] = vv[q];
+                                lj[cnt * kT3Epi] = (uint16_t)(j0 + q);
                             }
-                            if (cnt < kT3LogCap && v <= tcut) {
-                                lv[cnt * kT3Epi] = v;
-                                lj[cnt * kT3Epi] = (unsigned short)(r * kT3N + c0 + q);
-                                ++cnt;
+                            cnt += lg ? 1 : 0;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const float v = vv[q];
+                            if (v <= tcut) {
+                                if (cnt == kT3LogCap) {
+                                    if (a.stats) atomicAdd(a.stats + 6, 1);  // per-lane (divergent) compactions
+                                    const T3Compacted<KP> cr =
+                                        t3_compact_keep<KP>(lv, lj, vs, cnt, ins, xnorm, lmax, lnmax, a.d, a.dk, tcut);
+                                    cnt = ins = cr.m;
+                                    tcut = cr.tcut;
+                                    ovf |= cnt == kT3LogCap;
+                                }
+                                if (cnt < kT3LogCap && v <= tcut) {
+                                    lv[cnt * kT3Epi] = v;
+                                    lj[cnt * kT3Epi] = (unsigned short)(r * kT3N + c0 + q);
+                                    ++cnt;
+                                }
                             }
                         }
                     }
