@@ -350,7 +350,6 @@ def _embed_host_pipelined(host, model, k: int, dev) -> np.ndarray:
 
 def _embed_host_pipeline_run(host, model, k: int, dev) -> np.ndarray:
     n, d = host.shape
-    pm = PreparedModel(model.hi, model.lo, k, device=dev)
     flag = _dev.new_flag(dev)
     out = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
     comp = torch.cuda.current_stream(dev)
@@ -367,7 +366,10 @@ def _embed_host_pipeline_run(host, model, k: int, dev) -> np.ndarray:
     loaded = [torch.cuda.Event() for _ in range(nb)]
     computed = [None] * nb  # compute of the chunk that last used buffer b (Xd[b] free, Yd[b] ready)
     drained = [None] * nb   # D2H of the chunk that last used buffer b (Yd[b] free)
-    for it, s in enumerate(range(0, n, c)):
+    starts = list(range(0, n, c))
+
+    def load(it):  # H2D of chunk it into buffer it % nb (after that buffer's previous compute)
+        s = starts[it]
         m = min(c, n - s)
         b = it % nb
         if computed[b] is not None:
@@ -384,6 +386,14 @@ def _embed_host_pipeline_run(host, model, k: int, dev) -> np.ndarray:
         loaded[b].record(h2d)
         if staged:
             stage_free[b] = loaded[b]
+
+    load(0)  # the first chunk's H2D runs while the model is prepared (host + device)
+    pm = PreparedModel(model.hi, model.lo, k, device=dev)
+    for it, s in enumerate(starts):
+        if it + 1 < len(starts):
+            load(it + 1)
+        m = min(c, n - s)
+        b = it % nb
         comp.wait_event(loaded[b])
         if drained[b] is not None:
             comp.wait_event(drained[b])
