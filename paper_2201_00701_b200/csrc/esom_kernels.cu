@@ -634,8 +634,14 @@ __global__ void scores_kernel(const float* __restrict__ sqd, int64_t n, int k, d
 __global__ void project_kernel(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ hi,
                                const float* __restrict__ lo, const int32_t* __restrict__ idx,
                                const double* __restrict__ sc, int k, float* __restrict__ xy) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        project_row_faithful(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
+    // d <= 32 with 32-byte rows: the register-resident variant (one kernel-uniform branch)
+    const bool r32 = d <= 32 && (d & 7) == 0 && rows32(hi, d);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (r32)
+            project_row_faithful32(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
+        else
+            project_row_faithful(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
+    }
 }
 
 // ---------------------------------------------------------------------------
