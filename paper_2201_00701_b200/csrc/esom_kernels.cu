@@ -635,10 +635,13 @@ __global__ void project_kernel(const float* __restrict__ X, int64_t n, int d, co
                                const float* __restrict__ lo, const int32_t* __restrict__ idx,
                                const double* __restrict__ sc, int k, float* __restrict__ xy) {
     // d <= 32 with 32-byte rows: the register-resident variant (one kernel-uniform branch)
-    const bool r32 = d <= 32 && (d & 7) == 0 && rows32(hi, d);
+    const bool v8 = (d & 7) == 0 && rows32(hi, d) && rows32(X, d);
+    const bool r32 = v8 && d <= 32;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (r32)
             project_row_faithful32(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
+        else if (v8)
+            project_row_faithful_v8(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
         else
             project_row_faithful(X + i * d, hi, lo, idx + i * k, sc + i * k, d, k, xy + 2 * i);
     }

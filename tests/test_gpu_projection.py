@@ -328,3 +328,25 @@ def test_fused_exact_projection_equals_two_kernel_path(rows, cols, n):
     want = oracle.embed(pts[::997], hi, lo, 16)
     ext = float(np.ptp(lo, axis=0).max())
     assert float(np.abs(a[::997].cpu().numpy() - want).max()) <= 1e-4 * ext
+
+
+@pytest.mark.parametrize("d", [4, 8, 24, 32, 48, 64, 512])
+def test_faithful_projection_paths_bit_exact(d):
+    """The faithful projection kernel (ref: projection.py:68-121) takes a
+    register-resident path for d <= 32 and 256-bit row loads for d % 8 == 0
+    (else the generic loop): with the scores given (no exp involved) every
+    path equals the C oracle's restatement bit for bit."""
+    from paper_2201_00701_b200.projection import _project_dev
+    gen = np.random.default_rng(100 + d)
+    g, k, n = 80, 12, 600
+    hi = (gen.normal(size=(g, d)) * 3).astype(np.float32)
+    lo = (gen.random((g, 2)) * 10).astype(np.float32)
+    pts = (gen.normal(size=(n, d)) * 3).astype(np.float32)
+    idx = np.stack([gen.choice(g, k, replace=False) for _ in range(n)]).astype(np.int32)
+    sc = np.sort(gen.random((n, k)), axis=1)[:, ::-1].copy()
+    sc[:, -1] = 0.0
+    sc[::7, 3] = 0.0  # zero-score neighbours are skipped like the reference's
+    want = oracle.project(pts, hi, lo, idx, sc)
+    got = _project_dev(torch.from_numpy(pts).cuda(), torch.from_numpy(hi).cuda(), torch.from_numpy(lo).cuda(),
+                       torch.from_numpy(idx).cuda(), torch.from_numpy(sc).cuda()).cpu().numpy()
+    assert np.array_equal(got, want), float(np.abs(got - want).max())
