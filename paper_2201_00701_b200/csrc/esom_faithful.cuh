@@ -232,16 +232,4 @@ static __device__ __noinline__ void project_row_faithful(const float* __restrict
 
 
 
-// Out-of-line entry for the fast kernels' rare fallback (faithful_point): the
-// 256-bit-load loop when the rows allow it, else the generic one.
-static __device__ __noinline__ void project_row_faithful_any(const float* __restrict__ x, const float* __restrict__ hi,
-                                                             const float* __restrict__ lo,
-                                                             const int32_t* __restrict__ nbr,
-                                                             const double* __restrict__ sc, int d, int k, float* out) {
-    if ((d & 7) == 0 && rows32(hi, d) && rows32(x, 8))
-        project_row_faithful_v8(x, hi, lo, nbr, sc, d, k, out);
-    else
-        project_row_faithful(x, hi, lo, nbr, sc, d, k, out);
-}
-
 }  // namespace esom

@@ -294,7 +294,7 @@ static __device__ __noinline__ void faithful_point(const ProjArgs& a, int64_t i)
     double sc[64];
     const float* row = a.sqd + i * a.k;
     score_row_dev(a.k, [&](int t) { return __ldg(row + t); }, sc);
-    project_row_faithful_any(a.X + i * a.d, a.hi, a.lo, a.idx + i * a.k, sc, a.d, a.k, a.xy + 2 * i);
+    project_row_faithful(a.X + i * a.d, a.hi, a.lo, a.idx + i * a.k, sc, a.d, a.k, a.xy + 2 * i);
 }
 
 template <int KP>
