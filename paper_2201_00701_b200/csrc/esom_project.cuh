@@ -829,7 +829,7 @@ template <int KP>
 __global__ void __launch_bounds__(kRegThreads, 1) project_reg3_kernel(ProjArgs a) {
     constexpr int PT = kRegThreads;
     const int tid = threadIdx.x;
-    const int g = a.g, k = a.k;
+    const int k = a.k;
     const bool vec = (k == KP) && ((KP & 3) == 0);
     const bool vec8 = vec && (KP & 7) == 0 && rows32(a.idx, k) && rows32(a.sqd, k);
     const float4* __restrict__ rec = a.rec;
