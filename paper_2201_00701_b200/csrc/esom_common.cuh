@@ -60,6 +60,16 @@ __device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
+__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {  // a*b + c, one rounding per lane
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
 
 // 32 bytes per lane in ONE 256-bit load (ld.global.nc.v8 -> LDG.E.ENL2.256):
 // when every lane of a warp reads its own row, each load costs one L1 wavefront

@@ -29,7 +29,7 @@ __host__ __device__ inline size_t fused_proj_offset(int gpad, int ls) {
 inline size_t fused_smem_bytes(int gpad, int ls, int g) { return fused_proj_offset(gpad, ls) + reg2_hi64_offset(g); }
 inline size_t fused_list_bytes() { return (size_t)kExactListCap * kFusedThreads * 2; }
 
-template <int KP, bool LIST>
+template <int KP, bool LIST, bool FH>
 __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a, ProjArgs q) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar_load;
@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) embed_fused_kernel(Tc2Args a
         if (q.store_bmu) wi[0] = b0;  // the nearest landmark: batch-SOM statistics read column 0
         if (a.bmu) a.bmu[i] = b0;
         if (a.qe_sum) qe_local += (double)d0;
-        reg2_point<KP, true, false, false, true, true>(q, i, rj, rd, LO, RB, tsm, nullptr, nullptr, 0, tmax_model, Ls,
-                                                       a.ls, inv);
+        reg2_point<KP, true, false, FH, true, true>(q, i, rj, rd, LO, RB, tsm, nullptr, nullptr, 0, tmax_model, Ls,
+                                                    a.ls, inv);
     }
     if (a.stats && slow_local) atomicAdd(a.stats + 1, slow_local);
     if (a.qe_sum) {
@@ -132,7 +132,9 @@ inline int launch_embed_fused(Tc2Args a, ProjArgs q, cudaStream_t st) {
     if (smem > cap) return ESOM_ERR_UNSUPPORTED;
     const bool list = smem + fused_list_bytes() <= cap;
     if (list) smem += fused_list_bytes();
-    auto kern = list ? embed_fused_kernel<16, true> : embed_fused_kernel<16, false>;
+    const bool fh = q.far_heavy != 0;  // far-heavy (trained) frames: the packed pair loop
+    auto kern = list ? (fh ? embed_fused_kernel<16, true, true> : embed_fused_kernel<16, true, false>)
+                     : (fh ? embed_fused_kernel<16, false, true> : embed_fused_kernel<16, false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t grid = (a.n + kFusedThreads - 1) / kFusedThreads;
     if (grid > esom_host::num_sms()) grid = esom_host::num_sms();
