@@ -185,7 +185,8 @@ class FrameLoop:
 
         self._eager_frame()
         torch.cuda.synchronize(self.dev)
-        self._census()
+        if self._census_frames > 0:  # (eager frames before the capture may have decided it already:
+            self._census()           # a second census here would read the zeroed counter)
         self._census_frames = 0
         n0 = L.load().esom_launch_count()
         g = torch.cuda.CUDAGraph()
