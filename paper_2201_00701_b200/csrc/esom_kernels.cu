@@ -514,15 +514,18 @@ int bmu_sort(const int32_t* idx, int64_t n, int k, int g, int32_t* cntb, int32_t
 // int64) and adds one partial per segment it touches to S / C (~n/64 atomics
 // per address row instead of one per point and dimension; integer sums, so
 // the order of the partials does not matter).
-constexpr int kSegPart = 64;
+constexpr int kSegPart = 256;
 
-__global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict__ X, int d,
+__global__ void __launch_bounds__(256, 4) bmu_segsum_kernel(const float* __restrict__ X, int d,
                                                          const int32_t* __restrict__ perm,
                                                          const int32_t* __restrict__ ends, int g, int64_t n,
-                                                         acc_t* __restrict__ S, acc_t* __restrict__ C, double scale) {
+                                                         acc_t* __restrict__ S, acc_t* __restrict__ C, double scale,
+                                                         const int32_t* __restrict__ idx, int k) {
     // warp w sums sorted positions [w*kSegPart, (w+1)*kSegPart) (times the 32-dim
     // slices): every launched warp has work; a range crossing a BMU boundary
-    // flushes one partial per segment it touches (binary search for the first)
+    // flushes one partial per segment it touches.  The first segment is the BMU
+    // of the range's first point (idx[perm[p0] * k]: two dependent loads instead of
+    // a 10-step binary search over ends, which dominated the short ranges)
     const int lane = threadIdx.x & 31;
     const int nsl = (d + 31) / 32;
     const int64_t nch = (n + kSegPart - 1) / kSegPart;
@@ -533,14 +536,8 @@ __global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict
         const int64_t p0 = (w / nsl) * kSegPart;
         const int64_t p1 = p0 + kSegPart < n ? p0 + kSegPart : n;
         const int c = sl * 32 + lane;
-        // segment of p0: first b with ends[b] > p0
-        int lo_b = 0, hi_b = g - 1;
-        while (lo_b < hi_b) {
-            const int mid = (lo_b + hi_b) >> 1;
-            if (__ldg(ends + mid) > p0) hi_b = mid;
-            else lo_b = mid + 1;
-        }
-        int b = lo_b;
+        // segment of p0 = the BMU of its point (the counting sort's key)
+        int b = __ldg(idx + (int64_t)__ldg(perm + p0) * k);
         int64_t pos = p0;
         while (pos < p1) {
             const int64_t e = min((int64_t)__ldg(ends + b), p1);
@@ -549,18 +546,21 @@ __global__ void __launch_bounds__(256) bmu_segsum_kernel(const float* __restrict
                 for (int64_t base = pos; base < e; base += 32) {  // 32 perm entries per coalesced load
                     const int pe = base + lane < e ? __ldg(perm + base + lane) : 0;
                     const int nb = e - base < 32 ? (int)(e - base) : 32;
-                    float v[32];  // 32 row loads in flight per lane
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        const int r = __shfl_sync(0xffffffffu, pe, q);
-                        v[q] = (q < nb && c < d) ? __ldg(X + (int64_t)r * d + c) : 0.0f;
-                    }
+                    for (int h = 0; h < 32; h += 16) {
+                        float v[16];  // 16 row loads in flight per lane (4 CTAs per SM without spills)
 #pragma unroll
-                    for (int q = 0; q < 32; q += 4) {
-                        acc += acc_fx(v[q], scale);
-                        acc1 += acc_fx(v[q + 1], scale);
-                        acc2 += acc_fx(v[q + 2], scale);
-                        acc3 += acc_fx(v[q + 3], scale);
+                        for (int q = 0; q < 16; ++q) {
+                            const int r = __shfl_sync(0xffffffffu, pe, h + q);
+                            v[q] = (h + q < nb && c < d) ? __ldg(X + (int64_t)r * d + c) : 0.0f;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 16; q += 4) {
+                            acc += acc_fx(v[q], scale);
+                            acc1 += acc_fx(v[q + 1], scale);
+                            acc2 += acc_fx(v[q + 2], scale);
+                            acc3 += acc_fx(v[q + 3], scale);
+                        }
                     }
                 }
             acc += (acc1 + acc2) + acc3;
@@ -1595,7 +1595,7 @@ int esom_embed_prepared_ex(const float* X, int64_t n, int32_t d, const float* hi
             if ((acc_S || acc_C) && !acc_smem) {
                 const int64_t warps = (m + kSegPart - 1) / kSegPart * ((d + 31) / 32);
                 bmu_segsum_kernel<<<grid_for(warps * 32, 256), 256, 0, stream>>>(X + s * d, d, perm, cntb, g, m,
-                                                                                  acc_S, acc_C, acc_scale);
+                                                                                  acc_S, acc_C, acc_scale, idx, k);
                 if (int e = cuda_check("bmu_segsum_kernel")) return e;
             }
             if (l2_table || use_rec || bmu_order) q.perm = perm;
