@@ -212,3 +212,35 @@ def test_batch_som_fixed_point_vs_oracle(golden):
     got = acc.cpu().numpy()
     gd = hi.size
     assert np.array_equal(got[:gd].reshape(hi.shape), S) and np.array_equal(got[gd:], C)
+
+
+def test_frame_loop_capture_keeps_the_census_decision():
+    """The far-point census of the eager warm-up frames decides the visiting
+    order (BMU order for far-heavy, i.e. trained, models); capturing the frame
+    graph afterwards must keep that decision (a second census on the zeroed
+    counter used to switch it off for every captured frame)."""
+    pts, hi, lo = c2_inputs()
+    X = torch.from_numpy(pts[:200_000]).cuda()
+    model = esom.LandmarkModel.create(hi, lo)
+    rng = Rng(3)
+
+    class _D:
+        points = X
+
+    for _ in range(40):  # the interactive steady state: a trained SOM, far-point heavy
+        model = esom.LandmarkModel.create(esom.som_tick(_D, model, esom.SomConfig(), rng).cpu().numpy(), lo)
+    eager = FrameLoop(X, model.hi, lo, 16, train=False)
+    for _ in range(3):
+        eager.frame()
+    assert eager.bmu_order  # (the census found the far-heavy regime)
+    cap = FrameLoop(X, model.hi, lo, 16, train=False)
+    for _ in range(3):
+        cap.frame()
+    cap.capture()
+    assert cap.bmu_order
+    cap.frame()
+    torch.cuda.synchronize()
+    assert torch.equal(cap.xy, eager.xy)
+    fresh = FrameLoop(X, model.hi, lo, 16, train=False)
+    fresh.capture()  # census from capture's own eager frame
+    assert fresh.bmu_order
