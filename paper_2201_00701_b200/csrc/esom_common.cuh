@@ -33,7 +33,10 @@ typedef unsigned long long f2;     // two packed f32 lanes (lo = first, hi = sec
 // (a power-of-two scale) followed by one deterministic rounding.
 typedef unsigned long long acc_t;
 __device__ __forceinline__ acc_t acc_fx(float x, double scale) {
-    return (acc_t)__double2ll_rn((double)x * scale);
+    // scale = 2^fx (0 <= fx <= 40) and |x| 2^fx < 2^61: x * 2^fx is exact in f32
+    // as in f64, so rounding the f32 product gives the same integer as rounding
+    // (double)x * scale -- one F2I instead of F2F + DMUL + F2I
+    return (acc_t)__float2ll_rn(x * (float)scale);
 }
 
 __device__ __forceinline__ f2 f2_pack(float a, float b) {

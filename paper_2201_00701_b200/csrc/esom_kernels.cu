@@ -596,18 +596,20 @@ __global__ void __launch_bounds__(kAccThreads) bmu_accum_smem_kernel(const float
     const int64_t nwarps = (int64_t)gridDim.x * (kAccThreads / 32);
     for (int64_t i0 = gw * 8; i0 < n; i0 += nwarps * 8) {
         float v[8];
-        int b[8];
+        // lane u < 8 loads point i0 + u's BMU once (not 8 broadcast loads per lane) and
+        // counts it: one count atomic instruction per 8 points
+        const int bl = (lane < 8 && i0 + lane < n) ? __ldg(idx + (i0 + lane) * k) : -1;
+        if (bl >= 0) atomicAdd(sC + bl, 1ull);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int64_t i = i0 + u;
-            b[u] = i < n ? __ldg(idx + i * k) : -1;
             v[u] = (i < n && lane < d) ? __ldg(X + i * d + lane) : 0.0f;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            if (b[u] < 0) continue;
-            if (lane < d) atomicAdd(sS + (size_t)b[u] * d + lane, acc_fx(v[u], scale));
-            if (lane == 0) atomicAdd(sC + b[u], 1ull);
+            const int b = __shfl_sync(0xffffffffu, bl, u);
+            if (b < 0) continue;
+            if (lane < d) atomicAdd(sS + (size_t)b * d + lane, acc_fx(v[u], scale));
         }
     }
     __syncthreads();
